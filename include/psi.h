@@ -1,0 +1,154 @@
+/*
+ * psi.h -- C-ABI of libpsi: the Power-psi hot path (arXiv 2206.09960) on one B200.
+ *
+ * The library computes the psi-score of every user of a follower graph,
+ *
+ *     psi^T = (1/N) [ (sum_t c^T A^t) B + d^T ]                 (Eq. (12))
+ *
+ * by the paper's Alg. 2 "Power-psi": s_0 = c, s_t^T = s_{t-1}^T A + c^T
+ * (Eq. (14)), stop when gap_t = ||B|| * ||s_t - s_{t-1}||_1 <= eps
+ * (Eqs. (15)-(16) and Alg. 2), then
+ * psi = (s^T B + d^T)/N (Alg. 2).  The model matrices are those of
+ * P:171-175:  A[j,i] = mu_i/W_j 1{i in L(j)},  B[j,i] = lambda_i/W_j 1{i in L(j)},
+ * W_j = sum_{l in L(j)} (lambda_l + mu_l),  c = mu/(lambda+mu),  d = lambda/(lambda+mu).
+ * Readings of the paper where it is silent or ambiguous (the norm ||B||, leaderless
+ * users, the iteration count, ...) are R1..R14 in DESIGN.md.
+ *
+ * Conventions
+ *  - Return codes: 0 = OK, > 0 = warning with a valid result, < 0 = error
+ *    (the message is in psi_last_error(), thread-local).
+ *  - All device work runs on the CUDA stream given to psi_build_graph
+ *    (a cudaStream_t passed as void*; NULL = the legacy default stream).
+ *  - A psi_ctx is not thread-safe; separate contexts are independent.
+ *  - Device memory is owned by the context and freed by psi_destroy.
+ *  - Limits: 1 <= n <= 2^31 - 1 and m <= 2^31 - 1 (int32 indices and offsets
+ *    on the device).
+ */
+#ifndef PSI_H
+#define PSI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct psi_ctx psi_ctx;
+typedef int psi_status;
+
+enum {
+  PSI_OK = 0,
+  PSI_NOT_CONVERGED = 1,   /* max_iters reached with gap > eps; psi is still valid */
+  PSI_E_INVALID_ARG = -1,  /* bad scalar argument or NULL pointer */
+  PSI_E_GRAPH = -2,        /* CSR violates the input contract (see psi_build_graph) */
+  PSI_E_ACTIVITY = -3,     /* lambda/mu NaN, Inf, negative, or lambda+mu <= 0 */
+  PSI_E_OOM = -4,          /* device or pinned host allocation failed */
+  PSI_E_CUDA = -5,         /* any other CUDA runtime error */
+  PSI_E_STATE = -6,        /* call out of order (e.g. get_psi before a successful iterate) */
+  PSI_E_NUMERIC = -7       /* epsilon_t became NaN or Inf during the iteration */
+};
+
+enum { PSI_MEM_HOST = 0, PSI_MEM_DEVICE = 1 };
+
+/* Which matrix norm ||B|| multiplies epsilon_t in Alg. 2 (the paper
+ * leaves it open).  ROW (default, reading R1) = max row sum of B, the norm
+ * induced by L1 on row vectors that makes bound (19) hold; COL = max column sum
+ * of B (SPEC's reading); ONE = 1 (Eq. (16) without the factor). */
+enum { PSI_NORM_ROW = 0, PSI_NORM_COL = 1, PSI_NORM_ONE = 2 };
+
+typedef struct psi_info {
+  int64_t n;              /* users */
+  int64_t m;              /* follow edges */
+  int64_t n_f;            /* users with >= 1 follower (rows whose s can change) */
+  int64_t n_g;            /* users with >= 1 leader (whose s is gathered) */
+  int64_t n_leaderless;   /* users with W_j = 0 (reading R5) */
+  double kappa_row;       /* max row sum of B    = max_j Lambda_j / W_j        */
+  double kappa_col;       /* max column sum of B = max_i lambda_i sum_{j in F(i)} 1/W_j */
+  double rho_A;           /* max row sum of A    = max_j (sum_{l in L(j)} mu_l) / W_j */
+  double ingest_ms;       /* device time of psi_build_graph's kernels (CUDA events) */
+  double iterate_ms;      /* device time of the last psi_iterate (init + sweeps + readout) */
+  int64_t last_iters;     /* T of the last psi_iterate */
+  double last_gap;        /* gap_T of the last psi_iterate */
+  int64_t num_tiles;      /* work tiles of one sweep (packed-row tiles + long-row chunks) */
+  int64_t num_long_rows;  /* rows split across several CTAs */
+  int64_t grid;           /* persistent CTAs per sweep launch */
+  int64_t device_bytes;   /* device memory held by the context */
+  int64_t relabeled;      /* 1 if users were relabeled for locality at ingest */
+} psi_info;
+
+/*
+ * psi_build_graph -- ingest (one-time).
+ *
+ * The graph is a CSR of FOLLOWERS PER LEADER ((i,j) in E means "i follows j"):
+ *   row_ptr   int64[n+1]: row_ptr[0] = 0, non-decreasing, row_ptr[n] = m;
+ *   followers int32[m]:   followers[row_ptr[j] .. row_ptr[j+1]) = F(j), the users
+ *                         who follow j, strictly increasing, each in [0, n), j not
+ *                         in F(j) (no self loops);
+ *   lambda, mu double[n]: posting / re-posting rates, finite, >= 0,
+ *                         lambda + mu > 0.
+ * mem_kind says whether the four arrays are host (PSI_MEM_HOST; pinned memory
+ * gives the fastest copy) or device (PSI_MEM_DEVICE) pointers.  They are BORROWED
+ * for the duration of the call only: everything is copied or transformed into
+ * context-owned device memory, so the caller may free them when it returns.
+ * On the device the call validates the contract, computes W, c, d, ||B|| (all
+ * three norms), rho_A, relabels users for locality, and builds the sweep's
+ * work tiles.  Blocks until done.
+ *
+ * Errors: PSI_E_INVALID_ARG (n < 1, m < 0, n or m > 2^31-1, NULL pointer, bad
+ * mem_kind); PSI_E_GRAPH (row_ptr[0] != 0, row_ptr[n] != m, decreasing row_ptr,
+ * index out of range, self loop, row not strictly increasing); PSI_E_ACTIVITY;
+ * PSI_E_OOM; PSI_E_CUDA.  *out is set only on PSI_OK.
+ */
+psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr,
+                           const int32_t* followers, const double* lambda,
+                           const double* mu, int mem_kind, void* stream, psi_ctx** out);
+
+/*
+ * psi_iterate -- Alg. 2 from s_0 = c, every call (no warm start).
+ *
+ * Runs sweeps s <- s A + c with the fused L1 residual and the stop rule
+ * gap_t = ||B||_norm * epsilon_t <= eps (gap_0 = 1, Alg. 2, so eps >= 1
+ * gives T = 0) entirely on the device (a CUDA-graph conditional loop: no host
+ * round trip per sweep), then the readout psi = (s^T B + d^T)/N.  Also stops
+ * at T = max_iters.  eps = 0 runs exactly max_iters sweeps unless the fp
+ * iteration reaches an exact fixed point first (gap_t == 0): the fixed-count
+ * parity mode.  Blocks until T is known; psi is ready on return.
+ *
+ * Outputs (either may be NULL): *iters_out = T (number of A products; the
+ * readout is one more B product), *last_gap_out = gap_T (1 if T = 0).
+ * Returns PSI_OK, PSI_NOT_CONVERGED (gap_T > eps at T = max_iters; psi valid),
+ * PSI_E_INVALID_ARG (NULL ctx, eps < 0 or NaN, max_iters < 0, bad norm),
+ * PSI_E_NUMERIC (epsilon_t NaN/Inf), PSI_E_CUDA.
+ */
+psi_status psi_iterate(psi_ctx* ctx, double eps, int64_t max_iters, int norm,
+                       int64_t* iters_out, double* last_gap_out);
+
+/* psi_get_psi -- copy psi[n] (fp64, the CALLER'S ORIGINAL user labels) to `out`,
+ * a host (PSI_MEM_HOST) or device (PSI_MEM_DEVICE) buffer of n doubles owned by
+ * the caller.  PSI_E_STATE if no psi_iterate has succeeded on this context. */
+psi_status psi_get_psi(const psi_ctx* ctx, double* out, int mem_kind);
+
+/* psi_get_series -- copy s_T[n] (the paper's series iterate after the last
+ * psi_iterate, Eq. (13)-(14), original labels) to a host or device buffer. */
+psi_status psi_get_series(const psi_ctx* ctx, double* out, int mem_kind);
+
+/* psi_get_residual_history -- raw epsilon_t = ||s_t - s_{t-1}||_1 for t = 1..T
+ * (Eq. (15), NOT multiplied by ||B||) into host buffer `out` of capacity `cap`;
+ * *len_out = T (the copy is truncated to min(T, cap, 2^24)).  PSI_E_STATE as above. */
+psi_status psi_get_residual_history(const psi_ctx* ctx, double* out, int64_t cap,
+                                    int64_t* len_out);
+
+/* psi_get_info -- sizes, norms and timings (see psi_info). */
+psi_status psi_get_info(const psi_ctx* ctx, psi_info* out);
+
+/* psi_destroy -- free all device and host memory of the context (NULL is a no-op). */
+void psi_destroy(psi_ctx* ctx);
+
+/* psi_last_error -- message of the last error on the calling thread ("" if none). */
+const char* psi_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSI_H */

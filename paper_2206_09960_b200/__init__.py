@@ -1,0 +1,216 @@
+"""Power-psi on one B200: thin Python binding over the C-ABI library libpsi.so.
+
+The binding only marshals arguments (pointers, sizes, the CUDA stream) to the C
+entry points declared in ``include/psi.h``; every step of the hot path runs in
+the library's sm_100a kernels.  PyTorch is used for device memory and streams.
+There is no CPU fallback: if libpsi.so cannot be built or loaded, every call
+raises.
+
+    import torch, paper_2206_09960_b200 as psi
+    g = psi.PsiGraph(row_ptr, followers, lam, mu)      # torch CUDA tensors or host arrays
+    status, T, gap = g.iterate(eps=1e-9)
+    scores = g.get_psi()                                # torch.float64 on the device
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+PSI_OK = 0
+PSI_NOT_CONVERGED = 1
+PSI_E_INVALID_ARG = -1
+PSI_E_GRAPH = -2
+PSI_E_ACTIVITY = -3
+PSI_E_OOM = -4
+PSI_E_CUDA = -5
+PSI_E_STATE = -6
+PSI_E_NUMERIC = -7
+PSI_MEM_HOST = 0
+PSI_MEM_DEVICE = 1
+NORMS = {"row": 0, "col": 1, "one": 2}
+
+_STATUS_NAMES = {0: "PSI_OK", 1: "PSI_NOT_CONVERGED", -1: "PSI_E_INVALID_ARG", -2: "PSI_E_GRAPH",
+                 -3: "PSI_E_ACTIVITY", -4: "PSI_E_OOM", -5: "PSI_E_CUDA", -6: "PSI_E_STATE",
+                 -7: "PSI_E_NUMERIC"}
+
+EXPORTED = ["psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
+            "psi_get_residual_history", "psi_get_info", "psi_destroy", "psi_last_error"]
+
+
+class PsiError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class psi_info(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("m", ctypes.c_int64), ("n_f", ctypes.c_int64),
+                ("n_g", ctypes.c_int64), ("n_leaderless", ctypes.c_int64),
+                ("kappa_row", ctypes.c_double), ("kappa_col", ctypes.c_double),
+                ("rho_A", ctypes.c_double), ("ingest_ms", ctypes.c_double),
+                ("iterate_ms", ctypes.c_double), ("last_iters", ctypes.c_int64),
+                ("last_gap", ctypes.c_double), ("num_tiles", ctypes.c_int64),
+                ("num_long_rows", ctypes.c_int64), ("grid", ctypes.c_int64),
+                ("device_bytes", ctypes.c_int64), ("relabeled", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def load_library(build_if_stale: bool = True):
+    """Load libpsi.so (building it in-tree with nvcc if missing/stale). Raises on failure."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if build_if_stale and _build._stale():
+        _build.build()
+    if not os.path.exists(path):
+        raise RuntimeError(f"libpsi.so not found at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
+    vp, i64, dbl, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+    lib.psi_build_graph.argtypes = [i64, i64, vp, vp, vp, vp, ci, vp, ctypes.POINTER(vp)]
+    lib.psi_iterate.argtypes = [vp, dbl, i64, ci, ctypes.POINTER(i64), ctypes.POINTER(dbl)]
+    lib.psi_get_psi.argtypes = [vp, vp, ci]
+    lib.psi_get_series.argtypes = [vp, vp, ci]
+    lib.psi_get_residual_history.argtypes = [vp, vp, i64, ctypes.POINTER(i64)]
+    lib.psi_get_info.argtypes = [vp, ctypes.POINTER(psi_info)]
+    lib.psi_destroy.argtypes = [vp]
+    lib.psi_destroy.restype = None
+    lib.psi_last_error.restype = ctypes.c_char_p
+    for f in ("psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
+              "psi_get_residual_history", "psi_get_info"):
+        getattr(lib, f).restype = ci
+    _lib = lib
+    return lib
+
+
+def _err(lib) -> str:
+    return (lib.psi_last_error() or b"").decode()
+
+
+def _ptr_kind(a):
+    """(pointer, mem_kind, keepalive) for a torch tensor or numpy array."""
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            if not a.is_contiguous():
+                a = a.contiguous()
+            return a.data_ptr(), (PSI_MEM_DEVICE if a.is_cuda else PSI_MEM_HOST), a
+    except ImportError:
+        pass
+    arr = np.ascontiguousarray(a)
+    return arr.ctypes.data, PSI_MEM_HOST, arr
+
+
+def _current_stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class PsiGraph:
+    """One ingested follower graph + activity (a psi_ctx).
+
+    row_ptr int64[N+1], followers int32[M] (CSR of followers per leader), lam/mu float64[N];
+    all four on the device (torch CUDA tensors) or all on the host (pinned torch tensors or
+    numpy arrays).  Work runs on torch's current CUDA stream at construction.
+    """
+
+    def __init__(self, row_ptr, followers, lam, mu, stream=None):
+        self._lib = load_library()
+        self._ctx = ctypes.c_void_p()
+        parts = [_ptr_kind(x) for x in (row_ptr, followers, lam, mu)]
+        kinds = {k for _, k, _ in parts}
+        if len(kinds) != 1:
+            raise ValueError("row_ptr, followers, lam, mu must all be host or all device")
+        self.n = int(len(lam))
+        self.m = int(len(followers))
+        self.stream = stream if stream is not None else _current_stream()
+        st = self._lib.psi_build_graph(self.n, self.m, parts[0][0], parts[1][0], parts[2][0],
+                                       parts[3][0], kinds.pop(), self.stream,
+                                       ctypes.byref(self._ctx))
+        if st != PSI_OK:
+            raise PsiError(st, _err(self._lib))
+
+    # -- Alg. 2
+    def iterate(self, eps: float = 1e-9, max_iters: int = 100_000, norm: str = "row"):
+        """Returns (status, T, gap_T); status is PSI_OK or PSI_NOT_CONVERGED."""
+        T = ctypes.c_int64()
+        gap = ctypes.c_double()
+        st = self._lib.psi_iterate(self._ctx, float(eps), int(max_iters), NORMS[norm],
+                                   ctypes.byref(T), ctypes.byref(gap))
+        if st < 0:
+            raise PsiError(st, _err(self._lib))
+        return st, T.value, gap.value
+
+    def _get(self, fn, out, device):
+        import torch
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.float64,
+                              device="cuda" if device else "cpu")
+        ptr, kind, keep = _ptr_kind(out)
+        st = fn(self._ctx, ptr, kind)
+        if st != PSI_OK:
+            raise PsiError(st, _err(self._lib))
+        return out
+
+    def get_psi(self, out=None, device: bool = True):
+        """psi[n] in the caller's original labels (torch.float64)."""
+        return self._get(self._lib.psi_get_psi, out, device)
+
+    def get_series(self, out=None, device: bool = True):
+        """s_T[n] (Eq. (13)-(14)) in original labels."""
+        return self._get(self._lib.psi_get_series, out, device)
+
+    def get_residual_history(self) -> np.ndarray:
+        n = ctypes.c_int64()
+        st = self._lib.psi_get_residual_history(self._ctx, None, 0, ctypes.byref(n))
+        if st != PSI_OK:
+            raise PsiError(st, _err(self._lib))
+        out = np.empty(max(n.value, 0), dtype=np.float64)
+        if n.value:
+            st = self._lib.psi_get_residual_history(self._ctx, out.ctypes.data, n.value,
+                                                    ctypes.byref(n))
+            if st != PSI_OK:
+                raise PsiError(st, _err(self._lib))
+        return out
+
+    def info(self) -> dict:
+        inf = psi_info()
+        st = self._lib.psi_get_info(self._ctx, ctypes.byref(inf))
+        if st != PSI_OK:
+            raise PsiError(st, _err(self._lib))
+        return {name: getattr(inf, name) for name, _ in psi_info._fields_}
+
+    def close(self):
+        if self._ctx:
+            self._lib.psi_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def psi_scores(row_ptr, followers, lam, mu, eps=1e-9, max_iters=100_000, norm="row"):
+    """One-shot convenience: ingest, Alg. 2 to eps, return (psi, T, status)."""
+    with PsiGraph(row_ptr, followers, lam, mu) as g:
+        st, T, _ = g.iterate(eps, max_iters, norm)
+        return g.get_psi(), T, st

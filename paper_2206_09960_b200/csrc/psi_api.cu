@@ -1,0 +1,418 @@
+// psi_api.cu -- the C-ABI of libpsi (include/psi.h): context, CUDA-graph loop, errors.
+//
+// psi_iterate launches ONE instantiated CUDA graph per call:
+//
+//    k_init  ->  WHILE(cond) { k_tiles<sweep> -> k_fix<sweep> }  ->  k_tiles<readout> -> k_fix<readout>
+//
+// k_init sets cond = (gap_0 = 1 > eps && max_iters > 0) (Alg. 2 lines 1-5); the last CTA of
+// every k_fix<sweep> sets cond = (gap_t > eps && t < max_iters) (lines 5, 8), so the whole
+// Alg. 2 loop runs on the device; the host reads back (T, gap_T, status) once.
+// Kernel arguments are frozen in the graph, so per-call values (eps, max_iters, ||B||,
+// history buffer) live in a device LoopParams block written before each launch, and the
+// ping-pong buffer of sweep t is selected on the device from the loop counter.
+#include "psi_internal.cuh"
+#include "../../include/psi.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+using namespace psi;
+
+namespace {
+
+thread_local std::string g_err;
+
+psi_status fail(psi_status code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+psi_status fail(psi_status code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define API_CK(call)                                                                     \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? PSI_E_OOM : PSI_E_CUDA,              \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);  \
+  } while (0)
+
+}  // namespace
+
+struct psi_ctx {
+  long long n = 0, m = 0;
+  cudaStream_t stream = nullptr;
+  IngestOut g;
+  double* x[2] = {nullptr, nullptr};
+  double* psi_dev = nullptr;
+  double* piece_first = nullptr;
+  double* piece_last = nullptr;
+  double* eps_part1 = nullptr;
+  double* eps_part2 = nullptr;
+  double* history = nullptr;
+  long long hist_cap = 0;
+  LoopState* st = nullptr;
+  LoopParams* prm = nullptr;
+  LoopState* h_st = nullptr;     // pinned
+  LoopParams* h_prm = nullptr;   // pinned
+  int grid1 = 0, grid2 = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool have_psi = false;
+  long long last_T = 0;
+  double last_gap = 1.0;
+  double ingest_ms = 0, iterate_ms = 0;
+  size_t device_bytes = 0;
+};
+
+namespace {
+
+void free_ctx(psi_ctx* c) {
+  if (!c) return;
+  if (c->exec) cudaGraphExecDestroy(c->exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  void* ptrs[] = {c->g.rp, c->g.idx, c->g.a, c->g.g, c->g.wt, c->g.d, c->g.lam,
+                  c->g.old_of_new, c->g.tile_coord, c->g.split, c->x[0], c->x[1], c->psi_dev,
+                  c->piece_first, c->piece_last, c->eps_part1, c->eps_part2, c->history,
+                  c->st, c->prm};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->h_st) cudaFreeHost(c->h_st);
+  if (c->h_prm) cudaFreeHost(c->h_prm);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  delete c;
+}
+
+SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
+  SweepArgs A{};
+  A.rp = c->g.rp;
+  A.idx = c->g.idx;
+  A.tile_coord = c->g.tile_coord;
+  A.ntiles = c->g.ntiles;
+  A.split = c->g.split;
+  A.nsplit = c->g.nsplit;
+  A.piece_first = c->piece_first;
+  A.piece_last = c->piece_last;
+  A.a = c->g.a;
+  A.g = c->g.g;
+  A.wt = c->g.wt;
+  A.d = c->g.d;
+  A.lam = c->g.lam;
+  A.inv_n = 1.0 / (double)c->n;
+  A.psi = c->psi_dev;
+  A.x0 = c->x[0];
+  A.x1 = c->x[1];
+  A.eps_part1 = c->eps_part1;
+  A.eps_part2 = c->eps_part2;
+  A.grid1 = c->grid1;
+  A.st = c->st;
+  A.prm = c->prm;
+  A.cond = cond;
+  return A;
+}
+
+cudaError_t add_kernel(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode_t* dep, size_t ndep,
+                       void* fn, int grid, int block, SweepArgs* args, int* n_extra) {
+  cudaKernelNodeParams p{};
+  p.func = fn;
+  p.gridDim = dim3(grid);
+  p.blockDim = dim3(block);
+  p.sharedMemBytes = 0;
+  void* kp[2] = {args, n_extra};
+  p.kernelParams = kp;
+  return cudaGraphAddKernelNode(node, g, dep, ndep, &p);
+}
+
+psi_status build_graph_exec(psi_ctx* c) {
+  API_CK(cudaGraphCreate(&c->graph, 0));
+  cudaGraphConditionalHandle cond;
+  API_CK(cudaGraphConditionalHandleCreate(&cond, c->graph, 0, cudaGraphCondAssignDefault));
+  SweepArgs A = make_args(c, cond);
+  int n_int = (int)c->n;
+
+  cudaGraphNode_t n_init, n_while, n_r1, n_r2;
+  int init_grid = (int)std::min<long long>((c->n + 255) / 256, 148LL * 8);
+  if (init_grid < 1) init_grid = 1;
+  API_CK(add_kernel(c->graph, &n_init, nullptr, 0, init_kernel_ptr(), init_grid, 256, &A, &n_int));
+
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  API_CK(cudaGraphAddNode(&n_while, c->graph, &n_init, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaGraphNode_t b1, b2;
+  API_CK(add_kernel(body, &b1, nullptr, 0, sweep_kernel_ptr(false), c->grid1, kBlock, &A, nullptr));
+  API_CK(add_kernel(body, &b2, &b1, 1, fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr));
+
+  API_CK(add_kernel(c->graph, &n_r1, &n_while, 1, sweep_kernel_ptr(true), c->grid1, kBlock, &A, nullptr));
+  API_CK(add_kernel(c->graph, &n_r2, &n_r1, 1, fix_kernel_ptr(true), c->grid2, kFixBlock, &A, nullptr));
+  API_CK(cudaGraphInstantiate(&c->exec, c->graph, 0));
+  return PSI_OK;
+}
+
+psi_status ensure_history(psi_ctx* c, long long need) {
+  const long long kMaxHist = 1LL << 24;
+  if (need > kMaxHist) need = kMaxHist;
+  if (need < 1) need = 1;
+  if (c->history && c->hist_cap >= need) return PSI_OK;
+  if (c->history) {
+    cudaFree(c->history);
+    c->device_bytes -= c->hist_cap * sizeof(double);
+    c->history = nullptr;
+  }
+  long long cap = need < 1024 ? 1024 : need;
+  API_CK(cudaMalloc(&c->history, cap * sizeof(double)));
+  c->hist_cap = cap;
+  c->device_bytes += cap * sizeof(double);
+  return PSI_OK;
+}
+
+__global__ void k_unpermute(const double* src, const double* scale, const int* old_of_new,
+                            long long n, double* dst) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = scale ? src[i] * scale[i] : src[i];
+    dst[old_of_new ? old_of_new[i] : i] = v;
+  }
+}
+
+psi_status copy_out(const psi_ctx* c, const double* src, const double* scale, double* out,
+                    int mem_kind) {
+  if (!c->g.old_of_new && !scale) {
+    API_CK(cudaMemcpyAsync(out, src, c->n * sizeof(double),
+                           mem_kind == PSI_MEM_HOST ? cudaMemcpyDeviceToHost
+                                                    : cudaMemcpyDeviceToDevice, c->stream));
+    API_CK(cudaStreamSynchronize(c->stream));
+    return PSI_OK;
+  }
+  double* dst = out;
+  double* tmp = nullptr;
+  if (mem_kind == PSI_MEM_HOST) {
+    API_CK(cudaMallocAsync((void**)&tmp, c->n * sizeof(double), c->stream));
+    dst = tmp;
+  }
+  int grid = (int)std::min<long long>((c->n + 255) / 256, 148LL * 16);
+  k_unpermute<<<grid < 1 ? 1 : grid, 256, 0, c->stream>>>(src, scale, c->g.old_of_new, c->n, dst);
+  API_CK(cudaGetLastError());
+  if (tmp) {
+    API_CK(cudaMemcpyAsync(out, tmp, c->n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    API_CK(cudaFreeAsync(tmp, c->stream));
+  }
+  API_CK(cudaStreamSynchronize(c->stream));
+  return PSI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* psi_last_error(void) { return g_err.c_str(); }
+
+psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* followers,
+                           const double* lambda, const double* mu, int mem_kind, void* stream,
+                           psi_ctx** out) {
+  g_err.clear();
+  if (!out) return fail(PSI_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || n > 2147483647LL) return fail(PSI_E_INVALID_ARG, "n = %lld outside [1, 2^31-1]", (long long)n);
+  if (m < 0 || m > 2147483647LL) return fail(PSI_E_INVALID_ARG, "m = %lld outside [0, 2^31-1]", (long long)m);
+  if (!row_ptr || !lambda || !mu || (m > 0 && !followers))
+    return fail(PSI_E_INVALID_ARG, "NULL input pointer");
+  if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
+    return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
+
+  psi_ctx* c = new psi_ctx;
+  c->n = n;
+  c->m = m;
+  c->stream = (cudaStream_t)stream;
+  auto bail = [&](psi_status st) { free_ctx(c); return st; };
+#define B_CK(call)                                                                          \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return bail(fail(e_ == cudaErrorMemoryAllocation ? PSI_E_OOM : PSI_E_CUDA,            \
+                       "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__)); \
+  } while (0)
+
+  B_CK(cudaEventCreate(&c->ev0));
+  B_CK(cudaEventCreate(&c->ev1));
+  B_CK(cudaEventRecord(c->ev0, c->stream));
+
+  // Stage host inputs (borrowed: copied, never retained).
+  const long long* rp_d = (const long long*)row_ptr;
+  const int* idx_d = followers;
+  const double* lam_d = lambda;
+  const double* mu_d = mu;
+  void* staged[4] = {nullptr, nullptr, nullptr, nullptr};
+  struct Free4 { void** p; ~Free4() { for (int i = 0; i < 4; ++i) if (p[i]) cudaFree(p[i]); } } f4{staged};
+  if (mem_kind == PSI_MEM_HOST) {
+    B_CK(cudaMalloc(&staged[0], (n + 1) * sizeof(long long)));
+    B_CK(cudaMalloc(&staged[1], (m > 0 ? m : 1) * sizeof(int)));
+    B_CK(cudaMalloc(&staged[2], n * sizeof(double)));
+    B_CK(cudaMalloc(&staged[3], n * sizeof(double)));
+    B_CK(cudaMemcpyAsync(staged[0], row_ptr, (n + 1) * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    if (m > 0)
+      B_CK(cudaMemcpyAsync(staged[1], followers, m * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    B_CK(cudaMemcpyAsync(staged[2], lambda, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    B_CK(cudaMemcpyAsync(staged[3], mu, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    rp_d = (const long long*)staged[0];
+    idx_d = (const int*)staged[1];
+    lam_d = (const double*)staged[2];
+    mu_d = (const double*)staged[3];
+  }
+
+  char msg[512] = {0};
+  int rc = ingest(n, m, rp_d, idx_d, lam_d, mu_d, true, c->stream, c->g, msg, sizeof(msg));
+  if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
+
+  // Iteration buffers.
+  c->grid1 = sweep_grid(c->g.ntiles);
+  c->grid2 = fix_grid(c->g.nsplit);
+  B_CK(cudaMalloc(&c->x[0], n * sizeof(double)));
+  B_CK(cudaMalloc(&c->x[1], n * sizeof(double)));
+  B_CK(cudaMalloc(&c->psi_dev, n * sizeof(double)));
+  B_CK(cudaMalloc(&c->piece_first, (c->g.ntiles + 1) * sizeof(double)));
+  B_CK(cudaMalloc(&c->piece_last, (c->g.ntiles + 1) * sizeof(double)));
+  B_CK(cudaMalloc(&c->eps_part1, c->grid1 * sizeof(double)));
+  B_CK(cudaMalloc(&c->eps_part2, c->grid2 * sizeof(double)));
+  B_CK(cudaMalloc(&c->st, sizeof(LoopState)));
+  B_CK(cudaMalloc(&c->prm, sizeof(LoopParams)));
+  B_CK(cudaMemsetAsync(c->st, 0, sizeof(LoopState), c->stream));
+  // Rows outside every tile keep x = a in both buffers (no-op for identity labels).
+  B_CK(cudaMemcpyAsync(c->x[0], c->g.a, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  B_CK(cudaMemcpyAsync(c->x[1], c->g.a, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  B_CK(cudaHostAlloc(&c->h_st, sizeof(LoopState), cudaHostAllocDefault));
+  B_CK(cudaHostAlloc(&c->h_prm, sizeof(LoopParams), cudaHostAllocDefault));
+  B_CK(cudaEventRecord(c->ev1, c->stream));
+  B_CK(cudaStreamSynchronize(c->stream));
+  float ms = 0;
+  B_CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  c->ingest_ms = ms;
+  c->device_bytes = (n + 1) * 4 + m * 4 + 8 * n * 8 + (c->g.ntiles + 1) * (8 + 16) +
+                    (long long)c->g.nsplit * 16 + (c->g.old_of_new ? n * 4 : 0);
+
+  psi_status gs = build_graph_exec(c);
+  if (gs != PSI_OK) return bail(gs);
+  *out = c;
+  return PSI_OK;
+#undef B_CK
+}
+
+psi_status psi_iterate(psi_ctx* c, double eps, int64_t max_iters, int norm, int64_t* iters_out,
+                       double* last_gap_out) {
+  g_err.clear();
+  if (!c) return fail(PSI_E_INVALID_ARG, "ctx is NULL");
+  if (!(eps >= 0.0)) return fail(PSI_E_INVALID_ARG, "eps must be >= 0 (got %g)", eps);
+  if (max_iters < 0) return fail(PSI_E_INVALID_ARG, "max_iters must be >= 0");
+  double kappa;
+  switch (norm) {
+    case PSI_NORM_ROW: kappa = c->g.kappa_row; break;
+    case PSI_NORM_COL: kappa = c->g.kappa_col; break;
+    case PSI_NORM_ONE: kappa = 1.0; break;
+    default: return fail(PSI_E_INVALID_ARG, "bad norm %d", norm);
+  }
+  c->have_psi = false;
+  psi_status hs = ensure_history(c, max_iters);
+  if (hs != PSI_OK) return hs;
+  c->h_prm->eps = eps;
+  c->h_prm->max_iters = max_iters;
+  c->h_prm->kappa = kappa;
+  c->h_prm->history = c->history;
+  c->h_prm->hist_cap = c->hist_cap;
+  API_CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(LoopParams), cudaMemcpyHostToDevice, c->stream));
+  API_CK(cudaEventRecord(c->ev0, c->stream));
+  API_CK(cudaGraphLaunch(c->exec, c->stream));
+  API_CK(cudaEventRecord(c->ev1, c->stream));
+  API_CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(LoopState), cudaMemcpyDeviceToHost, c->stream));
+  API_CK(cudaStreamSynchronize(c->stream));
+  float ms = 0;
+  API_CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  c->iterate_ms = ms;
+  c->last_T = c->h_st->iter;
+  c->last_gap = c->h_st->gap;
+  if (iters_out) *iters_out = c->last_T;
+  if (last_gap_out) *last_gap_out = c->last_gap;
+  if (c->h_st->status & 1)
+    return fail(PSI_E_NUMERIC, "epsilon_t became non-finite at t = %lld", c->last_T);
+  c->have_psi = true;
+  if (c->last_gap > eps) {
+    fail(PSI_NOT_CONVERGED, "not converged: gap %.3e > eps %.3e after %lld sweeps",
+         c->last_gap, eps, c->last_T);
+    return PSI_NOT_CONVERGED;
+  }
+  return PSI_OK;
+}
+
+psi_status psi_get_psi(const psi_ctx* c, double* out, int mem_kind) {
+  g_err.clear();
+  if (!c || !out) return fail(PSI_E_INVALID_ARG, "NULL argument");
+  if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
+    return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
+  if (!c->have_psi) return fail(PSI_E_STATE, "no successful psi_iterate on this context");
+  return copy_out(c, c->psi_dev, nullptr, out, mem_kind);
+}
+
+psi_status psi_get_series(const psi_ctx* c, double* out, int mem_kind) {
+  g_err.clear();
+  if (!c || !out) return fail(PSI_E_INVALID_ARG, "NULL argument");
+  if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
+    return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
+  if (!c->have_psi) return fail(PSI_E_STATE, "no successful psi_iterate on this context");
+  // s_T = Wt * x_T (kernel state, psi_internal.cuh)
+  return copy_out(c, c->x[c->last_T & 1], c->g.wt, out, mem_kind);
+}
+
+psi_status psi_get_residual_history(const psi_ctx* c, double* out, int64_t cap, int64_t* len_out) {
+  g_err.clear();
+  if (!c || (cap > 0 && !out)) return fail(PSI_E_INVALID_ARG, "NULL argument");
+  if (!c->have_psi) return fail(PSI_E_STATE, "no successful psi_iterate on this context");
+  if (len_out) *len_out = c->last_T;
+  long long k = c->last_T;
+  if (k > cap) k = cap;
+  if (k > c->hist_cap) k = c->hist_cap;
+  if (k > 0) {
+    API_CK(cudaMemcpyAsync(out, c->history, k * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    API_CK(cudaStreamSynchronize(c->stream));
+  }
+  return PSI_OK;
+}
+
+psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
+  g_err.clear();
+  if (!c || !out) return fail(PSI_E_INVALID_ARG, "NULL argument");
+  memset(out, 0, sizeof(*out));
+  out->n = c->n;
+  out->m = c->m;
+  out->n_f = c->g.n_f;
+  out->n_g = c->g.n_g;
+  out->n_leaderless = c->g.n_leaderless;
+  out->kappa_row = c->g.kappa_row;
+  out->kappa_col = c->g.kappa_col;
+  out->rho_A = c->g.rho_A;
+  out->ingest_ms = c->ingest_ms;
+  out->iterate_ms = c->iterate_ms;
+  out->last_iters = c->last_T;
+  out->last_gap = c->last_gap;
+  out->num_tiles = c->g.ntiles;
+  out->num_long_rows = c->g.nsplit;
+  out->grid = c->grid1;
+  out->device_bytes = (int64_t)c->device_bytes;
+  out->relabeled = c->g.relabeled;
+  return PSI_OK;
+}
+
+void psi_destroy(psi_ctx* c) { free_ctx(c); }
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+// psi_internal.cuh -- device data layout and kernel interfaces of libpsi (sm_100a).
+//
+// Kernel state (SURVEY §8 conventions):
+//   x_t = s_t / Wt,  Wt_j = W_j if W_j > 0 else 1                (s_t: Eq. (14))
+//   x_0 = a,  x_t,j = a_j + g_j * S_j(x_{t-1}),  S_j(x) = sum_{n in F(j)} x_n
+//   a = c / Wt,  g = mu / Wt
+//   eps_t = sum_j Wt_j |x_t,j - x_{t-1},j| = ||s_t - s_{t-1}||_1  (Eq. (15))
+//   psi_j = (d_j + lambda_j * S_j(x_T)) / N                      (Alg. 2)
+// This is the rank-1 factorisation A = P diag(c), B = P diag(d) with
+// P[n,j] = w_j / W_n 1{j in L(n)}: (s^T A)_j = mu_j sum_{n in F(j)} s_n / W_n,
+// so one gathered vector x serves A and B and no per-edge value is stored.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace psi {
+
+// Merge-path sweep tiles: TILE merge items (row completions + edges) per tile.
+constexpr int kBlock = 256;              // threads per CTA of the sweep kernel
+constexpr int kIpt = 8;                  // merge items per thread
+constexpr int kTile = kBlock * kIpt;     // 2048 items per tile
+constexpr int kFixBlock = 256;           // threads per CTA of the split-row fix-up kernel
+
+// Device-resident loop state (written by kernels, read back by the host once per iterate).
+struct LoopState {
+  long long iter;        // completed sweeps t
+  double gap;            // ||B|| * eps_t  (1 before the first sweep, Alg. 2)
+  double eps_t;          // last epsilon_t
+  unsigned int done;     // CTA arrival counter of the fix-up kernel
+  int status;            // bit 0: non-finite epsilon_t
+};
+
+// Per-call parameters (host writes them before every graph launch).
+struct LoopParams {
+  double eps;            // s-tolerance
+  long long max_iters;
+  double kappa;          // ||B|| for the selected norm
+  double* history;       // epsilon_t, t = 1..T
+  long long hist_cap;
+};
+
+// Everything one sweep / readout launch needs (passed by value; frozen in the graph).
+struct SweepArgs {
+  const int* rp;             // row_ptr (int32, relabelled) [n+1]
+  const int* idx;            // followers (int32, relabelled) [m]
+  const int2* tile_coord;    // merge-path start (row, edge) of tile k, k = 0..ntiles
+  int ntiles;
+  const int4* split;         // split rows: {row, first tile, last tile, 0}
+  int nsplit;
+  double* piece_first;       // per tile: partial sum of the tile's first row
+  double* piece_last;        // per tile: partial sum of the tile's trailing (unfinished) row
+  const double* a;
+  const double* g;
+  const double* wt;
+  const double* d;
+  const double* lam;
+  double inv_n;
+  double* psi;               // readout output (relabelled order)
+  double* x0;
+  double* x1;
+  double* eps_part1;         // per CTA of the tile kernel
+  double* eps_part2;         // per CTA of the fix-up kernel
+  int grid1;
+  LoopState* st;
+  const LoopParams* prm;
+  cudaGraphConditionalHandle cond;
+};
+
+// ---- launchers (psi_sweep.cu)
+int sweep_grid(int ntiles);          // persistent CTAs for the tile kernel
+int fix_grid(int nsplit);            // CTAs of the fix-up kernel
+void* sweep_kernel_ptr(bool readout);
+void* fix_kernel_ptr(bool readout);
+void* init_kernel_ptr();
+size_t sweep_smem_bytes();
+
+// ---- ingest (psi_ingest.cu)
+struct IngestOut {
+  int* rp = nullptr;         // [n+1]
+  int* idx = nullptr;        // [m]
+  double *a = nullptr, *g = nullptr, *wt = nullptr, *d = nullptr, *lam = nullptr;
+  int* old_of_new = nullptr; // [n] (relabel); nullptr = identity
+  int2* tile_coord = nullptr;
+  int ntiles = 0;
+  int4* split = nullptr;
+  int nsplit = 0;
+  double kappa_row = 0, kappa_col = 0, rho_A = 0;
+  long long n_f = 0, n_g = 0, n_leaderless = 0;
+  int relabeled = 0;
+};
+
+// Returns 0 or a negative psi_status; msg gets a description on error.
+int ingest(long long n, long long m, const long long* rp64_dev, const int* idx_dev,
+           const double* lam_dev, const double* mu_dev, bool relabel, cudaStream_t s,
+           IngestOut& out, char* msg, size_t msg_len);
+
+}  // namespace psi

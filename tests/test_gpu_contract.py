@@ -1,0 +1,109 @@
+"""C-ABI error contract and edge cases on the device (-m gpu), include/psi.h."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import psigen
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(*arrays):
+    import torch
+    return [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in arrays]
+
+
+def build_status(psi, rp, f, lam, mu):
+    try:
+        g = psi.PsiGraph(*dev(np.asarray(rp, np.int64), np.asarray(f, np.int32),
+                              np.asarray(lam, float), np.asarray(mu, float)))
+        g.close()
+        return psi.PSI_OK
+    except psi.PsiError as e:
+        return e.status
+
+
+@pytest.mark.parametrize("rp,f,why", [
+    ([1, 1, 2], [1, 0], "row_ptr[0] != 0"),
+    ([0, 1, 3], [1, 0], "row_ptr[n] != m"),
+    ([0, 2, 1], [1, 0], "decreasing"),
+    ([0, 1, 2], [5, 0], "index out of range"),
+    ([0, 1, 2], [-1, 0], "negative index"),
+    ([0, 1, 2], [0, 0], "self loop"),
+    ([0, 2, 2, 2], [2, 1, ], "unsorted row"),
+    ([0, 2, 2, 2], [1, 1], "duplicate follower"),
+])
+def test_graph_contract(gpu, rp, f, why):
+    n = len(rp) - 1
+    st = build_status(gpu, rp, f, np.ones(n), np.ones(n))
+    assert st == gpu.PSI_E_GRAPH, why
+
+
+@pytest.mark.parametrize("lam,mu", [([np.nan, 1], [1, 1]), ([1, np.inf], [1, 1]),
+                                    ([-1, 1], [1, 1]), ([0, 1], [0, 1])])
+def test_activity_contract(gpu, lam, mu):
+    assert build_status(gpu, [0, 1, 2], [1, 0], lam, mu) == gpu.PSI_E_ACTIVITY
+
+
+def test_invalid_args(gpu):
+    lib = gpu.load_library()
+    ctx = ctypes.c_void_p()
+    assert lib.psi_build_graph(3, 0, None, None, None, None, 1, None, ctypes.byref(ctx)) == gpu.PSI_E_INVALID_ARG
+    rp, f, lam, mu = dev(np.array([0, 1, 2], np.int64), np.array([1, 0], np.int32), np.ones(2), np.ones(2))
+    with gpu.PsiGraph(rp, f, lam, mu) as g:
+        with pytest.raises(gpu.PsiError) as e:
+            g.get_psi()
+        assert e.value.status == gpu.PSI_E_STATE
+        for bad in (dict(eps=-1.0), dict(eps=float("nan")), dict(max_iters=-1)):
+            kw = dict(eps=1e-9, max_iters=10)
+            kw.update(bad)
+            with pytest.raises(gpu.PsiError) as e:
+                g.iterate(**kw)
+            assert e.value.status == gpu.PSI_E_INVALID_ARG
+        st = lib.psi_iterate(g._ctx, 1e-9, 10, 7, None, None)
+        assert st == gpu.PSI_E_INVALID_ARG
+
+
+def test_not_converged_and_eps_ge_one(gpu):
+    w = psigen.make_config(1)
+    with gpu.PsiGraph(*dev(w.row_ptr, w.followers, w.lam, w.mu)) as g:
+        st, T, gap = g.iterate(1e-12, 5)
+        assert st == gpu.PSI_NOT_CONVERGED and T == 5 and gap > 1e-12
+        assert len(g.get_residual_history()) == 5
+        st, T, gap = g.iterate(1.0, 100)         # gap_0 = 1 is not > 1: T = 0 (Alg. 2)
+        assert st == gpu.PSI_OK and T == 0 and gap == 1.0
+        psi0 = g.get_psi().cpu().numpy()
+        st, T, _ = g.iterate(0.0, 0)             # max_iters = 0 -> T = 0, same psi_0
+        assert T == 0 and np.array_equal(g.get_psi().cpu().numpy(), psi0)
+    import oracle
+    ref = oracle.power_psi(w.row_ptr, w.followers, w.lam, w.mu, eps=1.0)
+    assert ref.iterations == 0
+    assert oracle.max_rel_error(ref.psi, psi0) < 1e-13
+
+
+def test_single_user_and_edgeless(gpu):
+    with gpu.PsiGraph(*dev(np.array([0, 0], np.int64), np.zeros(0, np.int32),
+                           np.array([0.3]), np.array([0.7]))) as g:
+        st, T, _ = g.iterate(1e-9)
+        assert g.get_psi().cpu().numpy()[0] == pytest.approx(0.3)
+    n = 5000
+    lam = np.linspace(0.1, 1, n)
+    mu = np.linspace(1, 0.1, n)
+    with gpu.PsiGraph(*dev(np.zeros(n + 1, np.int64), np.zeros(0, np.int32), lam, mu)) as g:
+        g.iterate(1e-9)
+        np.testing.assert_allclose(g.get_psi().cpu().numpy(), lam / (lam + mu) / n, rtol=1e-15)
+
+
+def test_numeric_divergence_reported(gpu):
+    """A closed set whose leaders all have lambda = 0 (rho(A) = 1, reading R6): eps_t does not
+    decay; the loop must stop at max_iters and say NOT_CONVERGED (never silent).  With the
+    ROW norm ||B|| = 0 here (B = 0), so Alg. 2 stops after one sweep; use norm ONE."""
+    rp, f = psigen.csr_from_edges(2, [(0, 1), (1, 0)])
+    with gpu.PsiGraph(*dev(rp, f, np.zeros(2), np.ones(2))) as g:
+        st, T, gap = g.iterate(1e-9, 50, norm="one")
+        assert st == gpu.PSI_NOT_CONVERGED and T == 50
+        assert np.all(g.get_residual_history() == 2.0)     # ||c^T A^t||_1 = 2 for all t
+        st, T, gap = g.iterate(1e-9, 50, norm="row")
+        assert st == gpu.PSI_OK and T == 1 and gap == 0.0

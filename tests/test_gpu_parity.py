@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle (-m gpu).
+
+Parity protocol:
+  1. the oracle runs Alg. 2 to eps and records T*, eps_t, psi;
+  2. the GPU runs psi_iterate(eps=0, max_iters=T*) (fixed count) -> max relative
+     error per psi entry <= 1e-10 (north_star), same top-k (ties R10);
+  3. the GPU runs psi_iterate(eps) -> |T_gpu - T*| <= 1 and matching eps_t histories.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import psigen
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10          # north_star: max relative error per psi entry, fp64
+
+
+def to_dev(*arrays):
+    import torch
+    return [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in arrays]
+
+
+def gpu_run(psi, rp, f, lam, mu, eps, max_iters=100_000, norm="row", host=False):
+    import torch
+    args = (rp, f, lam, mu) if host else to_dev(rp, f, lam, mu)
+    with psi.PsiGraph(*args) as g:
+        st, T, gap = g.iterate(eps, max_iters, norm)
+        out = g.get_psi().cpu().numpy()
+        s = g.get_series().cpu().numpy()
+        hist = g.get_residual_history()
+        info = g.info()
+    torch.cuda.synchronize()
+    return dict(psi=out, T=T, gap=gap, status=st, hist=hist, s=s, info=info)
+
+
+def check_topk(ref, got, ks=(10, 100, 1000)):
+    """Same top-k; pairs within 1e-10 relative may swap (reading R10)."""
+    for k in ks:
+        k = min(k, ref.size)
+        a, b = oracle.top_k(ref, k), oracle.top_k(got, k)
+        if np.array_equal(a, b):
+            continue
+        # allowed only for near-ties at the boundary / inside
+        diff = set(a.tolist()) ^ set(b.tolist())
+        kth = np.sort(ref)[::-1][k - 1]
+        for j in diff:
+            assert abs(ref[j] - kth) <= 1e-10 * kth, (k, j)
+        for x, y in zip(a, b):
+            if x != y:
+                assert abs(ref[x] - ref[y]) <= 1e-10 * max(ref[x], ref[y]), (k, x, y)
+
+
+def parity(psi, w, norm="row", eps=None, full=True):
+    eps = w.eps if eps is None else eps
+    ref = oracle.power_psi(w.row_ptr, w.followers, w.lam, w.mu, eps=eps, norm=norm)
+    got = gpu_run(psi, w.row_ptr, w.followers, w.lam, w.mu, 0.0, ref.iterations, norm)
+    assert got["T"] == ref.iterations
+    err = oracle.max_rel_error(ref.psi, got["psi"])
+    assert err <= TOL, err
+    assert oracle.relative_error(ref.psi, got["psi"]) <= TOL
+    check_topk(ref.psi, got["psi"])
+    assert oracle.max_rel_error(ref.s, got["s"]) <= TOL
+    if full:
+        g2 = gpu_run(psi, w.row_ptr, w.followers, w.lam, w.mu, eps, 10 * ref.iterations + 10, norm)
+        assert abs(g2["T"] - ref.iterations) <= 1, (g2["T"], ref.iterations)
+        h_ref = np.array(ref.history)
+        k = min(len(h_ref), len(g2["hist"]))
+        s1 = np.abs(ref.s).sum()
+        np.testing.assert_allclose(g2["hist"][:k], h_ref[:k], rtol=1e-6, atol=1e-13 * s1)
+    return ref, got
+
+
+# ---------------------------------------------------------------- fixtures
+
+@pytest.mark.parametrize("name", ["chain", "mutual", "cycle3_homogeneous", "edgeless"])
+def test_spec_fixtures_on_gpu(gpu, name):
+    import json, os
+    case = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                       "spec_examples.json")))[name]
+    rp, f = psigen.csr_from_edges(case["n"], case["edges"])
+    lam, mu = np.array(case["lam"]), np.array(case["mu"])
+    got = gpu_run(gpu, rp, f, lam, mu, 1e-14)
+    np.testing.assert_allclose(got["psi"], case["psi"], rtol=0, atol=1e-12)
+    if "psi_sum" in case:
+        assert abs(got["psi"].sum() - case["psi_sum"]) < 1e-12
+
+
+def test_chain_iteration_count_and_history(gpu):
+    rp, f = psigen.csr_from_edges(2, [(0, 1)])
+    got = gpu_run(gpu, rp, f, np.array([0.5, 0.5]), np.array([0.5, 0.5]), 1e-12)
+    assert got["T"] == 2 and got["hist"][0] == pytest.approx(0.25, abs=1e-15) and got["hist"][1] == 0
+    np.testing.assert_allclose(got["s"], [0.5, 0.75], atol=1e-15)
+
+
+def test_heterogeneous_cycle_and_star_closed_forms(gpu):
+    rng = np.random.default_rng(11)
+    n = 9
+    rp, f = psigen.csr_from_edges(n, [(j, (j + 1) % n) for j in range(n)])
+    lam, mu = rng.uniform(0.05, 1, n), rng.uniform(0.05, 1, n)
+    c, d = mu / (lam + mu), lam / (lam + mu)
+    u = np.array([sum(np.prod([c[(j - m) % n] for m in range(1, k + 1)]) for k in range(n))
+                  for j in range(n)]) / (1 - np.prod(c))
+    got = gpu_run(gpu, rp, f, lam, mu, 0.0, 3000)
+    np.testing.assert_allclose(got["psi"], d * u / n, rtol=1e-13)
+    k = 40
+    rp, f = psigen.csr_from_edges(k + 1, [(i, 0) for i in range(1, k + 1)])
+    lam, mu = rng.uniform(0.05, 1, k + 1), rng.uniform(0.05, 1, k + 1)
+    c, d = mu / (lam + mu), lam / (lam + mu)
+    got = gpu_run(gpu, rp, f, lam, mu, 1e-15)
+    want = d / (k + 1)
+    want[0] = d[0] * (1 + c[1:].sum()) / (k + 1)
+    np.testing.assert_allclose(got["psi"], want, rtol=1e-14)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_random_small_graphs_fixed_count(gpu, seed):
+    """Random graphs N in [10, 300] (leaderless, mu = 0 and lambda = 0 users): exact
+    Alg. 2 parity at a fixed T, all three norms."""
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.integers(10, 300))
+    p = float(rng.uniform(0.01, 0.3))
+    mask = rng.random((n, n)) < p
+    np.fill_diagonal(mask, False)
+    mask[rng.choice(n, n // 10, replace=False), :] = False            # leaderless users
+    fol, lead = np.nonzero(mask)
+    rp, f = psigen.csr_from_edges(n, np.stack([fol, lead], 1))
+    lam, mu = rng.uniform(0.05, 1, n), rng.uniform(0.05, 1, n)
+    pick = rng.permutation(n)
+    mu[pick[: n // 10]] = 0.0
+    lam[pick[n // 10: n // 10 + n // 20]] = 0.0
+    norm = ("row", "col", "one")[seed % 3]
+    T = int(rng.integers(0, 40))
+    ref = oracle.power_psi(rp, f, lam, mu, eps=0.0, max_iters=T, norm=norm)
+    got = gpu_run(gpu, rp, f, lam, mu, 0.0, T, norm)
+    assert got["T"] == ref.iterations
+    assert oracle.max_rel_error(ref.psi, got["psi"]) <= 1e-12
+    np.testing.assert_allclose(got["hist"], ref.history, rtol=1e-11, atol=1e-15)
+
+
+def test_long_rows_span_many_tiles(gpu):
+    """A hub followed by everybody (row longer than several 2048-item tiles) + a chain."""
+    n = 9000
+    edges = [(i, 0) for i in range(1, n)] + [(0, 1)] + [(i, i + 1) for i in range(1, n - 1)]
+    rp, f = psigen.csr_from_edges(n, edges)
+    rng = np.random.default_rng(3)
+    lam, mu = rng.uniform(0.05, 1, n), rng.uniform(0.05, 1, n)
+    ref = oracle.power_psi(rp, f, lam, mu, eps=1e-13)
+    got = gpu_run(gpu, rp, f, lam, mu, 0.0, ref.iterations)
+    assert oracle.max_rel_error(ref.psi, got["psi"]) <= TOL
+    assert got["info"]["num_long_rows"] >= 1
+
+
+# ---------------------------------------------------------------- configs
+
+def test_config0_and_nsystems(gpu):
+    w = psigen.make_config(0)
+    parity(gpu, w)
+    brute = oracle.psi_nsystems(w.row_ptr, w.followers, w.lam, w.mu)
+    got = gpu_run(gpu, w.row_ptr, w.followers, w.lam, w.mu, w.eps)
+    assert oracle.relative_error(brute, got["psi"]) < 1e-11
+
+
+@pytest.mark.parametrize("norm", ["row", "col", "one"])
+def test_config1_parity(gpu, norm):
+    w = psigen.make_config(1)
+    parity(gpu, w, norm=norm)
+
+
+def test_config1_vs_exact(gpu):
+    w = psigen.make_config(1)
+    exact = oracle.psi_exact(w.row_ptr, w.followers, w.lam, w.mu)
+    got = gpu_run(gpu, w.row_ptr, w.followers, w.lam, w.mu, w.eps)
+    assert oracle.max_rel_error(exact, got["psi"]) < 1e-10
+    assert abs(got["psi"].sum() - 1) < 1e-10
+
+
+def test_config2_parity_and_pagerank(gpu):
+    w = psigen.make_config(2)
+    ref, got = parity(gpu, w)
+    pi, _, _ = oracle.pagerank_power(w.row_ptr, w.followers, 0.5, eps=1e-14)
+    assert oracle.max_rel_error(pi, got["psi"]) < 1e-9     # psi = PageRank(0.5)
+
+
+def test_config3_parity(gpu):
+    w = psigen.make_config(3)
+    ref, got = parity(gpu, w, full=False)
+    assert got["info"]["n_leaderless"] > 0
+
+
+def test_config4_small_scale_parity(gpu):
+    w = psigen.make_config(4, scale=18)
+    parity(gpu, w)
+
+
+def test_config5_small_scale_parity(gpu):
+    w = psigen.make_config(5, scale=18)
+    parity(gpu, w)
+
+
+# ------------------------------------------------------------ determinism, host input
+
+def test_deterministic_and_host_equals_device(gpu):
+    w = psigen.make_config(4, scale=16)
+    a = gpu_run(gpu, w.row_ptr, w.followers, w.lam, w.mu, w.eps)
+    b = gpu_run(gpu, w.row_ptr, w.followers, w.lam, w.mu, w.eps)
+    c = gpu_run(gpu, w.row_ptr, w.followers, w.lam, w.mu, w.eps, host=True)
+    assert np.array_equal(a["psi"], b["psi"]) and np.array_equal(a["hist"], b["hist"])
+    assert np.array_equal(a["psi"], c["psi"])
+
+
+def test_repeated_iterate_on_one_context(gpu):
+    import torch
+    w = psigen.make_config(1)
+    with gpu.PsiGraph(*to_dev(w.row_ptr, w.followers, w.lam, w.mu)) as g:
+        _, T1, _ = g.iterate(1e-9)
+        p1 = g.get_psi().cpu().numpy()
+        _, T2, _ = g.iterate(1e-12)
+        _, T3, _ = g.iterate(1e-9)
+        p3 = g.get_psi().cpu().numpy()
+    assert T2 > T1 == T3 and np.array_equal(p1, p3)

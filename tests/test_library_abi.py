@@ -1,0 +1,62 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every symbol include/psi.h
+declares (no compute calls: this runs without a GPU)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2206_09960_b200 as psi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "psi.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(psi_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    assert declared_symbols() == sorted(psi.EXPORTED)
+
+
+def test_library_builds_and_exports_every_symbol():
+    path = psi._build.build()
+    lib = ctypes.CDLL(path)
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    out = subprocess.check_output(["nm", "-D", "--defined-only", path], text=True)
+    exported = set(re.findall(r" T (psi_\w+)", out))
+    assert set(declared_symbols()) <= exported
+
+
+def test_library_is_sm100a_code():
+    path = psi._build.build()
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", path], text=True)
+    assert "sm_100a" in out
+
+
+def test_error_paths_without_device():
+    """Argument validation happens before any CUDA call."""
+    lib = psi.load_library()
+    ctx = ctypes.c_void_p()
+    st = lib.psi_build_graph(0, 0, None, None, None, None, 0, None, ctypes.byref(ctx))
+    assert st == psi.PSI_E_INVALID_ARG and b"n = 0" in lib.psi_last_error()
+    st = lib.psi_iterate(None, 1e-9, 10, 0, None, None)
+    assert st == psi.PSI_E_INVALID_ARG
+    info = psi.psi_info()
+    assert lib.psi_get_info(None, ctypes.byref(info)) == psi.PSI_E_INVALID_ARG
+    lib.psi_destroy(None)   # no-op
+
+
+def test_no_oracle_import_in_product_package():
+    """The product path never touches oracle/ (parity would be void)."""
+    pkg = os.path.join(ROOT, "paper_2206_09960_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
