@@ -52,7 +52,6 @@ struct psi_ctx {
   cudaStream_t stream = nullptr;
   IngestOut g;
   double* x[2] = {nullptr, nullptr};
-  double* psi_dev = nullptr;
   double* piece_first = nullptr;
   double* piece_last = nullptr;
   double* eps_part1 = nullptr;
@@ -80,8 +79,8 @@ void free_ctx(psi_ctx* c) {
   if (!c) return;
   if (c->exec) cudaGraphExecDestroy(c->exec);
   if (c->graph) cudaGraphDestroy(c->graph);
-  void* ptrs[] = {c->g.rp, c->g.idx, c->g.a, c->g.g, c->g.wt, c->g.d, c->g.lam,
-                  c->g.old_of_new, c->g.tile_coord, c->g.split, c->x[0], c->x[1], c->psi_dev,
+  void* ptrs[] = {c->g.rp, c->g.idx, c->g.a0, c->g.a1, c->g.g, c->g.wt, c->g.d1, c->g.lam,
+                  c->g.psi, c->g.old_of_new, c->g.tile_coord, c->g.split, c->x[0], c->x[1],
                   c->piece_first, c->piece_last, c->eps_part1, c->eps_part2, c->history,
                   c->st, c->prm};
   for (void* p : ptrs)
@@ -103,13 +102,15 @@ SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   A.nsplit = c->g.nsplit;
   A.piece_first = c->piece_first;
   A.piece_last = c->piece_last;
-  A.a = c->g.a;
+  A.a0 = c->g.a0;
+  A.a = c->g.a1;
   A.g = c->g.g;
   A.wt = c->g.wt;
-  A.d = c->g.d;
+  A.d = c->g.d1;
   A.lam = c->g.lam;
-  A.inv_n = 1.0 / (double)c->n;
-  A.psi = c->psi_dev;
+  A.n_users = (double)c->n;
+  A.n_act = (int)c->g.n_act;
+  A.psi = c->g.psi;
   A.x0 = c->x[0];
   A.x1 = c->x[1];
   A.eps_part1 = c->eps_part1;
@@ -274,7 +275,7 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   }
 
   char msg[512] = {0};
-  int rc = ingest(n, m, rp_d, idx_d, lam_d, mu_d, true, c->stream, c->g, msg, sizeof(msg));
+  int rc = ingest(n, m, rp_d, idx_d, lam_d, mu_d, c->stream, c->g, msg, sizeof(msg));
   if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
 
   // Iteration buffers.
@@ -282,7 +283,6 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   c->grid2 = fix_grid(c->g.nsplit);
   B_CK(cudaMalloc(&c->x[0], n * sizeof(double)));
   B_CK(cudaMalloc(&c->x[1], n * sizeof(double)));
-  B_CK(cudaMalloc(&c->psi_dev, n * sizeof(double)));
   B_CK(cudaMalloc(&c->piece_first, (c->g.ntiles + 1) * sizeof(double)));
   B_CK(cudaMalloc(&c->piece_last, (c->g.ntiles + 1) * sizeof(double)));
   B_CK(cudaMalloc(&c->eps_part1, c->grid1 * sizeof(double)));
@@ -290,9 +290,9 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   B_CK(cudaMalloc(&c->st, sizeof(LoopState)));
   B_CK(cudaMalloc(&c->prm, sizeof(LoopParams)));
   B_CK(cudaMemsetAsync(c->st, 0, sizeof(LoopState), c->stream));
-  // Rows outside every tile keep x = a in both buffers (no-op for identity labels).
-  B_CK(cudaMemcpyAsync(c->x[0], c->g.a, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  B_CK(cudaMemcpyAsync(c->x[1], c->g.a, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  // Follower-less users keep x = a0 in both buffers for ever (they are never written).
+  B_CK(cudaMemcpyAsync(c->x[0], c->g.a0, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  B_CK(cudaMemcpyAsync(c->x[1], c->g.a0, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   B_CK(cudaHostAlloc(&c->h_st, sizeof(LoopState), cudaHostAllocDefault));
   B_CK(cudaHostAlloc(&c->h_prm, sizeof(LoopParams), cudaHostAllocDefault));
   B_CK(cudaEventRecord(c->ev1, c->stream));
@@ -300,8 +300,8 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   float ms = 0;
   B_CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   c->ingest_ms = ms;
-  c->device_bytes = (n + 1) * 4 + m * 4 + 8 * n * 8 + (c->g.ntiles + 1) * (8 + 16) +
-                    (long long)c->g.nsplit * 16 + (c->g.old_of_new ? n * 4 : 0);
+  c->device_bytes = (c->g.n_act + 1) * 4 + c->g.m_act * 4 + 6 * n * 8 + 4 * c->g.n_act * 8 +
+                    (c->g.ntiles + 1) * (8 + 16) + (long long)c->g.nsplit * 16 + n * 4;
 
   psi_status gs = build_graph_exec(c);
   if (gs != PSI_OK) return bail(gs);
@@ -361,7 +361,7 @@ psi_status psi_get_psi(const psi_ctx* c, double* out, int mem_kind) {
   if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
     return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
   if (!c->have_psi) return fail(PSI_E_STATE, "no successful psi_iterate on this context");
-  return copy_out(c, c->psi_dev, nullptr, out, mem_kind);
+  return copy_out(c, c->g.psi, nullptr, out, mem_kind);
 }
 
 psi_status psi_get_series(const psi_ctx* c, double* out, int mem_kind) {

@@ -12,12 +12,25 @@
 //     Wt = W (or 1 if W = 0, reading R5), a = c/Wt, g = mu/Wt;
 //  4. ||B|| in all three readings (R1): kappa_row = max_n Lambda_n/W_n,
 //     kappa_col = max_i lambda_i sum_{j in F(i)} 1/W_j; rho_A = max_n M_n/W_n;
-//  5. merge-path tile coordinates and the list of rows cut by tile boundaries.
+//  5. locality relabel: users WITH followers ("active": their s can
+//     change) get labels [0, n_act), follower-less users [n_act, n).  Inside the active
+//     range: users with >= 2 leaders sorted by leader count, descending (their x is
+//     gathered once per leader, so the most-gathered entries form a contiguous hot
+//     prefix that stays in L2); then leaderless active users; then single-leader users
+//     level by level in the order of their leader's label (each is gathered exactly once
+//     per sweep, by its leader's row, so rows processed in label order read them as a
+//     stream).  A follower-less user n never changes (x_n = a_n for all t), so its term
+//     is folded into per-row constants K_j = sum_{n in F(j), n follower-less} a_n:
+//     x_t,j = (a_j + g_j K_j) + g_j sum_{active n} x_n, and the readout uses
+//     d_j + lambda_j K_j; its psi is d_n/N (no B term).  Exact algebra, fixed order.
+//  6. the relabelled CSR over active rows (followers mapped to new labels, sorted per
+//     row), merge-path tile coordinates, and the rows cut by tile boundaries.
 #include "psi_internal.cuh"
 #include "../../include/psi.h"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 
@@ -30,14 +43,26 @@ namespace {
 enum : int {
   F_RP0 = 1, F_RPN = 2, F_RPMONO = 4, F_RANGE = 8, F_SELF = 16, F_ORDER = 32, F_ACT = 64,
 };
+// user classes of the relabel
+enum : unsigned char { C_HOT = 0, C_SINGLE = 1, C_ROOT = 2, C_INACTIVE = 3 };
+
+constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ unsigned long long dbits(double x) {
   return (unsigned long long)__double_as_longlong(x);
 }
 
+#define GRID_STRIDE(i, n)                                                                  \
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)(n); \
+       i += (long long)gridDim.x * blockDim.x)
+#define WARP_STRIDE(w, n)                                                                      \
+  for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; w < (long long)(n); \
+       w += (long long)gridDim.x * blockDim.x / 32)
+
+// ------------------------------------------------------------------ 1. validation
+
 __global__ void k_check_rowptr(const long long* rp, long long n, long long m, int* flags) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += stride) {
+  GRID_STRIDE(r, n) {
     const long long a = rp[r], b = rp[r + 1];
     int f = 0;
     if (b < a) f |= F_RPMONO;
@@ -48,16 +73,13 @@ __global__ void k_check_rowptr(const long long* rp, long long n, long long m, in
 }
 
 __global__ void k_rowptr32(const long long* rp64, int* rp32, long long n1) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n1; r += stride)
-    rp32[r] = (int)rp64[r];
+  GRID_STRIDE(r, n1) rp32[r] = (int)rp64[r];
 }
 
 // warp per row: range, self loop, strictly increasing
 __global__ void k_check_edges(const int* rp, const int* idx, int n, int* flags) {
   const int lane = threadIdx.x & 31;
-  const long long nw = (long long)gridDim.x * blockDim.x / 32;
-  for (long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; row < n; row += nw) {
+  WARP_STRIDE(row, n) {
     const int b = rp[row], e = rp[row + 1];
     int f = 0;
     for (int q = b + lane; q < e; q += 32) {
@@ -66,26 +88,26 @@ __global__ void k_check_edges(const int* rp, const int* idx, int n, int* flags) 
       if (v == (int)row) f |= F_SELF;
       if (q + 1 < e && idx[q + 1] <= v) f |= F_ORDER;
     }
-    f = __reduce_or_sync(0xffffffffu, f);
+    f = __reduce_or_sync(kFull, f);
     if (lane == 0 && f) atomicOr(flags, f);
   }
 }
 
 __global__ void k_check_activity(const double* lam, const double* mu, long long n, int* flags) {
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+  GRID_STRIDE(i, n) {
     const double l = lam[i], u = mu[i];
     const bool ok = isfinite(l) && isfinite(u) && l >= 0.0 && u >= 0.0 && (l + u) > 0.0;
     if (!ok) atomicOr(flags, F_ACT);
   }
 }
 
-// leader (row) of every edge, and #leaders of every follower
+// ------------------------------------------------------------------ 2.-4. normalisers
+
+// leader (row) of every edge, a copy of the follower, and #leaders of every follower
 __global__ void k_expand(const int* rp, const int* idx, int n, int* leader_of_edge,
                          int* follower_copy, int* n_leaders) {
   const int lane = threadIdx.x & 31;
-  const long long nw = (long long)gridDim.x * blockDim.x / 32;
-  for (long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; row < n; row += nw) {
+  WARP_STRIDE(row, n) {
     const int b = rp[row], e = rp[row + 1];
     for (int q = b + lane; q < e; q += 32) {
       const int v = idx[q];
@@ -96,13 +118,13 @@ __global__ void k_expand(const int* rp, const int* idx, int n, int* leader_of_ed
   }
 }
 
-// warp per user n: W_n, Lambda_n, M_n over its leaders (ascending), then the constants.
+// warp per user n: W_n, Lambda_n, M_n over its leaders (ascending, fixed tree), then constants.
 __global__ void k_normalisers(const int* loff, const int* leaders, const double* lam,
                               const double* mu, int n, double* a, double* g, double* wt,
-                              double* d, unsigned long long* kmax, unsigned long long* cnt) {
+                              double* d, int* first_leader, unsigned long long* kmax,
+                              unsigned long long* cnt) {
   const int lane = threadIdx.x & 31;
-  const long long nw = (long long)gridDim.x * blockDim.x / 32;
-  for (long long u = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; u < n; u += nw) {
+  WARP_STRIDE(u, n) {
     const int b = loff[u], e = loff[u + 1];
     double W = 0.0, L = 0.0, M = 0.0;
     for (int q = b + lane; q < e; q += 32) {
@@ -114,9 +136,9 @@ __global__ void k_normalisers(const int* loff, const int* leaders, const double*
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      W += __shfl_xor_sync(0xffffffffu, W, o);
-      L += __shfl_xor_sync(0xffffffffu, L, o);
-      M += __shfl_xor_sync(0xffffffffu, M, o);
+      W += __shfl_xor_sync(kFull, W, o);
+      L += __shfl_xor_sync(kFull, L, o);
+      M += __shfl_xor_sync(kFull, M, o);
     }
     if (lane == 0) {
       const double lu = lam[u], mu_u = mu[u];
@@ -127,6 +149,7 @@ __global__ void k_normalisers(const int* loff, const int* leaders, const double*
       wt[u] = W_t;
       a[u] = c / W_t;
       g[u] = mu_u / W_t;
+      first_leader[u] = e > b ? leaders[b] : -1;
       if (W > 0.0) {
         atomicMax(kmax + 0, dbits(L / W));             // row sum of B
         atomicMax(kmax + 1, dbits(M / W));             // row sum of A
@@ -137,29 +160,148 @@ __global__ void k_normalisers(const int* loff, const int* leaders, const double*
   }
 }
 
-// warp per leader i: column sum of B = lambda_i sum_{j in F(i)} 1/W_j; count rows with followers.
+// warp per leader i: column sum of B = lambda_i sum_{j in F(i)} 1/W_j.
 __global__ void k_kappa_col(const int* rp, const int* idx, const double* wt, const double* lam,
-                            int n, unsigned long long* kmax, unsigned long long* cnt) {
+                            int n, unsigned long long* kmax) {
   const int lane = threadIdx.x & 31;
-  const long long nw = (long long)gridDim.x * blockDim.x / 32;
-  for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; i < n; i += nw) {
+  WARP_STRIDE(i, n) {
     const int b = rp[i], e = rp[i + 1];
     double s = 0.0;
     for (int q = b + lane; q < e; q += 32) s += 1.0 / wt[idx[q]];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0 && e > b) {
-      atomicMax(kmax + 2, dbits(lam[i] * s));
-      atomicAdd(cnt + 1, 1ull);                        // N_f
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (lane == 0 && e > b) atomicMax(kmax + 2, dbits(lam[i] * s));
+  }
+}
+
+// ------------------------------------------------------------------ 5. relabel
+
+__global__ void k_classify(const int* rp, const int* nlead, int n, unsigned char* cls,
+                           int* new_of_old, unsigned long long* counts) {
+  GRID_STRIDE(u, n) {
+    const bool active = rp[u + 1] > rp[u];
+    const int nl = nlead[u];
+    unsigned char c = !active ? C_INACTIVE : nl >= 2 ? C_HOT : nl == 1 ? C_SINGLE : C_ROOT;
+    cls[u] = c;
+    new_of_old[u] = -1;
+    atomicAdd(counts + c, 1ull);
+  }
+}
+
+// selection keys for one relabel stage
+//   stage 0: hot users, key = (INT_MAX - #leaders) << 32 | u   (descending leader count)
+//   stage 1: leaderless active users, key = u
+//   stage 2: single-leader users whose leader is labelled, key = label(leader) << 32 | u
+//   stage 3: remaining single-leader users (cycles), key = leader << 32 | u
+//   stage 4: follower-less users, key = u
+__global__ void k_stage_keys(int stage, const unsigned char* cls, const int* nlead,
+                             const int* first_leader, const int* new_of_old, int n,
+                             unsigned long long* key, unsigned char* flag) {
+  GRID_STRIDE(u, n) {
+    const unsigned char c = cls[u];
+    unsigned char f = 0;
+    unsigned long long k = (unsigned long long)u;
+    if (stage == 0) {
+      f = c == C_HOT;
+      k |= (unsigned long long)(0x7fffffff - nlead[u]) << 32;
+    } else if (stage == 1) {
+      f = c == C_ROOT;
+    } else if (stage == 2) {
+      if (c == C_SINGLE && new_of_old[u] < 0) {
+        const int lab = new_of_old[first_leader[u]];
+        if (lab >= 0) { f = 1; k |= (unsigned long long)lab << 32; }
+      }
+    } else if (stage == 3) {
+      if (c == C_SINGLE && new_of_old[u] < 0) {
+        f = 1;
+        k |= (unsigned long long)first_leader[u] << 32;
+      }
+    } else {
+      f = c == C_INACTIVE;
+    }
+    flag[u] = f;
+    key[u] = k;
+  }
+}
+
+__global__ void k_assign(const unsigned long long* sel, long long cnt, int base, int* new_of_old,
+                         int* old_of_new) {
+  GRID_STRIDE(i, cnt) {
+    const int u = (int)(sel[i] & 0xffffffffull);
+    new_of_old[u] = base + (int)i;
+    old_of_new[base + i] = u;
+  }
+}
+
+// warp per new active row r: #active followers, and K_r = sum of a_n over follower-less ones
+__global__ void k_row_count(const int* rp, const int* idx, const int* old_of_new,
+                            const unsigned char* cls, const double* a_old, int n_act, int* cnt,
+                            double* K) {
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(r, n_act) {
+    const int o = old_of_new[r];
+    const int b = rp[o], e = rp[o + 1];
+    int c = 0;
+    double k = 0.0;
+    for (int q = b + lane; q < e; q += 32) {
+      const int v = idx[q];
+      if (cls[v] == C_INACTIVE) k += a_old[v]; else ++c;
+    }
+    c = __reduce_add_sync(kFull, c);
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) k += __shfl_xor_sync(kFull, k, s);
+    if (lane == 0) { cnt[r] = c; K[r] = k; }
+  }
+}
+
+// warp per new active row: write the active followers' new labels (unsorted, stable)
+__global__ void k_row_fill(const int* rp, const int* idx, const int* old_of_new,
+                           const unsigned char* cls, const int* new_of_old, const int* rp_new,
+                           int n_act, int* idx_new) {
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(r, n_act) {
+    const int o = old_of_new[r];
+    const int b = rp[o], e = rp[o + 1];
+    int out = rp_new[r];
+    for (int q0 = b; q0 < e; q0 += 32) {
+      const int q = q0 + lane;
+      int v = -1;
+      bool act = false;
+      if (q < e) { v = idx[q]; act = cls[v] != C_INACTIVE; }
+      const unsigned mask = __ballot_sync(kFull, act);
+      if (act) idx_new[out + __popc(mask & ((1u << lane) - 1u))] = new_of_old[v];
+      out += __popc(mask);
     }
   }
 }
 
+__global__ void k_permute_vectors(const int* old_of_new, int n, int n_act, const double* a_old,
+                                  const double* g_old, const double* wt_old, const double* d_old,
+                                  const double* lam, const double* K, double n_users,
+                                  double* a0, double* a1, double* g1, double* wt_new, double* d1,
+                                  double* lam1, double* psi) {
+  GRID_STRIDE(r, n) {
+    const int o = old_of_new[r];
+    a0[r] = a_old[o];
+    wt_new[r] = wt_old[o];
+    if (r < n_act) {
+      const double k = K[r];
+      a1[r] = fma(g_old[o], k, a_old[o]);
+      g1[r] = g_old[o];
+      d1[r] = fma(lam[o], k, d_old[o]);
+      lam1[r] = lam[o];
+    } else {
+      psi[r] = d_old[o] / n_users;          // follower-less: (s^T B)_r = 0
+    }
+  }
+}
+
+// ------------------------------------------------------------------ 6. tiles
+
 // merge-path coordinate (row, edge) of diagonal k*kTile: a = row ends rp[1..n], b = 0..m-1
 __global__ void k_tile_coords(const int* rp, int n, int m, int ntiles, int2* tc) {
-  const int stride = gridDim.x * blockDim.x;
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= ntiles; k += stride) {
-    long long diag = (long long)k * kTile;
+  GRID_STRIDE(k, ntiles + 1) {
+    long long diag = k * (long long)kTile;
     if (diag > (long long)n + m) diag = (long long)n + m;
     long long lo = diag - m > 0 ? diag - m : 0;
     long long hi = diag < n ? diag : n;
@@ -171,31 +313,30 @@ __global__ void k_tile_coords(const int* rp, int n, int m, int ntiles, int2* tc)
   }
 }
 
-// rows whose merge items fall in more than one tile
-__global__ void k_split_flags(const int* rp, int n, int* flag) {
-  const int stride = gridDim.x * blockDim.x;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+// rows with edges whose merge items fall in more than one tile
+__global__ void k_split_flags(const int* rp, int n, unsigned char* flag) {
+  GRID_STRIDE(r, n) {
     const long long b = rp[r], e = rp[r + 1];
     const long long ta = (b + r) / kTile, tb = (e + r) / kTile;
     flag[r] = (e > b && ta != tb) ? 1 : 0;
   }
 }
 
-__global__ void k_split_fill(const int* rows, const int* nsel, const int* rp, int4* split) {
-  const int ns = *nsel;
-  const int stride = gridDim.x * blockDim.x;
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += stride) {
+__global__ void k_split_fill(const int* rows, long long ns, const int* rp, int4* split) {
+  GRID_STRIDE(s, ns) {
     const int r = rows[s];
     const long long b = rp[r], e = rp[r + 1];
     split[s] = make_int4(r, (int)((b + r) / kTile), (int)((e + r) / kTile), 0);
   }
 }
 
-// RAII device buffer for temporaries
-struct Tmp {
+// ------------------------------------------------------------------ host helpers
+
+struct Tmp {  // RAII device buffer for temporaries
   void* p = nullptr;
-  ~Tmp() { if (p) cudaFree(p); }
-  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
+  ~Tmp() { reset(); }
+  void reset() { if (p) cudaFree(p); p = nullptr; }
+  cudaError_t alloc(size_t bytes) { reset(); return cudaMalloc(&p, bytes ? bytes : 16); }
   template <class T> T* as() const { return (T*)p; }
 };
 
@@ -219,9 +360,8 @@ int grid_for(long long work, int block, int cap = 148 * 16) {
   } while (0)
 
 int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
-           const double* lam, const double* mu, bool relabel, cudaStream_t s,
-           IngestOut& out, char* msg, size_t msg_len) {
-  (void)relabel;
+           const double* lam, const double* mu, cudaStream_t s, IngestOut& out, char* msg,
+           size_t msg_len) {
   const int N = (int)n, Mm = (int)m;
   Tmp flags;
   IG_CK(flags.alloc(sizeof(int)));
@@ -238,9 +378,11 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
              : (hflags & F_RPN) ? "row_ptr[n] != m" : "is decreasing");
     return PSI_E_GRAPH;
   }
-  IG_CK(cudaMalloc(&out.rp, (size_t)(n + 1) * sizeof(int)));
-  k_rowptr32<<<grid_for(n + 1, 256), 256, 0, s>>>(rp64, out.rp, n + 1);
-  k_check_edges<<<grid_for(n * 32, 256), 256, 0, s>>>(out.rp, idx_in, N, flags.as<int>());
+  Tmp rp_old;
+  IG_CK(rp_old.alloc((size_t)(n + 1) * sizeof(int)));
+  const int* rp = rp_old.as<int>();
+  k_rowptr32<<<grid_for(n + 1, 256), 256, 0, s>>>(rp64, rp_old.as<int>(), n + 1);
+  k_check_edges<<<grid_for(n * 32, 256), 256, 0, s>>>(rp, idx_in, N, flags.as<int>());
   IG_CK(cudaMemcpyAsync(&hflags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   IG_CK(cudaStreamSynchronize(s));
   if (hflags & (F_RANGE | F_SELF | F_ORDER)) {
@@ -254,20 +396,31 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     return PSI_E_ACTIVITY;
   }
 
-  // ---- 2. transpose: leaders of every follower, ascending (stable LSD radix sort)
-  Tmp leader_e, follower_e, leader_s, follower_s, nlead, loff, sort_tmp, scan_tmp;
-  IG_CK(leader_e.alloc((size_t)m * sizeof(int)));
-  IG_CK(follower_e.alloc((size_t)m * sizeof(int)));
-  IG_CK(leader_s.alloc((size_t)m * sizeof(int)));
-  IG_CK(follower_s.alloc((size_t)m * sizeof(int)));
+  // ---- 2.-4. transpose, normalisers, constants (old labels)
+  Tmp a_old, g_old, wt_old, d_old, first_leader, nlead, red;
+  IG_CK(a_old.alloc((size_t)n * sizeof(double)));
+  IG_CK(g_old.alloc((size_t)n * sizeof(double)));
+  IG_CK(wt_old.alloc((size_t)n * sizeof(double)));
+  IG_CK(d_old.alloc((size_t)n * sizeof(double)));
+  IG_CK(first_leader.alloc((size_t)n * sizeof(int)));
   IG_CK(nlead.alloc((size_t)(n + 1) * sizeof(int)));
-  IG_CK(loff.alloc((size_t)(n + 1) * sizeof(int)));
+  IG_CK(red.alloc(16 * sizeof(unsigned long long)));
+  IG_CK(cudaMemsetAsync(red.p, 0, 16 * sizeof(unsigned long long), s));
   IG_CK(cudaMemsetAsync(nlead.p, 0, (size_t)(n + 1) * sizeof(int), s));
-  k_expand<<<grid_for(n * 32, 256), 256, 0, s>>>(out.rp, idx_in, N, leader_e.as<int>(),
-                                                 follower_e.as<int>(), nlead.as<int>());
+  unsigned long long* kmax = red.as<unsigned long long>();
+  unsigned long long* cnt = kmax + 4;
+  unsigned long long* ccount = kmax + 8;     // class counts
   int end_bit = 1;
   while ((1ll << end_bit) < n) ++end_bit;
   {
+    Tmp leader_e, follower_e, leader_s, follower_s, loff, sort_tmp, scan_tmp;
+    IG_CK(leader_e.alloc((size_t)m * sizeof(int)));
+    IG_CK(follower_e.alloc((size_t)m * sizeof(int)));
+    IG_CK(leader_s.alloc((size_t)m * sizeof(int)));
+    IG_CK(follower_s.alloc((size_t)m * sizeof(int)));
+    IG_CK(loff.alloc((size_t)(n + 1) * sizeof(int)));
+    k_expand<<<grid_for(n * 32, 256), 256, 0, s>>>(rp, idx_in, N, leader_e.as<int>(),
+                                                   follower_e.as<int>(), nlead.as<int>());
     cub::DoubleBuffer<unsigned> keys((unsigned*)follower_e.p, (unsigned*)follower_s.p);
     cub::DoubleBuffer<int> vals(leader_e.as<int>(), leader_s.as<int>());
     size_t tb = 0;
@@ -278,66 +431,175 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, nlead.as<int>(), loff.as<int>(), N + 1, s));
     IG_CK(scan_tmp.alloc(sb));
     IG_CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, sb, nlead.as<int>(), loff.as<int>(), N + 1, s));
-
-    // ---- 3./4. normalisers, constants, norms
-    IG_CK(cudaMalloc(&out.a, (size_t)n * sizeof(double)));
-    IG_CK(cudaMalloc(&out.g, (size_t)n * sizeof(double)));
-    IG_CK(cudaMalloc(&out.wt, (size_t)n * sizeof(double)));
-    IG_CK(cudaMalloc(&out.d, (size_t)n * sizeof(double)));
-    IG_CK(cudaMalloc(&out.lam, (size_t)n * sizeof(double)));
-    IG_CK(cudaMemcpyAsync(out.lam, lam, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    Tmp red;
-    IG_CK(red.alloc(8 * sizeof(unsigned long long)));
-    IG_CK(cudaMemsetAsync(red.p, 0, 8 * sizeof(unsigned long long), s));
-    unsigned long long* kmax = red.as<unsigned long long>();
-    unsigned long long* cnt = kmax + 4;
-    k_normalisers<<<grid_for(n * 32, 256), 256, 0, s>>>(loff.as<int>(), vals.Current(), lam, mu,
-                                                        N, out.a, out.g, out.wt, out.d, kmax, cnt);
-    k_kappa_col<<<grid_for(n * 32, 256), 256, 0, s>>>(out.rp, idx_in, out.wt, lam, N, kmax, cnt);
-    unsigned long long h[8];
-    IG_CK(cudaMemcpyAsync(h, red.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-    IG_CK(cudaStreamSynchronize(s));
-    memcpy(&out.kappa_row, &h[0], 8);
-    memcpy(&out.rho_A, &h[1], 8);
-    memcpy(&out.kappa_col, &h[2], 8);
-    out.n_leaderless = (long long)h[4];
-    out.n_f = (long long)h[5];
-    out.n_g = n - out.n_leaderless;
+    k_normalisers<<<grid_for(n * 32, 256), 256, 0, s>>>(
+        loff.as<int>(), vals.Current(), lam, mu, N, a_old.as<double>(), g_old.as<double>(),
+        wt_old.as<double>(), d_old.as<double>(), first_leader.as<int>(), kmax, cnt);
+    k_kappa_col<<<grid_for(n * 32, 256), 256, 0, s>>>(rp, idx_in, wt_old.as<double>(), lam, N, kmax);
   }
 
-  // ---- the sweep's index array (identity labels)
-  IG_CK(cudaMalloc(&out.idx, (size_t)(m > 0 ? m : 1) * sizeof(int)));
-  if (m > 0)
-    IG_CK(cudaMemcpyAsync(out.idx, idx_in, (size_t)m * sizeof(int), cudaMemcpyDeviceToDevice, s));
-  out.relabeled = 0;
+  // ---- 5. relabel
+  Tmp cls, new_of_old, key, sel, flag8, nsel, stage_tmp, sort_tmp2, sorted;
+  IG_CK(cls.alloc((size_t)n));
+  IG_CK(new_of_old.alloc((size_t)n * sizeof(int)));
+  IG_CK(cudaMalloc(&out.old_of_new, (size_t)n * sizeof(int)));
+  k_classify<<<grid_for(n, 256), 256, 0, s>>>(rp, nlead.as<int>(), N, cls.as<unsigned char>(),
+                                              new_of_old.as<int>(), ccount);
+  unsigned long long h[16];
+  IG_CK(cudaMemcpyAsync(h, red.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  IG_CK(cudaStreamSynchronize(s));
+  memcpy(&out.kappa_row, &h[0], 8);
+  memcpy(&out.rho_A, &h[1], 8);
+  memcpy(&out.kappa_col, &h[2], 8);
+  out.n_leaderless = (long long)h[4];
+  out.n_g = n - out.n_leaderless;
+  const long long n_inactive = (long long)h[8 + C_INACTIVE];
+  out.n_act = n - n_inactive;
+  out.n_f = out.n_act;
+  out.n_hot = (long long)h[8 + C_HOT];
 
-  // ---- 5. merge-path tiles and split rows
-  const long long items = n + m;
+  IG_CK(key.alloc((size_t)n * 8));
+  IG_CK(sel.alloc((size_t)n * 8));
+  IG_CK(sorted.alloc((size_t)n * 8));
+  IG_CK(flag8.alloc((size_t)n));
+  IG_CK(nsel.alloc(sizeof(long long)));
+  size_t sel_bytes = 0, sort_bytes = 0;
+  IG_CK(cub::DeviceSelect::Flagged(nullptr, sel_bytes, key.as<unsigned long long>(),
+                                   flag8.as<unsigned char>(), sel.as<unsigned long long>(),
+                                   nsel.as<long long>(), N, s));
+  IG_CK(stage_tmp.alloc(sel_bytes));
+  IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, sel.as<unsigned long long>(),
+                                       sorted.as<unsigned long long>(), N, 0, 64, s));
+  IG_CK(sort_tmp2.alloc(sort_bytes));
+  int base = 0;
+  int levels = 0;
+  auto run_stage = [&](int stage, bool sort_keys, long long* count) -> int {
+    k_stage_keys<<<grid_for(n, 256), 256, 0, s>>>(stage, cls.as<unsigned char>(), nlead.as<int>(),
+                                                  first_leader.as<int>(), new_of_old.as<int>(), N,
+                                                  key.as<unsigned long long>(),
+                                                  flag8.as<unsigned char>());
+    size_t b1 = sel_bytes;
+    IG_CK(cub::DeviceSelect::Flagged(stage_tmp.p, b1, key.as<unsigned long long>(),
+                                     flag8.as<unsigned char>(), sel.as<unsigned long long>(),
+                                     nsel.as<long long>(), N, s));
+    long long c = 0;
+    IG_CK(cudaMemcpyAsync(&c, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+    *count = c;
+    if (c == 0) return PSI_OK;
+    const unsigned long long* src = sel.as<unsigned long long>();
+    if (sort_keys) {
+      size_t b2 = sort_bytes;
+      IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp2.p, b2, sel.as<unsigned long long>(),
+                                           sorted.as<unsigned long long>(), (int)c, 0, 64, s));
+      src = sorted.as<unsigned long long>();
+    }
+    k_assign<<<grid_for(c, 256), 256, 0, s>>>(src, c, base, new_of_old.as<int>(), out.old_of_new);
+    base += (int)c;
+    return PSI_OK;
+  };
+  long long c = 0;
+  int rc;
+  if ((rc = run_stage(0, true, &c)) != PSI_OK) return rc;          // hot, by leader count
+  if ((rc = run_stage(1, false, &c)) != PSI_OK) return rc;         // leaderless active
+  while (true) {                                                   // single-leader, by level
+    if ((rc = run_stage(2, true, &c)) != PSI_OK) return rc;
+    if (c == 0) break;
+    ++levels;
+  }
+  if ((rc = run_stage(3, true, &c)) != PSI_OK) return rc;          // leftovers (cycles)
+  if (base != out.n_act) {
+    snprintf(msg, msg_len, "internal: relabel covered %d of %lld active users", base, out.n_act);
+    return PSI_E_CUDA;
+  }
+  if ((rc = run_stage(4, false, &c)) != PSI_OK) return rc;         // follower-less
+  out.relabel_levels = levels;
+  key.reset(); sel.reset(); sorted.reset(); flag8.reset(); stage_tmp.reset(); sort_tmp2.reset();
+
+  // ---- 6. relabelled CSR over active rows, folded constants
+  const int NA = (int)out.n_act;
+  Tmp cntr, K;
+  IG_CK(cntr.alloc((size_t)(NA + 1) * sizeof(int)));
+  IG_CK(K.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(double)));
+  IG_CK(cudaMemsetAsync(cntr.p, 0, (size_t)(NA + 1) * sizeof(int), s));
+  IG_CK(cudaMalloc(&out.rp, (size_t)(NA + 1) * sizeof(int)));
+  if (NA > 0)
+    k_row_count<<<grid_for((long long)NA * 32, 256), 256, 0, s>>>(
+        rp, idx_in, out.old_of_new, cls.as<unsigned char>(), a_old.as<double>(), NA,
+        cntr.as<int>(), K.as<double>());
+  {
+    Tmp scan_tmp;
+    size_t sb = 0;
+    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cntr.as<int>(), out.rp, NA + 1, s));
+    IG_CK(scan_tmp.alloc(sb));
+    IG_CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, sb, cntr.as<int>(), out.rp, NA + 1, s));
+  }
+  int m_act = 0;
+  IG_CK(cudaMemcpyAsync(&m_act, out.rp + NA, sizeof(int), cudaMemcpyDeviceToHost, s));
+  IG_CK(cudaStreamSynchronize(s));
+  out.m_act = m_act;
+  {
+    Tmp idx2, seg_tmp;
+    IG_CK(cudaMalloc(&out.idx, (size_t)(m_act > 0 ? m_act : 1) * sizeof(int)));
+    IG_CK(idx2.alloc((size_t)(m_act > 0 ? m_act : 1) * sizeof(int)));
+    if (NA > 0)
+      k_row_fill<<<grid_for((long long)NA * 32, 256), 256, 0, s>>>(
+          rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(), out.rp, NA,
+          out.idx);
+    if (m_act > 0) {
+      cub::DoubleBuffer<int> kb(out.idx, idx2.as<int>());
+      size_t tb = 0;
+      IG_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, kb, m_act, NA, out.rp, out.rp + 1, s));
+      IG_CK(seg_tmp.alloc(tb));
+      IG_CK(cub::DeviceSegmentedSort::SortKeys(seg_tmp.p, tb, kb, m_act, NA, out.rp, out.rp + 1, s));
+      if (kb.Current() != out.idx)
+        IG_CK(cudaMemcpyAsync(out.idx, kb.Current(), (size_t)m_act * sizeof(int),
+                              cudaMemcpyDeviceToDevice, s));
+    }
+    IG_CK(cudaStreamSynchronize(s));
+  }
+  const size_t na_b = (size_t)(NA > 0 ? NA : 1) * sizeof(double);
+  IG_CK(cudaMalloc(&out.a0, (size_t)n * sizeof(double)));
+  IG_CK(cudaMalloc(&out.wt, (size_t)n * sizeof(double)));
+  IG_CK(cudaMalloc(&out.psi, (size_t)n * sizeof(double)));
+  IG_CK(cudaMalloc(&out.a1, na_b));
+  IG_CK(cudaMalloc(&out.g, na_b));
+  IG_CK(cudaMalloc(&out.d1, na_b));
+  IG_CK(cudaMalloc(&out.lam, na_b));
+  k_permute_vectors<<<grid_for(n, 256), 256, 0, s>>>(
+      out.old_of_new, N, NA, a_old.as<double>(), g_old.as<double>(), wt_old.as<double>(),
+      d_old.as<double>(), lam, K.as<double>(), (double)n, out.a0, out.a1, out.g, out.wt, out.d1,
+      out.lam, out.psi);
+  out.relabeled = 1;
+
+  // ---- 7. merge-path tiles and split rows (over the n_act x m_act CSR)
+  const long long items = (long long)NA + m_act;
   out.ntiles = (int)((items + kTile - 1) / kTile);
   IG_CK(cudaMalloc(&out.tile_coord, (size_t)(out.ntiles + 1) * sizeof(int2)));
-  k_tile_coords<<<grid_for(out.ntiles + 1, 256), 256, 0, s>>>(out.rp, N, Mm, out.ntiles,
+  k_tile_coords<<<grid_for(out.ntiles + 1, 256), 256, 0, s>>>(out.rp, NA, m_act, out.ntiles,
                                                               out.tile_coord);
   {
-    Tmp flag, rows, nsel, sel_tmp;
-    IG_CK(flag.alloc((size_t)n * sizeof(int)));
-    IG_CK(rows.alloc((size_t)n * sizeof(int)));
-    IG_CK(nsel.alloc(sizeof(int)));
-    k_split_flags<<<grid_for(n, 256), 256, 0, s>>>(out.rp, N, flag.as<int>());
-    cub::CountingInputIterator<int> it(0);
-    size_t tb = 0;
-    IG_CK(cub::DeviceSelect::Flagged(nullptr, tb, it, flag.as<int>(), rows.as<int>(),
-                                     nsel.as<int>(), N, s));
-    IG_CK(sel_tmp.alloc(tb));
-    IG_CK(cub::DeviceSelect::Flagged(sel_tmp.p, tb, it, flag.as<int>(), rows.as<int>(),
-                                     nsel.as<int>(), N, s));
-    int hs = 0;
-    IG_CK(cudaMemcpyAsync(&hs, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-    IG_CK(cudaStreamSynchronize(s));
-    out.nsplit = hs;
+    Tmp fl, rows, ns, sel_tmp;
+    IG_CK(fl.alloc((size_t)(NA > 0 ? NA : 1)));
+    IG_CK(rows.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(int)));
+    IG_CK(ns.alloc(sizeof(long long)));
+    IG_CK(cudaMemsetAsync(ns.p, 0, sizeof(long long), s));
+    long long hs = 0;
+    if (NA > 0) {
+      k_split_flags<<<grid_for(NA, 256), 256, 0, s>>>(out.rp, NA, fl.as<unsigned char>());
+      cub::CountingInputIterator<int> it(0);
+      size_t tb = 0;
+      IG_CK(cub::DeviceSelect::Flagged(nullptr, tb, it, fl.as<unsigned char>(), rows.as<int>(),
+                                       ns.as<long long>(), NA, s));
+      IG_CK(sel_tmp.alloc(tb));
+      IG_CK(cub::DeviceSelect::Flagged(sel_tmp.p, tb, it, fl.as<unsigned char>(), rows.as<int>(),
+                                       ns.as<long long>(), NA, s));
+      IG_CK(cudaMemcpyAsync(&hs, ns.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+      IG_CK(cudaStreamSynchronize(s));
+    }
+    out.nsplit = (int)hs;
     IG_CK(cudaMalloc(&out.split, (size_t)(hs > 0 ? hs : 1) * sizeof(int4)));
     if (hs > 0)
-      k_split_fill<<<grid_for(hs, 256), 256, 0, s>>>(rows.as<int>(), nsel.as<int>(), out.rp,
-                                                     out.split);
+      k_split_fill<<<grid_for(hs, 256), 256, 0, s>>>(rows.as<int>(), hs, out.rp, out.split);
     IG_CK(cudaStreamSynchronize(s));
   }
   IG_CK(cudaGetLastError());

@@ -50,12 +50,14 @@ struct SweepArgs {
   int nsplit;
   double* piece_first;       // per tile: partial sum of the tile's first row
   double* piece_last;        // per tile: partial sum of the tile's trailing (unfinished) row
-  const double* a;
-  const double* g;
-  const double* wt;
-  const double* d;
-  const double* lam;
-  double inv_n;
+  const double* a0;          // x_0 (init) [n_act used]
+  const double* a;           // sweep constant a + g K        [n_act]
+  const double* g;           //                                [n_act]
+  const double* wt;          // Wt                             [n]
+  const double* d;           // readout constant d + lambda K  [n_act]
+  const double* lam;         //                                [n_act]
+  double n_users;            // N of psi = (...)/N
+  int n_act;
   double* psi;               // readout output (relabelled order)
   double* x0;
   double* x1;
@@ -76,15 +78,25 @@ void* init_kernel_ptr();
 size_t sweep_smem_bytes();
 
 // ---- ingest (psi_ingest.cu)
+// Device arrays in the NEW (relabelled) user order; active users [0, n_act) have >= 1
+// follower, follower-less users [n_act, n) never change (x = a0, psi = d/N).
 struct IngestOut {
-  int* rp = nullptr;         // [n+1]
-  int* idx = nullptr;        // [m]
-  double *a = nullptr, *g = nullptr, *wt = nullptr, *d = nullptr, *lam = nullptr;
-  int* old_of_new = nullptr; // [n] (relabel); nullptr = identity
+  int* rp = nullptr;          // [n_act+1] CSR over active rows
+  int* idx = nullptr;         // [m_act]   active followers, new labels, ascending per row
+  double* a0 = nullptr;       // [n]     x_0 = c / Wt
+  double* a1 = nullptr;       // [n_act] sweep constant a + g K (K: folded follower-less terms)
+  double* g = nullptr;        // [n_act] mu / Wt
+  double* wt = nullptr;       // [n]     Wt (s = Wt x)
+  double* d1 = nullptr;       // [n_act] readout constant d + lambda K
+  double* lam = nullptr;      // [n_act]
+  double* psi = nullptr;      // [n]     readout buffer; [n_act, n) prefilled with d/N
+  int* old_of_new = nullptr;  // [n]
   int2* tile_coord = nullptr;
   int ntiles = 0;
   int4* split = nullptr;
   int nsplit = 0;
+  long long n_act = 0, m_act = 0, n_hot = 0;
+  int relabel_levels = 0;
   double kappa_row = 0, kappa_col = 0, rho_A = 0;
   long long n_f = 0, n_g = 0, n_leaderless = 0;
   int relabeled = 0;
@@ -92,7 +104,7 @@ struct IngestOut {
 
 // Returns 0 or a negative psi_status; msg gets a description on error.
 int ingest(long long n, long long m, const long long* rp64_dev, const int* idx_dev,
-           const double* lam_dev, const double* mu_dev, bool relabel, cudaStream_t s,
-           IngestOut& out, char* msg, size_t msg_len);
+           const double* lam_dev, const double* mu_dev, cudaStream_t s, IngestOut& out,
+           char* msg, size_t msg_len);
 
 }  // namespace psi

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_tiles(SweepArgs A) {
       const int r = r0 + ii;
       const double Sr = sm.rowsum[ii];
       if (READOUT) {
-        A.psi[r] = (__ldg(A.d + r) + __ldg(A.lam + r) * Sr) * A.inv_n;
+        A.psi[r] = (__ldg(A.d + r) + __ldg(A.lam + r) * Sr) / A.n_users;
       } else {
         const double xn = fma(__ldg(A.g + r), Sr, __ldg(A.a + r));
         eps_acc += __ldg(A.wt + r) * fabs(xn - xs[r]);
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
     for (int k = sp.y; k <= sp.z; ++k)
       S += (A.tile_coord[k].x == r) ? A.piece_first[k] : A.piece_last[k];
     if (READOUT) {
-      A.psi[r] = (A.d[r] + A.lam[r] * S) * A.inv_n;
+      A.psi[r] = (A.d[r] + A.lam[r] * S) / A.n_users;
     } else {
       const double xn = fma(A.g[r], S, A.a[r]);
       eps_acc += A.wt[r] * fabs(xn - xs[r]);
@@ -232,9 +232,10 @@ __global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
 }
 
 // x_0 = a (s_0 = c, Alg. 2 line 1), t = 0, gap = 1 (line 4), WHILE condition = (1 > eps).
+// Only active users are reset: follower-less users hold x = a0 in both buffers forever.
 __global__ void k_init(SweepArgs A, int n) {
   const int stride = gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) A.x0[i] = A.a[i];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n_act; i += stride) A.x0[i] = A.a0[i];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.st->iter = 0;
     A.st->gap = 1.0;
