@@ -299,20 +299,10 @@ def run_ours(args, ws, rank, local):
     value = edges_all / (ms_total * 1e-3) / 1e9
     launches = sum(2 * t + 3 for t in Ts)
 
-    # ---- per-sweep time (differential fixed-count runs: eps = 0, K2 - K1 sweeps)
-    def solve_ms(k):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        g.iterate(0.0, k)
-        b.record(stream)
-        torch.cuda.synchronize()
-        return a.elapsed_time(b)
-
-    k1, k2 = 5, 25
-    diffs = []
-    for _ in range(3):
-        diffs.append((solve_ms(k2) - solve_ms(k1)) / (k2 - k1))
-    sweep_ms = statistics.median(diffs)
+    # ---- per-launch device time of the sweep kernels: CUDA events on the library's stream
+    # around every k_tiles / k_fix launch (psi_time_sweep, direct launches, 20 sweeps)
+    tiles_ms, fix_ms = g.time_sweep(20)
+    sweep_ms = tiles_ms + fix_ms
     g.iterate(eps)   # leave the context at the eps solution
 
     # ---- e2e through the C-ABI with host (pinned) buffers
@@ -348,8 +338,9 @@ def run_ours(args, ws, rank, local):
     achieved = bsweep / (sweep_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": _traffic_from_profiles("k_tiles", args.config),
-            "kernel": "sweep = k_tiles<sweep> + k_fix<sweep> (marginal time per sweep, "
-                      "differential fixed-count runs K=25 vs K=5)",
+            "kernel": "one sweep = k_tiles<sweep> + k_fix<sweep>; each launch timed with CUDA "
+                      "events on the library stream (psi_time_sweep, 20 sweeps)",
+            "k_tiles_ms": round(tiles_ms, 4), "k_fix_ms": round(fix_ms, 4),
             "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
             "algorithmic_bytes_per_sweep": bsweep,
             "sweep_ms": round(sweep_ms, 4), "sweep_gteps": round(m / (sweep_ms * 1e-3) / 1e9, 2),

@@ -138,6 +138,14 @@ psi_status psi_get_series(const psi_ctx* ctx, double* out, int mem_kind);
 psi_status psi_get_residual_history(const psi_ctx* ctx, double* out, int64_t cap,
                                     int64_t* len_out);
 
+/* psi_time_sweep -- measurement entry: runs `sweeps` sweeps of Eq. (14) from s_0 = c
+ * (eps = 0) as direct stream launches and returns the average device time of the
+ * sweep's two kernels, each bracketed by CUDA events on the context's stream:
+ * *tiles_ms = merge-path gather + epilogue (k_tiles), *fix_ms = split rows + eps_t
+ * reduction + stop rule (k_fix).  Leaves no psi (call psi_iterate afterwards).
+ * PSI_E_INVALID_ARG if ctx is NULL or sweeps < 1. */
+psi_status psi_time_sweep(psi_ctx* ctx, int64_t sweeps, double* tiles_ms, double* fix_ms);
+
 /* psi_get_info -- sizes, norms and timings (see psi_info). */
 psi_status psi_get_info(const psi_ctx* ctx, psi_info* out);
 

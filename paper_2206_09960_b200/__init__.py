@@ -39,7 +39,8 @@ _STATUS_NAMES = {0: "PSI_OK", 1: "PSI_NOT_CONVERGED", -1: "PSI_E_INVALID_ARG", -
                  -7: "PSI_E_NUMERIC"}
 
 EXPORTED = ["psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
-            "psi_get_residual_history", "psi_get_info", "psi_destroy", "psi_last_error"]
+            "psi_get_residual_history", "psi_time_sweep", "psi_get_info", "psi_destroy",
+            "psi_last_error"]
 
 
 class PsiError(RuntimeError):
@@ -84,11 +85,12 @@ def load_library(build_if_stale: bool = True):
     lib.psi_get_series.argtypes = [vp, vp, ci]
     lib.psi_get_residual_history.argtypes = [vp, vp, i64, ctypes.POINTER(i64)]
     lib.psi_get_info.argtypes = [vp, ctypes.POINTER(psi_info)]
+    lib.psi_time_sweep.argtypes = [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
     lib.psi_destroy.argtypes = [vp]
     lib.psi_destroy.restype = None
     lib.psi_last_error.restype = ctypes.c_char_p
     for f in ("psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
-              "psi_get_residual_history", "psi_get_info"):
+              "psi_get_residual_history", "psi_get_info", "psi_time_sweep"):
         getattr(lib, f).restype = ci
     _lib = lib
     return lib
@@ -183,6 +185,14 @@ class PsiGraph:
             if st != PSI_OK:
                 raise PsiError(st, _err(self._lib))
         return out
+
+    def time_sweep(self, sweeps: int = 20):
+        """(k_tiles ms, k_fix ms): average per-launch device time over `sweeps` sweeps."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        st = self._lib.psi_time_sweep(self._ctx, int(sweeps), ctypes.byref(a), ctypes.byref(b))
+        if st != PSI_OK:
+            raise PsiError(st, _err(self._lib))
+        return a.value, b.value
 
     def info(self) -> dict:
         inf = psi_info()

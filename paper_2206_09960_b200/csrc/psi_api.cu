@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -119,6 +120,7 @@ SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   A.st = c->st;
   A.prm = c->prm;
   A.cond = cond;
+  A.use_cond = 1;
   return A;
 }
 
@@ -161,6 +163,42 @@ psi_status build_graph_exec(psi_ctx* c) {
   API_CK(add_kernel(c->graph, &n_r2, &n_r1, 1, fix_kernel_ptr(true), c->grid2, kFixBlock, &A, nullptr));
   API_CK(cudaGraphInstantiate(&c->exec, c->graph, 0));
   return PSI_OK;
+}
+
+cudaError_t launch(void* fn, int grid, int block, SweepArgs* A, int* extra, cudaStream_t s) {
+  void* kp[2] = {A, extra};
+  return cudaLaunchKernel(fn, dim3(grid), dim3(block), kp, 0, s);
+}
+
+// Direct stream launches of the same kernels (no CUDA graph, no conditional node): used by
+// psi_time_sweep and, with PSI_GRAPH=0, by psi_iterate (profilers cannot see kernel nodes
+// of graphs with conditional nodes).  The stop rule is evaluated on the host after every
+// sweep from the device LoopState, exactly as the graph's WHILE condition does.
+psi_status iterate_direct(psi_ctx* c) {
+  SweepArgs A = make_args(c, 0);
+  A.use_cond = 0;
+  int n_int = (int)c->n;
+  int init_grid = (int)std::min<long long>((c->g.n_act + 255) / 256, 148LL * 8);
+  if (init_grid < 1) init_grid = 1;
+  API_CK(launch(init_kernel_ptr(), init_grid, 256, &A, &n_int, c->stream));
+  const double eps = c->h_prm->eps;
+  const long long max_iters = c->h_prm->max_iters;
+  bool cont = 1.0 > eps && max_iters > 0;
+  while (cont) {
+    API_CK(launch(sweep_kernel_ptr(false), c->grid1, kBlock, &A, nullptr, c->stream));
+    API_CK(launch(fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr, c->stream));
+    API_CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(LoopState), cudaMemcpyDeviceToHost, c->stream));
+    API_CK(cudaStreamSynchronize(c->stream));
+    cont = !(c->h_st->status & 1) && c->h_st->gap > eps && c->h_st->iter < max_iters;
+  }
+  API_CK(launch(sweep_kernel_ptr(true), c->grid1, kBlock, &A, nullptr, c->stream));
+  API_CK(launch(fix_kernel_ptr(true), c->grid2, kFixBlock, &A, nullptr, c->stream));
+  return PSI_OK;
+}
+
+bool use_graph() {
+  const char* e = getenv("PSI_GRAPH");
+  return !(e && e[0] == '0');
 }
 
 psi_status ensure_history(psi_ctx* c, long long need) {
@@ -333,7 +371,12 @@ psi_status psi_iterate(psi_ctx* c, double eps, int64_t max_iters, int norm, int6
   c->h_prm->hist_cap = c->hist_cap;
   API_CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(LoopParams), cudaMemcpyHostToDevice, c->stream));
   API_CK(cudaEventRecord(c->ev0, c->stream));
-  API_CK(cudaGraphLaunch(c->exec, c->stream));
+  if (use_graph()) {
+    API_CK(cudaGraphLaunch(c->exec, c->stream));
+  } else {
+    psi_status ds = iterate_direct(c);
+    if (ds != PSI_OK) return ds;
+  }
   API_CK(cudaEventRecord(c->ev1, c->stream));
   API_CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(LoopState), cudaMemcpyDeviceToHost, c->stream));
   API_CK(cudaStreamSynchronize(c->stream));
@@ -410,6 +453,49 @@ psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
   out->grid = c->grid1;
   out->device_bytes = (int64_t)c->device_bytes;
   out->relabeled = c->g.relabeled;
+  return PSI_OK;
+}
+
+psi_status psi_time_sweep(psi_ctx* c, int64_t sweeps, double* tiles_ms, double* fix_ms) {
+  g_err.clear();
+  if (!c || sweeps < 1) return fail(PSI_E_INVALID_ARG, "ctx NULL or sweeps < 1");
+  psi_status hs = ensure_history(c, sweeps);
+  if (hs != PSI_OK) return hs;
+  c->h_prm->eps = 0.0;
+  c->h_prm->max_iters = sweeps;
+  c->h_prm->kappa = c->g.kappa_row;
+  c->h_prm->history = c->history;
+  c->h_prm->hist_cap = c->hist_cap;
+  API_CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(LoopParams), cudaMemcpyHostToDevice, c->stream));
+  SweepArgs A = make_args(c, 0);
+  A.use_cond = 0;
+  int n_int = (int)c->n;
+  int init_grid = (int)std::min<long long>((c->g.n_act + 255) / 256, 148LL * 8);
+  if (init_grid < 1) init_grid = 1;
+  API_CK(launch(init_kernel_ptr(), init_grid, 256, &A, &n_int, c->stream));
+  cudaEvent_t e[3];
+  for (auto& x : e) API_CK(cudaEventCreate(&x));
+  double t1 = 0, t2 = 0;
+  psi_status rc = PSI_OK;
+  for (int64_t k = 0; k < sweeps && rc == PSI_OK; ++k) {
+    float a = 0, b = 0;
+    if (cudaEventRecord(e[0], c->stream) != cudaSuccess ||
+        launch(sweep_kernel_ptr(false), c->grid1, kBlock, &A, nullptr, c->stream) != cudaSuccess ||
+        cudaEventRecord(e[1], c->stream) != cudaSuccess ||
+        launch(fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr, c->stream) != cudaSuccess ||
+        cudaEventRecord(e[2], c->stream) != cudaSuccess ||
+        cudaEventSynchronize(e[2]) != cudaSuccess ||
+        cudaEventElapsedTime(&a, e[0], e[1]) != cudaSuccess ||
+        cudaEventElapsedTime(&b, e[1], e[2]) != cudaSuccess)
+      rc = fail(PSI_E_CUDA, "psi_time_sweep: %s", cudaGetErrorString(cudaGetLastError()));
+    t1 += a;
+    t2 += b;
+  }
+  for (auto& x : e) cudaEventDestroy(x);
+  if (rc != PSI_OK) return rc;
+  c->have_psi = false;     // the iterate state is mid-solve: require a new psi_iterate
+  if (tiles_ms) *tiles_ms = t1 / sweeps;
+  if (fix_ms) *fix_ms = t2 / sweeps;
   return PSI_OK;
 }
 

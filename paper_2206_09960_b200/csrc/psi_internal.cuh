@@ -67,6 +67,7 @@ struct SweepArgs {
   LoopState* st;
   const LoopParams* prm;
   cudaGraphConditionalHandle cond;
+  int use_cond;              // 1 inside the CUDA graph; 0 for direct stream launches
 };
 
 // ---- launchers (psi_sweep.cu)

@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
     A.st->done = 0;
     if (bad) A.st->status |= 1;
     const unsigned cont = (!bad && gap > P.eps && t + 1 < P.max_iters) ? 1u : 0u;
-    cudaGraphSetConditional(A.cond, cont);
+    if (A.use_cond) cudaGraphSetConditional(A.cond, cont);
   }
 }
 
@@ -243,7 +243,7 @@ __global__ void k_init(SweepArgs A, int n) {
     A.st->done = 0;
     A.st->status = 0;
     const LoopParams P = *A.prm;
-    cudaGraphSetConditional(A.cond, (1.0 > P.eps && P.max_iters > 0) ? 1u : 0u);
+    if (A.use_cond) cudaGraphSetConditional(A.cond, (1.0 > P.eps && P.max_iters > 0) ? 1u : 0u);
   }
 }
 
