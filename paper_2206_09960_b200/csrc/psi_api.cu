@@ -53,8 +53,8 @@ struct psi_ctx {
   cudaStream_t stream = nullptr;
   IngestOut g;
   double* x[2] = {nullptr, nullptr};
-  double* piece_first = nullptr;
-  double* piece_last = nullptr;
+  double* p_in = nullptr;        // per tile: partial of the row open at the tile start
+  double* p_out = nullptr;       // per tile: partial of its last row if that row continues
   double* eps_part1 = nullptr;
   double* eps_part2 = nullptr;
   double* history = nullptr;
@@ -72,6 +72,7 @@ struct psi_ctx {
   double last_gap = 1.0;
   double ingest_ms = 0, iterate_ms = 0;
   size_t device_bytes = 0;
+  long long hot_lim = 0;         // x labels kept in L2 with evict_last (both buffers)
 };
 
 namespace {
@@ -80,10 +81,9 @@ void free_ctx(psi_ctx* c) {
   if (!c) return;
   if (c->exec) cudaGraphExecDestroy(c->exec);
   if (c->graph) cudaGraphDestroy(c->graph);
-  void* ptrs[] = {c->g.rp, c->g.idx, c->g.a0, c->g.a1, c->g.g, c->g.wt, c->g.d1, c->g.lam,
-                  c->g.psi, c->g.old_of_new, c->g.tile_coord, c->g.split, c->x[0], c->x[1],
-                  c->piece_first, c->piece_last, c->eps_part1, c->eps_part2, c->history,
-                  c->st, c->prm};
+  void* ptrs[] = {c->g.edges, c->g.tile_row, c->g.a0, c->g.a1, c->g.g, c->g.wt, c->g.d1,
+                  c->g.lam, c->g.psi, c->g.old_of_new, c->g.split, c->x[0], c->x[1],
+                  c->p_in, c->p_out, c->eps_part1, c->eps_part2, c->history, c->st, c->prm};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -95,14 +95,13 @@ void free_ctx(psi_ctx* c) {
 
 SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   SweepArgs A{};
-  A.rp = c->g.rp;
-  A.idx = c->g.idx;
-  A.tile_coord = c->g.tile_coord;
+  A.edges = c->g.edges;
+  A.tile_row = c->g.tile_row;
   A.ntiles = c->g.ntiles;
   A.split = c->g.split;
   A.nsplit = c->g.nsplit;
-  A.piece_first = c->piece_first;
-  A.piece_last = c->piece_last;
+  A.p_in = c->p_in;
+  A.p_out = c->p_out;
   A.a0 = c->g.a0;
   A.a = c->g.a1;
   A.g = c->g.g;
@@ -111,6 +110,7 @@ SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   A.lam = c->g.lam;
   A.n_users = (double)c->n;
   A.n_act = (int)c->g.n_act;
+  A.hot_lim = (int)c->hot_lim;
   A.psi = c->g.psi;
   A.x0 = c->x[0];
   A.x1 = c->x[1];
@@ -318,11 +318,28 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
 
   // Iteration buffers.
   c->grid1 = sweep_grid(c->g.ntiles);
+  {
+    // Hot prefix of x kept in L2 (evict_last) in BOTH ping-pong buffers: PSI_HOT_MB per
+    // buffer (default: a third of L2 each), never more than the users with >= 2 leaders.
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    double hot_mb = l2 / 3.0 / (1 << 20);
+    if (const char* e = getenv("PSI_HOT_MB")) hot_mb = atof(e);
+    long long lim = (long long)(hot_mb * (1 << 20) / 8.0);
+    c->hot_lim = std::min<long long>(std::max<long long>(lim, 0), c->g.n_hot);
+    // Random 8-byte gathers: ask L2 to fetch single 32-byte sectors from DRAM.
+    int fetch = 32;
+    if (const char* e = getenv("PSI_L2_FETCH")) fetch = atoi(e);
+    if (fetch > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)fetch);
+  }
   c->grid2 = fix_grid(c->g.nsplit);
-  B_CK(cudaMalloc(&c->x[0], n * sizeof(double)));
-  B_CK(cudaMalloc(&c->x[1], n * sizeof(double)));
-  B_CK(cudaMalloc(&c->piece_first, (c->g.ntiles + 1) * sizeof(double)));
-  B_CK(cudaMalloc(&c->piece_last, (c->g.ntiles + 1) * sizeof(double)));
+  B_CK(cudaMalloc(&c->x[0], (n + 1) * sizeof(double)));      // + sentinel x[n] = 0
+  B_CK(cudaMalloc(&c->x[1], (n + 1) * sizeof(double)));
+  B_CK(cudaMemsetAsync(c->x[0] + n, 0, sizeof(double), c->stream));
+  B_CK(cudaMemsetAsync(c->x[1] + n, 0, sizeof(double), c->stream));
+  B_CK(cudaMalloc(&c->p_in, (c->g.ntiles + 1) * sizeof(double)));
+  B_CK(cudaMalloc(&c->p_out, (c->g.ntiles + 1) * sizeof(double)));
   B_CK(cudaMalloc(&c->eps_part1, c->grid1 * sizeof(double)));
   B_CK(cudaMalloc(&c->eps_part2, c->grid2 * sizeof(double)));
   B_CK(cudaMalloc(&c->st, sizeof(LoopState)));
@@ -338,8 +355,8 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   float ms = 0;
   B_CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   c->ingest_ms = ms;
-  c->device_bytes = (c->g.n_act + 1) * 4 + c->g.m_act * 4 + 6 * n * 8 + 4 * c->g.n_act * 8 +
-                    (c->g.ntiles + 1) * (8 + 16) + (long long)c->g.nsplit * 16 + n * 4;
+  c->device_bytes = (long long)c->g.ntiles * kTile * 4 + 6 * n * 8 + 4 * c->g.n_act * 8 +
+                    (c->g.ntiles + 1) * (4 + 16) + (long long)c->g.nsplit * 16 + n * 4;
 
   psi_status gs = build_graph_exec(c);
   if (gs != PSI_OK) return bail(gs);

@@ -250,19 +250,21 @@ __global__ void k_row_count(const int* rp, const int* idx, const int* old_of_new
     c = __reduce_add_sync(kFull, c);
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) k += __shfl_xor_sync(kFull, k, s);
-    if (lane == 0) { cnt[r] = c; K[r] = k; }
+    if (lane == 0) { cnt[r] = c > 0 ? c : 1; K[r] = k; }   // 0 -> one pseudo edge
   }
 }
 
-// warp per new active row: write the active followers' new labels (unsorted, stable)
+// warp per new active row: write the active followers' new labels (unsorted, stable); a row
+// with no active follower gets one pseudo edge to the sentinel label n (x[n] = 0).
 __global__ void k_row_fill(const int* rp, const int* idx, const int* old_of_new,
                            const unsigned char* cls, const int* new_of_old, const int* rp_new,
-                           int n_act, int* idx_new) {
+                           int n_act, int n, int* idx_new) {
   const int lane = threadIdx.x & 31;
   WARP_STRIDE(r, n_act) {
     const int o = old_of_new[r];
     const int b = rp[o], e = rp[o + 1];
-    int out = rp_new[r];
+    const int start = rp_new[r];
+    int out = start;
     for (int q0 = b; q0 < e; q0 += 32) {
       const int q = q0 + lane;
       int v = -1;
@@ -272,7 +274,15 @@ __global__ void k_row_fill(const int* rp, const int* idx, const int* old_of_new,
       if (act) idx_new[out + __popc(mask & ((1u << lane) - 1u))] = new_of_old[v];
       out += __popc(mask);
     }
+    if (lane == 0 && out == start) idx_new[start] = n;
   }
+}
+
+// flag the first word of every row; pad [m_act, m_pad) with unflagged sentinel words
+__global__ void k_flag_rows(const int* rp_new, int n_act, long long m_act, long long m_pad, int n,
+                            unsigned* edges) {
+  GRID_STRIDE(r, n_act) edges[rp_new[r]] |= kRowFlag;
+  GRID_STRIDE(q, m_pad - m_act) edges[m_act + q] = (unsigned)n;
 }
 
 __global__ void k_permute_vectors(const int* old_of_new, int n, int n_act, const double* a_old,
@@ -296,37 +306,30 @@ __global__ void k_permute_vectors(const int* old_of_new, int n, int n_act, const
   }
 }
 
-// ------------------------------------------------------------------ 6. tiles
+// ------------------------------------------------------------------ 7. tiles
 
-// merge-path coordinate (row, edge) of diagonal k*kTile: a = row ends rp[1..n], b = 0..m-1
-__global__ void k_tile_coords(const int* rp, int n, int m, int ntiles, int2* tc) {
+// tile_row[k] = number of rows whose first edge lies before edge k*kTile
+__global__ void k_tile_rows(const int* rp, int n_act, int ntiles, int* tile_row) {
   GRID_STRIDE(k, ntiles + 1) {
-    long long diag = k * (long long)kTile;
-    if (diag > (long long)n + m) diag = (long long)n + m;
-    long long lo = diag - m > 0 ? diag - m : 0;
-    long long hi = diag < n ? diag : n;
+    const long long e = k * (long long)kTile;
+    int lo = 0, hi = n_act;                 // first row r with rp[r] >= e
     while (lo < hi) {
-      const long long mid = (lo + hi) >> 1;
-      if ((long long)rp[mid + 1] <= diag - mid - 1) lo = mid + 1; else hi = mid;
+      const int mid = (lo + hi) >> 1;
+      if ((long long)rp[mid] < e) lo = mid + 1; else hi = mid;
     }
-    tc[k] = make_int2((int)lo, (int)(diag - lo));
+    tile_row[k] = lo;
   }
 }
 
-// rows with edges whose merge items fall in more than one tile
+// rows whose edges fall in more than one tile
 __global__ void k_split_flags(const int* rp, int n, unsigned char* flag) {
-  GRID_STRIDE(r, n) {
-    const long long b = rp[r], e = rp[r + 1];
-    const long long ta = (b + r) / kTile, tb = (e + r) / kTile;
-    flag[r] = (e > b && ta != tb) ? 1 : 0;
-  }
+  GRID_STRIDE(r, n) flag[r] = (rp[r] / kTile) != ((rp[r + 1] - 1) / kTile) ? 1 : 0;
 }
 
 __global__ void k_split_fill(const int* rows, long long ns, const int* rp, int4* split) {
   GRID_STRIDE(s, ns) {
     const int r = rows[s];
-    const long long b = rp[r], e = rp[r + 1];
-    split[s] = make_int4(r, (int)((b + r) / kTile), (int)((e + r) / kTile), 0);
+    split[s] = make_int4(r, rp[r] / kTile, (rp[r + 1] - 1) / kTile, 0);
   }
 }
 
@@ -515,13 +518,13 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   out.relabel_levels = levels;
   key.reset(); sel.reset(); sorted.reset(); flag8.reset(); stage_tmp.reset(); sort_tmp2.reset();
 
-  // ---- 6. relabelled CSR over active rows, folded constants
+  // ---- 6. relabelled edge stream over active rows, folded constants
   const int NA = (int)out.n_act;
-  Tmp cntr, K;
+  Tmp cntr, K, rp_new;
   IG_CK(cntr.alloc((size_t)(NA + 1) * sizeof(int)));
   IG_CK(K.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(double)));
+  IG_CK(rp_new.alloc((size_t)(NA + 1) * sizeof(int)));
   IG_CK(cudaMemsetAsync(cntr.p, 0, (size_t)(NA + 1) * sizeof(int), s));
-  IG_CK(cudaMalloc(&out.rp, (size_t)(NA + 1) * sizeof(int)));
   if (NA > 0)
     k_row_count<<<grid_for((long long)NA * 32, 256), 256, 0, s>>>(
         rp, idx_in, out.old_of_new, cls.as<unsigned char>(), a_old.as<double>(), NA,
@@ -529,31 +532,38 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   {
     Tmp scan_tmp;
     size_t sb = 0;
-    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cntr.as<int>(), out.rp, NA + 1, s));
+    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cntr.as<int>(), rp_new.as<int>(), NA + 1, s));
     IG_CK(scan_tmp.alloc(sb));
-    IG_CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, sb, cntr.as<int>(), out.rp, NA + 1, s));
+    IG_CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, sb, cntr.as<int>(), rp_new.as<int>(), NA + 1, s));
   }
   int m_act = 0;
-  IG_CK(cudaMemcpyAsync(&m_act, out.rp + NA, sizeof(int), cudaMemcpyDeviceToHost, s));
+  IG_CK(cudaMemcpyAsync(&m_act, rp_new.as<int>() + NA, sizeof(int), cudaMemcpyDeviceToHost, s));
   IG_CK(cudaStreamSynchronize(s));
   out.m_act = m_act;
+  out.ntiles = (int)(((long long)m_act + kTile - 1) / kTile);
+  const long long m_pad = (long long)out.ntiles * kTile;
   {
     Tmp idx2, seg_tmp;
-    IG_CK(cudaMalloc(&out.idx, (size_t)(m_act > 0 ? m_act : 1) * sizeof(int)));
+    IG_CK(cudaMalloc(&out.edges, (size_t)(m_pad > 0 ? m_pad : 4) * sizeof(unsigned)));
     IG_CK(idx2.alloc((size_t)(m_act > 0 ? m_act : 1) * sizeof(int)));
+    int* ed = (int*)out.edges;
     if (NA > 0)
       k_row_fill<<<grid_for((long long)NA * 32, 256), 256, 0, s>>>(
-          rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(), out.rp, NA,
-          out.idx);
+          rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
+          rp_new.as<int>(), NA, N, ed);
     if (m_act > 0) {
-      cub::DoubleBuffer<int> kb(out.idx, idx2.as<int>());
+      cub::DoubleBuffer<int> kb(ed, idx2.as<int>());
       size_t tb = 0;
-      IG_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, kb, m_act, NA, out.rp, out.rp + 1, s));
+      IG_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, kb, m_act, NA, rp_new.as<int>(),
+                                               rp_new.as<int>() + 1, s));
       IG_CK(seg_tmp.alloc(tb));
-      IG_CK(cub::DeviceSegmentedSort::SortKeys(seg_tmp.p, tb, kb, m_act, NA, out.rp, out.rp + 1, s));
-      if (kb.Current() != out.idx)
-        IG_CK(cudaMemcpyAsync(out.idx, kb.Current(), (size_t)m_act * sizeof(int),
+      IG_CK(cub::DeviceSegmentedSort::SortKeys(seg_tmp.p, tb, kb, m_act, NA, rp_new.as<int>(),
+                                               rp_new.as<int>() + 1, s));
+      if (kb.Current() != ed)
+        IG_CK(cudaMemcpyAsync(ed, kb.Current(), (size_t)m_act * sizeof(int),
                               cudaMemcpyDeviceToDevice, s));
+      k_flag_rows<<<grid_for(NA, 256), 256, 0, s>>>(rp_new.as<int>(), NA, m_act, m_pad, N,
+                                                    out.edges);
     }
     IG_CK(cudaStreamSynchronize(s));
   }
@@ -571,12 +581,10 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
       out.lam, out.psi);
   out.relabeled = 1;
 
-  // ---- 7. merge-path tiles and split rows (over the n_act x m_act CSR)
-  const long long items = (long long)NA + m_act;
-  out.ntiles = (int)((items + kTile - 1) / kTile);
-  IG_CK(cudaMalloc(&out.tile_coord, (size_t)(out.ntiles + 1) * sizeof(int2)));
-  k_tile_coords<<<grid_for(out.ntiles + 1, 256), 256, 0, s>>>(out.rp, NA, m_act, out.ntiles,
-                                                              out.tile_coord);
+  // ---- 7. edge tiles: first row of every tile, rows spanning tiles
+  IG_CK(cudaMalloc(&out.tile_row, (size_t)(out.ntiles + 1) * sizeof(int)));
+  k_tile_rows<<<grid_for(out.ntiles + 1, 256), 256, 0, s>>>(rp_new.as<int>(), NA, out.ntiles,
+                                                            out.tile_row);
   {
     Tmp fl, rows, ns, sel_tmp;
     IG_CK(fl.alloc((size_t)(NA > 0 ? NA : 1)));
@@ -585,7 +593,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     IG_CK(cudaMemsetAsync(ns.p, 0, sizeof(long long), s));
     long long hs = 0;
     if (NA > 0) {
-      k_split_flags<<<grid_for(NA, 256), 256, 0, s>>>(out.rp, NA, fl.as<unsigned char>());
+      k_split_flags<<<grid_for(NA, 256), 256, 0, s>>>(rp_new.as<int>(), NA, fl.as<unsigned char>());
       cub::CountingInputIterator<int> it(0);
       size_t tb = 0;
       IG_CK(cub::DeviceSelect::Flagged(nullptr, tb, it, fl.as<unsigned char>(), rows.as<int>(),
@@ -599,7 +607,8 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     out.nsplit = (int)hs;
     IG_CK(cudaMalloc(&out.split, (size_t)(hs > 0 ? hs : 1) * sizeof(int4)));
     if (hs > 0)
-      k_split_fill<<<grid_for(hs, 256), 256, 0, s>>>(rows.as<int>(), hs, out.rp, out.split);
+      k_split_fill<<<grid_for(hs, 256), 256, 0, s>>>(rows.as<int>(), hs, rp_new.as<int>(),
+                                                     out.split);
     IG_CK(cudaStreamSynchronize(s));
   }
   IG_CK(cudaGetLastError());

@@ -9,6 +9,13 @@
 // This is the rank-1 factorisation A = P diag(c), B = P diag(d) with
 // P[n,j] = w_j / W_n 1{j in L(n)}: (s^T A)_j = mu_j sum_{n in F(j)} s_n / W_n,
 // so one gathered vector x serves A and B and no per-edge value is stored.
+//
+// Edge stream: the follower lists of the active rows [0, n_act), in
+// row order, as uint32 words: bits 0..30 = follower label, bit 31 = "first edge of a row".
+// Every active row has >= 1 word (a row whose followers were all folded away gets one
+// pseudo edge to the sentinel label n, whose x is 0), so row r is simply the r-th flag:
+// no row_ptr is read by the sweep.  The stream is padded to a multiple of kTile with
+// unflagged sentinel words.
 #pragma once
 
 #include <cstdint>
@@ -16,11 +23,11 @@
 
 namespace psi {
 
-// Merge-path sweep tiles: TILE merge items (row completions + edges) per tile.
 constexpr int kBlock = 256;              // threads per CTA of the sweep kernel
-constexpr int kIpt = 8;                  // merge items per thread
-constexpr int kTile = kBlock * kIpt;     // 2048 items per tile
+constexpr int kEpt = 8;                  // edges per thread
+constexpr int kTile = kBlock * kEpt;     // 2048 edges per tile
 constexpr int kFixBlock = 256;           // threads per CTA of the split-row fix-up kernel
+constexpr unsigned kRowFlag = 0x80000000u;
 
 // Device-resident loop state (written by kernels, read back by the host once per iterate).
 struct LoopState {
@@ -42,24 +49,24 @@ struct LoopParams {
 
 // Everything one sweep / readout launch needs (passed by value; frozen in the graph).
 struct SweepArgs {
-  const int* rp;             // row_ptr (int32, relabelled) [n+1]
-  const int* idx;            // followers (int32, relabelled) [m]
-  const int2* tile_coord;    // merge-path start (row, edge) of tile k, k = 0..ntiles
+  const unsigned* edges;     // flagged edge stream [ntiles * kTile]
+  const int* tile_row;       // tile_row[k] = number of row flags before edge k*kTile (k <= ntiles)
   int ntiles;
-  const int4* split;         // split rows: {row, first tile, last tile, 0}
+  const int4* split;         // rows spanning tiles: {row, first tile, last tile, 0}
   int nsplit;
-  double* piece_first;       // per tile: partial sum of the tile's first row
-  double* piece_last;        // per tile: partial sum of the tile's trailing (unfinished) row
-  const double* a0;          // x_0 (init) [n_act used]
-  const double* a;           // sweep constant a + g K        [n_act]
-  const double* g;           //                                [n_act]
-  const double* wt;          // Wt                             [n]
-  const double* d;           // readout constant d + lambda K  [n_act]
-  const double* lam;         //                                [n_act]
+  double* p_in;              // per tile: partial of the row open at the tile's start
+  double* p_out;             // per tile: partial of the last row started in it, if it continues
+  const double* a0;          // x_0 (init)                       [n_act]
+  const double* a;           // sweep constant a + g K           [n_act]
+  const double* g;           //                                  [n_act]
+  const double* wt;          // Wt                               [n]
+  const double* d;           // readout constant d + lambda K    [n_act]
+  const double* lam;         //                                  [n_act]
   double n_users;            // N of psi = (...)/N
   int n_act;
+  int hot_lim;               // labels < hot_lim: L2 evict_last for x gathers/stores
   double* psi;               // readout output (relabelled order)
-  double* x0;
+  double* x0;                // ping-pong iterate buffers [n + 1], x[n] = 0 (sentinel)
   double* x1;
   double* eps_part1;         // per CTA of the tile kernel
   double* eps_part2;         // per CTA of the fix-up kernel
@@ -76,14 +83,13 @@ int fix_grid(int nsplit);            // CTAs of the fix-up kernel
 void* sweep_kernel_ptr(bool readout);
 void* fix_kernel_ptr(bool readout);
 void* init_kernel_ptr();
-size_t sweep_smem_bytes();
 
 // ---- ingest (psi_ingest.cu)
 // Device arrays in the NEW (relabelled) user order; active users [0, n_act) have >= 1
 // follower, follower-less users [n_act, n) never change (x = a0, psi = d/N).
 struct IngestOut {
-  int* rp = nullptr;          // [n_act+1] CSR over active rows
-  int* idx = nullptr;         // [m_act]   active followers, new labels, ascending per row
+  unsigned* edges = nullptr;  // [ntiles*kTile] flagged edge stream (see above)
+  int* tile_row = nullptr;    // [ntiles+1]
   double* a0 = nullptr;       // [n]     x_0 = c / Wt
   double* a1 = nullptr;       // [n_act] sweep constant a + g K (K: folded follower-less terms)
   double* g = nullptr;        // [n_act] mu / Wt
@@ -92,11 +98,10 @@ struct IngestOut {
   double* lam = nullptr;      // [n_act]
   double* psi = nullptr;      // [n]     readout buffer; [n_act, n) prefilled with d/N
   int* old_of_new = nullptr;  // [n]
-  int2* tile_coord = nullptr;
   int ntiles = 0;
   int4* split = nullptr;
   int nsplit = 0;
-  long long n_act = 0, m_act = 0, n_hot = 0;
+  long long n_act = 0, m_act = 0, n_hot = 0, n_pseudo = 0;
   int relabel_levels = 0;
   double kappa_row = 0, kappa_col = 0, rho_A = 0;
   long long n_f = 0, n_g = 0, n_leaderless = 0;

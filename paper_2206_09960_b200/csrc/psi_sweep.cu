@@ -2,34 +2,77 @@
 //
 // One sweep = two launches inside the CUDA-graph WHILE loop (psi_api.cu):
 //
-//  k_tiles   persistent merge-path gather-SpMV over the follower CSR (Merrill & Garland's
-//            merge-based CsrMV).  Tile k owns merge items [k*kTile, (k+1)*kTile) of the
-//            (row completions + edges) path, so every CTA does the same amount of work
-//            whatever the degree distribution (power-law rows, SURVEY §7 "load balance").
-//            Per tile: stage row ends + the gathered x_{t-1}[F(j)] in shared memory
-//            (coalesced int32 index loads, independent 8-byte gathers in flight), merge-path
-//            consume, block segmented scan of the per-thread carries, then a row-parallel
-//            epilogue x_t = a + g*S, |dx|*Wt accumulated for eps_t (Eq. (15)).
-//            Rows cut by a tile boundary leave partial sums ("pieces").
-//  k_fix     finishes the rows cut by tile boundaries (sum of pieces in tile order), then
-//            the LAST CTA to arrive reduces the per-CTA eps partials in a fixed order,
-//            appends eps_t to the history, updates gap = ||B|| eps_t (Alg. 2),
-//            t += 1, and sets the graph's WHILE condition (gap > eps && t < max_iters):
-//            the stop rule of Eq. (16)/Alg. 2 line 320 without a host round trip.
+//  k_tiles   persistent, edge-balanced gather-SpMV over the flagged edge stream
+//            (psi_internal.cuh).  Tile k = edges [k*kTile, (k+1)*kTile): every CTA does the
+//            same number of gathers whatever the power-law row lengths.  Per
+//            tile each thread loads 8 consecutive edge words (two 128-bit loads, prefetched
+//            one tile ahead), issues 8 independent 8-byte gathers of x_{t-1}, reduces its
+//            values by the row-start flags in registers, and a block-wide segmented scan
+//            (warp shuffles + one smem step) carries partial row sums across threads.
+//            Row sums land in shared memory; a row-parallel epilogue then writes
+//            x_t = a + g*S coalesced and accumulates Wt*|x_t - x_{t-1}| for eps_t (Eq. (15)).
+//            Rows that continue across tile boundaries leave two partials per tile
+//            (p_in: the row open at the tile start; p_out: the last row started in it).
+//  k_fix     finishes the rows cut by tile boundaries (p_out of the first tile + p_in of
+//            the following ones, in tile order), then the LAST CTA to arrive reduces the
+//            per-CTA eps partials in a fixed order, appends eps_t to the history, updates
+//            gap = ||B|| eps_t (Alg. 2), t += 1, and sets the graph's WHILE
+//            condition (gap > eps && t < max_iters): the stop rule of Eq. (16) / Alg. 2
+//            line 320 without a host round trip.
 //
 // The readout (Alg. 2) is the same pair of kernels with the epilogue
 // psi_j = (d_j + lambda_j S_j) / N.
 //
-// Determinism: no floating-point atomics anywhere; tile -> CTA assignment is static, every
+// Determinism: no floating-point atomics; tile -> CTA assignment is static and every
 // reduction has a fixed order, so two runs give bitwise identical psi and eps_t.
 #include "psi_internal.cuh"
-
-#include <climits>
 
 namespace psi {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr unsigned kLabelMask = 0x7fffffffu;
+
+// ---- L2 cache policies (createpolicy + .L2::cache_hint).  Streams read once per sweep
+// (edge words, per-row constants) are evict_first and bypass L1, so they do not push the
+// hot prefix of x out of L2; gathers and stores of x labels below hot_lim (the
+// most-gathered users) are evict_last.
+__device__ __forceinline__ unsigned long long pol_evict_first() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long pol_evict_last() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ld_stream4(const unsigned* p, unsigned long long pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ unsigned ld_stream(const unsigned* p, unsigned long long pol) {
+  unsigned v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_hint(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -55,14 +98,12 @@ __device__ double block_sum(double v, double* red) {
 }
 
 struct TileSmem {
-  double val[kTile];          // x_{t-1}[idx[e]] for the tile's edges
-  double rowsum[kTile];       // per completed row: sum of its in-tile edges
-  int rowend[kTile + 1];      // local end offset of each completed row (+ sentinel)
-  double scan[kBlock];        // segmented inclusive scan of thread carries
-  double wS[kBlock / 32];
-  int wK[kBlock / 32];
+  double rowsum[kTile];       // S of the rows started in this tile (local row index)
+  double wv[kBlock / 32];     // warp aggregates of the segmented scan
+  int wf[kBlock / 32];
+  int wn[kBlock / 32];
   double red[33];
-  int split_in;
+  int next_flag;              // does the edge after this tile start a row?
 };
 
 template <bool READOUT>
@@ -72,95 +113,117 @@ __global__ void __launch_bounds__(kBlock, 4) k_tiles(SweepArgs A) {
   const double* __restrict__ xs = (t & 1) ? A.x1 : A.x0;    // x_{t-1}
   double* __restrict__ xd = (t & 1) ? A.x0 : A.x1;          // x_t
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned long long pf = pol_evict_first(), pl = pol_evict_last();
+  const unsigned hot_lim = (unsigned)A.hot_lim;
+  const int ntiles = A.ntiles;
   double eps_acc = 0.0;
 
-  for (int k = blockIdx.x; k < A.ntiles; k += gridDim.x) {
-    const int2 c0 = A.tile_coord[k];
-    const int2 c1 = A.tile_coord[k + 1];
-    const int r0 = c0.x, e0 = c0.y;
-    const int nr = c1.x - r0;      // rows completed in this tile
-    const int ne = c1.y - e0;      // edges consumed in this tile
+  int k = blockIdx.x;
+  uint4 u0 = make_uint4(0, 0, 0, 0), u1 = u0;
+  if (k < ntiles) {
+    const unsigned* p = A.edges + (size_t)k * kTile + tid * kEpt;
+    u0 = ld_stream4(p, pf);
+    u1 = ld_stream4(p + 4, pf);
+  }
+  for (; k < ntiles; k += gridDim.x) {
+    const int f0 = __ldg(A.tile_row + k);
+    const int F = __ldg(A.tile_row + k + 1) - f0;      // rows started in this tile
+    const unsigned w[kEpt] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
 
-    // ---- stage: row ends and gathered x values
-    for (int i = tid; i < nr; i += kBlock) sm.rowend[i] = __ldg(A.rp + r0 + i + 1) - e0;
-    if (tid == 0) {
-      sm.rowend[nr] = INT_MAX;
-      sm.split_in = __ldg(A.rp + r0) < e0;     // first row began in an earlier tile
-    }
-    {
-      int j[kIpt];
+    // ---- 8 independent gathers of x_{t-1}
+    double v[kEpt];
+    unsigned fl = 0;
 #pragma unroll
-      for (int u = 0; u < kIpt; ++u) {
-        const int q = u * kBlock + tid;
-        j[u] = q < ne ? __ldg(A.idx + e0 + q) : 0;
-      }
-      double v[kIpt];
-#pragma unroll
-      for (int u = 0; u < kIpt; ++u) {
-        const int q = u * kBlock + tid;
-        v[u] = q < ne ? __ldg(xs + j[u]) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kIpt; ++u) {
-        const int q = u * kBlock + tid;
-        if (q < ne) sm.val[q] = v[u];
-      }
+    for (int q = 0; q < kEpt; ++q) {
+      const unsigned lab = w[q] & kLabelMask;
+      fl |= (w[q] >> 31) << q;
+      v[q] = ld_hint(xs + lab, lab < hot_lim ? pl : pf);
     }
-    __syncthreads();
-    const int split_in = sm.split_in;
-
-    // ---- merge-path consume: kIpt items per thread
-    const int total = nr + ne;
-    const int diag = min(tid * kIpt, total);
-    const int dend = min(diag + kIpt, total);
-    int lo = max(0, diag - ne), hi = min(diag, nr);
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (sm.rowend[mid] <= diag - mid - 1) lo = mid + 1; else hi = mid;
-    }
-    int i = lo, q = diag - lo;
-    const int i0 = i;
-    double run = 0.0;
-    for (int dd = diag; dd < dend; ++dd) {
-      if (q < sm.rowend[i]) { run += sm.val[q]; ++q; }
-      else { sm.rowsum[i] = run; run = 0.0; ++i; }
+    if (tid == 0)
+      sm.next_flag = (k + 1 >= ntiles) ? 1 : (int)(ld_stream(A.edges + (size_t)(k + 1) * kTile, pf) >> 31);
+    // ---- prefetch the next tile's edge words
+    const int kn = k + gridDim.x;
+    if (kn < ntiles) {
+      const unsigned* p = A.edges + (size_t)kn * kTile + tid * kEpt;
+      u0 = ld_stream4(p, pf);
+      u1 = ld_stream4(p + 4, pf);
     }
 
-    // ---- block segmented scan of carries (key = row the thread ended in)
-    const int key = i;
-    double S = run;
+    // ---- thread-local reduction by row flags
+    const int nf = __popc(fl);
+    double head = 0.0, run = 0.0;
+    bool seen = false;
+#pragma unroll
+    for (int q = 0; q < kEpt; ++q) {
+      if ((fl >> q) & 1u) {
+        if (!seen) head = run;
+        seen = true;
+        run = 0.0;
+      }
+      run += v[q];
+    }
+    // scan element: (has flag, partial of the row open at the thread's end)
+    int f_in = nf > 0;
+    double v_in = run;            // tail if a flag was seen, total otherwise
+    int n_in = nf;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const double s2 = __shfl_up_sync(kFull, S, o);
-      const int k2 = __shfl_up_sync(kFull, key, o);
-      if (lane >= o && k2 == key) S += s2;
+      const int n2 = __shfl_up_sync(kFull, n_in, o);
+      const double v2 = __shfl_up_sync(kFull, v_in, o);
+      const int f2 = __shfl_up_sync(kFull, f_in, o);
+      if (lane >= o) {
+        n_in += n2;
+        if (!f_in) v_in += v2;
+        f_in |= f2;
+      }
     }
-    if (lane == 31) { sm.wS[warp] = S; sm.wK[warp] = key; }
+    if (lane == 31) { sm.wv[warp] = v_in; sm.wf[warp] = f_in; sm.wn[warp] = n_in; }
     __syncthreads();
-    for (int w2 = warp - 1; w2 >= 0 && sm.wK[w2] == key; --w2) S += sm.wS[w2];
-    sm.scan[tid] = S;
-    __syncthreads();
-    if (i > i0 && tid > 0) sm.rowsum[i0] += sm.scan[tid - 1];   // carry into first completed row
-    __syncthreads();
+    const int next_flag = sm.next_flag;
+    int nP = 0, fP = 0;
+    double vP = 0.0;
+    for (int w2 = 0; w2 < warp; ++w2) {              // fold of earlier warps, fixed order
+      nP += sm.wn[w2];
+      vP = sm.wf[w2] ? sm.wv[w2] : vP + sm.wv[w2];
+      fP |= sm.wf[w2];
+    }
+    const double v_full = f_in ? v_in : vP + v_in;
+    const double v_prev = __shfl_up_sync(kFull, v_full, 1);
+    double carry = lane == 0 ? vP : v_prev;          // partial of the row open at thread start
+    const int n_ex = nP + n_in - nf;                 // flags before this thread in the tile
 
-    // ---- pieces of rows cut by tile boundaries (finished in k_fix)
-    if (tid == 0) {
-      const double tail = sm.scan[kBlock - 1];
-      if (nr == 0) { A.piece_first[k] = tail; A.piece_last[k] = 0.0; }
-      else { A.piece_first[k] = sm.rowsum[0]; A.piece_last[k] = tail; }
+    // ---- emit completed row sums
+    int row = n_ex - 1;                              // local index of the open row
+    run = carry;
+#pragma unroll
+    for (int q = 0; q < kEpt; ++q) {
+      if ((fl >> q) & 1u) {
+        if (row >= 0) sm.rowsum[row] = run;
+        else A.p_in[k] = run;                        // first flag of the tile ends row f0-1
+        ++row;
+        run = 0.0;
+      }
+      run += v[q];
     }
+    if (tid == kBlock - 1) {                         // the tile's last open row
+      if (F == 0) { A.p_in[k] = run; A.p_out[k] = 0.0; }
+      else if (next_flag) { sm.rowsum[F - 1] = run; A.p_out[k] = 0.0; }
+      else A.p_out[k] = run;
+    }
+    __syncthreads();
 
     // ---- epilogue over the rows completed in this tile (coalesced)
-    for (int ii = tid; ii < nr; ii += kBlock) {
-      if (ii == 0 && split_in) continue;
-      const int r = r0 + ii;
-      const double Sr = sm.rowsum[ii];
+    const int nrows = (F > 0 && !next_flag) ? F - 1 : F;
+    for (int i = tid; i < nrows; i += kBlock) {
+      const int r = f0 + i;
+      const double Sr = sm.rowsum[i];
       if (READOUT) {
-        A.psi[r] = (__ldg(A.d + r) + __ldg(A.lam + r) * Sr) / A.n_users;
+        A.psi[r] = (ld_stream(A.d + r, pf) + ld_stream(A.lam + r, pf) * Sr) / A.n_users;
       } else {
-        const double xn = fma(__ldg(A.g + r), Sr, __ldg(A.a + r));
-        eps_acc += __ldg(A.wt + r) * fabs(xn - xs[r]);
-        xd[r] = xn;
+        const unsigned long long px = (unsigned)r < hot_lim ? pl : pf;
+        const double xn = fma(ld_stream(A.g + r, pf), Sr, ld_stream(A.a + r, pf));
+        eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - ld_hint(xs + r, px));
+        st_hint(xd + r, xn, px);
       }
     }
   }
@@ -184,9 +247,8 @@ __global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
   for (int s = blockIdx.x * kFixBlock + tid; s < A.nsplit; s += gridDim.x * kFixBlock) {
     const int4 sp = A.split[s];
     const int r = sp.x;
-    double S = 0.0;
-    for (int k = sp.y; k <= sp.z; ++k)
-      S += (A.tile_coord[k].x == r) ? A.piece_first[k] : A.piece_last[k];
+    double S = A.p_out[sp.y];
+    for (int k = sp.y + 1; k <= sp.z; ++k) S += A.p_in[k];
     if (READOUT) {
       A.psi[r] = (A.d[r] + A.lam[r] * S) / A.n_users;
     } else {
@@ -279,6 +341,5 @@ void* fix_kernel_ptr(bool readout) {
   return readout ? (void*)k_fix<true> : (void*)k_fix<false>;
 }
 void* init_kernel_ptr() { return (void*)k_init; }
-size_t sweep_smem_bytes() { return sizeof(TileSmem); }
 
 }  // namespace psi
