@@ -52,7 +52,6 @@ struct psi_ctx {
   long long n = 0, m = 0;
   cudaStream_t stream = nullptr;
   IngestOut g;
-  Partition part;
   double* x[2] = {nullptr, nullptr};
   double* p_in = nullptr;        // per tile: partial of the row open at the tile start
   double* p_out = nullptr;       // per tile: partial of its last row if that row continues
@@ -82,9 +81,8 @@ void free_ctx(psi_ctx* c) {
   if (!c) return;
   if (c->exec) cudaGraphExecDestroy(c->exec);
   if (c->graph) cudaGraphDestroy(c->graph);
-  void* ptrs[] = {c->g.edges, c->g.chunk_row, c->g.rp_new, c->g.a0, c->g.a1, c->g.g, c->g.wt,
-                  c->g.d1, c->g.lam, c->g.psi, c->g.old_of_new, c->part.warp_chunk,
-                  c->part.warp_row, c->part.split, c->x[0], c->x[1],
+  void* ptrs[] = {c->g.edges, c->g.tile_row, c->g.a0, c->g.a1, c->g.g, c->g.wt, c->g.d1,
+                  c->g.lam, c->g.psi, c->g.old_of_new, c->g.split, c->x[0], c->x[1],
                   c->p_in, c->p_out, c->eps_part1, c->eps_part2, c->history, c->st, c->prm};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -98,12 +96,10 @@ void free_ctx(psi_ctx* c) {
 SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   SweepArgs A{};
   A.edges = c->g.edges;
-  A.nchunks = c->g.nchunks;
-  A.warp_chunk = c->part.warp_chunk;
-  A.warp_row = c->part.warp_row;
-  A.nwarps = c->part.nwarps;
-  A.split = c->part.split;
-  A.nsplit = c->part.nsplit;
+  A.tile_row = c->g.tile_row;
+  A.ntiles = c->g.ntiles;
+  A.split = c->g.split;
+  A.nsplit = c->g.nsplit;
   A.p_in = c->p_in;
   A.p_out = c->p_out;
   A.a0 = c->g.a0;
@@ -321,13 +317,7 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
 
   // Iteration buffers.
-  c->grid1 = sweep_grid();
-  rc = partition(c->g, c->grid1 * kWarps, c->stream, c->part, msg, sizeof(msg));
-  if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
-  cudaFree(c->g.chunk_row);
-  cudaFree(c->g.rp_new);
-  c->g.chunk_row = nullptr;
-  c->g.rp_new = nullptr;
+  c->grid1 = sweep_grid(c->g.ntiles);
   {
     // Hot prefix of x kept in L2 (evict_last) in BOTH ping-pong buffers: PSI_HOT_MB per
     // buffer (default: a third of L2 each), never more than the users with >= 2 leaders.
@@ -343,13 +333,13 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
     if (const char* e = getenv("PSI_L2_FETCH")) fetch = atoi(e);
     if (fetch > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)fetch);
   }
-  c->grid2 = fix_grid(c->part.nsplit);
+  c->grid2 = fix_grid(c->g.nsplit);
   B_CK(cudaMalloc(&c->x[0], (n + 1) * sizeof(double)));      // + sentinel x[n] = 0
   B_CK(cudaMalloc(&c->x[1], (n + 1) * sizeof(double)));
   B_CK(cudaMemsetAsync(c->x[0] + n, 0, sizeof(double), c->stream));
   B_CK(cudaMemsetAsync(c->x[1] + n, 0, sizeof(double), c->stream));
-  B_CK(cudaMalloc(&c->p_in, (c->part.nwarps + 1) * sizeof(double)));
-  B_CK(cudaMalloc(&c->p_out, (c->part.nwarps + 1) * sizeof(double)));
+  B_CK(cudaMalloc(&c->p_in, (c->g.ntiles + 1) * sizeof(double)));
+  B_CK(cudaMalloc(&c->p_out, (c->g.ntiles + 1) * sizeof(double)));
   B_CK(cudaMalloc(&c->eps_part1, c->grid1 * sizeof(double)));
   B_CK(cudaMalloc(&c->eps_part2, c->grid2 * sizeof(double)));
   B_CK(cudaMalloc(&c->st, sizeof(LoopState)));
@@ -365,8 +355,8 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   float ms = 0;
   B_CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   c->ingest_ms = ms;
-  c->device_bytes = (long long)c->g.nchunks * kChunk * 4 + 6 * n * 8 + 4 * c->g.n_act * 8 +
-                    (long long)c->part.nwarps * 24 + (long long)c->part.nsplit * 16 + n * 4;
+  c->device_bytes = (long long)c->g.ntiles * kTile * 4 + 6 * n * 8 + 4 * c->g.n_act * 8 +
+                    (c->g.ntiles + 1) * (4 + 16) + (long long)c->g.nsplit * 16 + n * 4;
 
   psi_status gs = build_graph_exec(c);
   if (gs != PSI_OK) return bail(gs);
@@ -475,8 +465,8 @@ psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
   out->iterate_ms = c->iterate_ms;
   out->last_iters = c->last_T;
   out->last_gap = c->last_gap;
-  out->num_tiles = c->g.nchunks;
-  out->num_long_rows = c->part.nsplit;
+  out->num_tiles = c->g.ntiles;
+  out->num_long_rows = c->g.nsplit;
   out->grid = c->grid1;
   out->device_bytes = (int64_t)c->device_bytes;
   out->relabeled = c->g.relabeled;

@@ -36,7 +36,6 @@
 
 #include <cstdio>
 #include <cstring>
-#include <vector>
 
 namespace psi {
 namespace {
@@ -307,51 +306,30 @@ __global__ void k_permute_vectors(const int* old_of_new, int n, int n_act, const
   }
 }
 
-// ------------------------------------------------------------------ 7. chunks, warp ranges
+// ------------------------------------------------------------------ 7. tiles
 
-// chunk_row[k] = number of rows whose first edge lies before edge k*kChunk
-__global__ void k_chunk_rows(const int* rp, int n_act, int nchunks, int* chunk_row) {
-  GRID_STRIDE(k, nchunks + 1) {
-    const long long e = k * (long long)kChunk;
+// tile_row[k] = number of rows whose first edge lies before edge k*kTile
+__global__ void k_tile_rows(const int* rp, int n_act, int ntiles, int* tile_row) {
+  GRID_STRIDE(k, ntiles + 1) {
+    const long long e = k * (long long)kTile;
     int lo = 0, hi = n_act;                 // first row r with rp[r] >= e
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if ((long long)rp[mid] < e) lo = mid + 1; else hi = mid;
     }
-    chunk_row[k] = lo;
+    tile_row[k] = lo;
   }
 }
 
-// Warp w gets chunks [b_w, b_{w+1}) with b_w = first chunk whose cost prefix
-// P(c) = c*kChunk + kRowCost*chunk_row[c] reaches w/nwarps of the total.
-__global__ void k_warp_bounds(const int* chunk_row, int nchunks, int nwarps, int* warp_chunk,
-                              int* warp_row) {
-  GRID_STRIDE(w, nwarps + 1) {
-    const double total = (double)nchunks * kChunk + (double)kRowCost * chunk_row[nchunks];
-    const double target = total * (double)w / nwarps;
-    int lo = 0, hi = nchunks;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((double)mid * kChunk + (double)kRowCost * chunk_row[mid] < target) lo = mid + 1; else hi = mid;
-    }
-    if (w == nwarps) lo = nchunks;
-    warp_chunk[w] = lo;
-    if (w < nwarps) warp_row[w] = chunk_row[lo];
-  }
+// rows whose edges fall in more than one tile
+__global__ void k_split_flags(const int* rp, int n, unsigned char* flag) {
+  GRID_STRIDE(r, n) flag[r] = (rp[r] / kTile) != ((rp[r + 1] - 1) / kTile) ? 1 : 0;
 }
 
-// For every warp boundary w >= 1: the row open across it (first word not a row start), or -1;
-// with the chunks of that row's first and last edge.
-__global__ void k_boundary_rows(const int* warp_chunk, const int* chunk_row, const unsigned* edges,
-                                const int* rp, int nwarps, int nchunks, int4* cand) {
-  GRID_STRIDE(w, nwarps) {
-    int4 o = make_int4(-1, 0, 0, 0);
-    const int c = warp_chunk[w];
-    if (w > 0 && c < nchunks && !(edges[(size_t)c * kChunk] & kRowFlag)) {
-      const int r = chunk_row[c] - 1;
-      o = make_int4(r, rp[r] / kChunk, (rp[r + 1] - 1) / kChunk, 0);
-    }
-    cand[w] = o;
+__global__ void k_split_fill(const int* rows, long long ns, const int* rp, int4* split) {
+  GRID_STRIDE(s, ns) {
+    const int r = rows[s];
+    split[s] = make_int4(r, rp[r] / kTile, (rp[r + 1] - 1) / kTile, 0);
   }
 }
 
@@ -562,8 +540,8 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   IG_CK(cudaMemcpyAsync(&m_act, rp_new.as<int>() + NA, sizeof(int), cudaMemcpyDeviceToHost, s));
   IG_CK(cudaStreamSynchronize(s));
   out.m_act = m_act;
-  out.nchunks = (int)(((long long)m_act + kChunk - 1) / kChunk);
-  const long long m_pad = (long long)out.nchunks * kChunk;
+  out.ntiles = (int)(((long long)m_act + kTile - 1) / kTile);
+  const long long m_pad = (long long)out.ntiles * kTile;
   {
     Tmp idx2, seg_tmp;
     IG_CK(cudaMalloc(&out.edges, (size_t)(m_pad > 0 ? m_pad : 4) * sizeof(unsigned)));
@@ -603,55 +581,37 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
       out.lam, out.psi);
   out.relabeled = 1;
 
-  // ---- 7. chunk row counts (for the warp partition, psi_api.cu -> partition())
-  IG_CK(cudaMalloc(&out.chunk_row, (size_t)(out.nchunks + 1) * sizeof(int)));
-  k_chunk_rows<<<grid_for(out.nchunks + 1, 256), 256, 0, s>>>(rp_new.as<int>(), NA, out.nchunks,
-                                                              out.chunk_row);
-  out.rp_new = rp_new.as<int>();
-  rp_new.p = nullptr;                      // ownership moves to out (freed after partition)
-  IG_CK(cudaGetLastError());
-  return PSI_OK;
-}
-
-int partition(const IngestOut& g, int nwarps, cudaStream_t s, Partition& out, char* msg,
-              size_t msg_len) {
-  out.nwarps = nwarps;
-  IG_CK(cudaMalloc(&out.warp_chunk, (size_t)(nwarps + 1) * sizeof(int)));
-  IG_CK(cudaMalloc(&out.warp_row, (size_t)nwarps * sizeof(int)));
-  k_warp_bounds<<<grid_for(nwarps + 1, 256), 256, 0, s>>>(g.chunk_row, g.nchunks, nwarps,
-                                                          out.warp_chunk, out.warp_row);
-  Tmp cand;
-  IG_CK(cand.alloc((size_t)nwarps * sizeof(int4)));
-  k_boundary_rows<<<grid_for(nwarps, 256), 256, 0, s>>>(out.warp_chunk, g.chunk_row, g.edges,
-                                                        g.rp_new, nwarps, g.nchunks,
-                                                        cand.as<int4>());
-  std::vector<int4> hc(nwarps);
-  std::vector<int> hb(nwarps + 1);
-  IG_CK(cudaMemcpyAsync(hc.data(), cand.p, nwarps * sizeof(int4), cudaMemcpyDeviceToHost, s));
-  IG_CK(cudaMemcpyAsync(hb.data(), out.warp_chunk, (nwarps + 1) * sizeof(int),
-                        cudaMemcpyDeviceToHost, s));
-  IG_CK(cudaStreamSynchronize(s));
-  // warp owning chunk c: last w with b_w <= c (empty ranges skipped)
-  auto owner = [&](int c) {
-    int lo = 0, hi = nwarps;               // first w with b_w > c, minus one
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (hb[mid] <= c) lo = mid + 1; else hi = mid;
+  // ---- 7. edge tiles: first row of every tile, rows spanning tiles
+  IG_CK(cudaMalloc(&out.tile_row, (size_t)(out.ntiles + 1) * sizeof(int)));
+  k_tile_rows<<<grid_for(out.ntiles + 1, 256), 256, 0, s>>>(rp_new.as<int>(), NA, out.ntiles,
+                                                            out.tile_row);
+  {
+    Tmp fl, rows, ns, sel_tmp;
+    IG_CK(fl.alloc((size_t)(NA > 0 ? NA : 1)));
+    IG_CK(rows.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(int)));
+    IG_CK(ns.alloc(sizeof(long long)));
+    IG_CK(cudaMemsetAsync(ns.p, 0, sizeof(long long), s));
+    long long hs = 0;
+    if (NA > 0) {
+      k_split_flags<<<grid_for(NA, 256), 256, 0, s>>>(rp_new.as<int>(), NA, fl.as<unsigned char>());
+      cub::CountingInputIterator<int> it(0);
+      size_t tb = 0;
+      IG_CK(cub::DeviceSelect::Flagged(nullptr, tb, it, fl.as<unsigned char>(), rows.as<int>(),
+                                       ns.as<long long>(), NA, s));
+      IG_CK(sel_tmp.alloc(tb));
+      IG_CK(cub::DeviceSelect::Flagged(sel_tmp.p, tb, it, fl.as<unsigned char>(), rows.as<int>(),
+                                       ns.as<long long>(), NA, s));
+      IG_CK(cudaMemcpyAsync(&hs, ns.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+      IG_CK(cudaStreamSynchronize(s));
     }
-    return lo - 1;
-  };
-  std::vector<int4> split;
-  for (int w = 1; w < nwarps; ++w) {
-    const int4 c = hc[w];
-    if (c.x < 0 || (!split.empty() && split.back().x == c.x)) continue;
-    split.push_back(make_int4(c.x, owner(c.y), owner(c.z), 0));
+    out.nsplit = (int)hs;
+    IG_CK(cudaMalloc(&out.split, (size_t)(hs > 0 ? hs : 1) * sizeof(int4)));
+    if (hs > 0)
+      k_split_fill<<<grid_for(hs, 256), 256, 0, s>>>(rows.as<int>(), hs, rp_new.as<int>(),
+                                                     out.split);
+    IG_CK(cudaStreamSynchronize(s));
   }
-  out.nsplit = (int)split.size();
-  IG_CK(cudaMalloc(&out.split, (size_t)(split.empty() ? 1 : split.size()) * sizeof(int4)));
-  if (!split.empty())
-    IG_CK(cudaMemcpyAsync(out.split, split.data(), split.size() * sizeof(int4),
-                          cudaMemcpyHostToDevice, s));
-  IG_CK(cudaStreamSynchronize(s));
+  IG_CK(cudaGetLastError());
   return PSI_OK;
 }
 

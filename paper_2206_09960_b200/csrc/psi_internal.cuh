@@ -16,10 +16,6 @@
 // pseudo edge to the sentinel label n, whose x is 0), so row r is simply the r-th flag:
 // no row_ptr is read by the sweep.  The stream is padded to a multiple of kTile with
 // unflagged sentinel words.
-//
-// Work split: every warp of the persistent sweep grid owns a contiguous range of 256-edge
-// chunks, balanced on (edges + kRowCost * rows) at ingest, and carries the partial sum of
-// its open row from chunk to chunk; only rows crossing warp ranges are finished by k_fix.
 #pragma once
 
 #include <cstdint>
@@ -28,9 +24,8 @@
 namespace psi {
 
 constexpr int kBlock = 256;              // threads per CTA of the sweep kernel
-constexpr int kWarps = kBlock / 32;      // warps per CTA
-constexpr int kEpt = 8;                  // edges per lane per chunk
-constexpr int kChunk = 32 * kEpt;        // 256 edges per warp chunk
+constexpr int kEpt = 8;                  // edges per thread
+constexpr int kTile = kBlock * kEpt;     // 2048 edges per tile
 constexpr int kFixBlock = 256;           // threads per CTA of the split-row fix-up kernel
 constexpr unsigned kRowFlag = 0x80000000u;
 
@@ -54,15 +49,13 @@ struct LoopParams {
 
 // Everything one sweep / readout launch needs (passed by value; frozen in the graph).
 struct SweepArgs {
-  const unsigned* edges;     // flagged edge stream [nchunks * kChunk]
-  int nchunks;
-  const int* warp_chunk;     // [nwarps+1] chunk range of every sweep warp
-  const int* warp_row;       // [nwarps]   number of row flags before the warp's first chunk
-  int nwarps;
-  const int4* split;         // rows spanning warp ranges: {row, first warp, last warp, 0}
+  const unsigned* edges;     // flagged edge stream [ntiles * kTile]
+  const int* tile_row;       // tile_row[k] = number of row flags before edge k*kTile (k <= ntiles)
+  int ntiles;
+  const int4* split;         // rows spanning tiles: {row, first tile, last tile, 0}
   int nsplit;
-  double* p_in;              // per warp: partial of the row open at the range start
-  double* p_out;             // per warp: partial of its last row if that row continues
+  double* p_in;              // per tile: partial of the row open at the tile's start
+  double* p_out;             // per tile: partial of the last row started in it, if it continues
   const double* a0;          // x_0 (init)                       [n_act]
   const double* a;           // sweep constant a + g K           [n_act]
   const double* g;           //                                  [n_act]
@@ -85,9 +78,8 @@ struct SweepArgs {
 };
 
 // ---- launchers (psi_sweep.cu)
-int sweep_grid();                    // persistent CTAs of the sweep kernel (SMs x occupancy)
+int sweep_grid(int ntiles);          // persistent CTAs for the tile kernel
 int fix_grid(int nsplit);            // CTAs of the fix-up kernel
-constexpr int kRowCost = 3;          // partition weight of a row relative to one edge
 void* sweep_kernel_ptr(bool readout);
 void* fix_kernel_ptr(bool readout);
 void* init_kernel_ptr();
@@ -96,9 +88,8 @@ void* init_kernel_ptr();
 // Device arrays in the NEW (relabelled) user order; active users [0, n_act) have >= 1
 // follower, follower-less users [n_act, n) never change (x = a0, psi = d/N).
 struct IngestOut {
-  unsigned* edges = nullptr;  // [nchunks*kChunk] flagged edge stream (see above)
-  int* chunk_row = nullptr;   // [nchunks+1] row flags before each chunk (ingest only)
-  int* rp_new = nullptr;      // [n_act+1] first edge of each active row (ingest only)
+  unsigned* edges = nullptr;  // [ntiles*kTile] flagged edge stream (see above)
+  int* tile_row = nullptr;    // [ntiles+1]
   double* a0 = nullptr;       // [n]     x_0 = c / Wt
   double* a1 = nullptr;       // [n_act] sweep constant a + g K (K: folded follower-less terms)
   double* g = nullptr;        // [n_act] mu / Wt
@@ -107,23 +98,15 @@ struct IngestOut {
   double* lam = nullptr;      // [n_act]
   double* psi = nullptr;      // [n]     readout buffer; [n_act, n) prefilled with d/N
   int* old_of_new = nullptr;  // [n]
-  int nchunks = 0;
+  int ntiles = 0;
+  int4* split = nullptr;
+  int nsplit = 0;
   long long n_act = 0, m_act = 0, n_hot = 0, n_pseudo = 0;
   int relabel_levels = 0;
   double kappa_row = 0, kappa_col = 0, rho_A = 0;
   long long n_f = 0, n_g = 0, n_leaderless = 0;
   int relabeled = 0;
 };
-
-// Warp ranges for a sweep grid of `nwarps` warps (after ingest).
-struct Partition {
-  int* warp_chunk = nullptr;  // [nwarps+1]
-  int* warp_row = nullptr;    // [nwarps]
-  int4* split = nullptr;      // [nsplit]
-  int nwarps = 0, nsplit = 0;
-};
-int partition(const IngestOut& g, int nwarps, cudaStream_t s, Partition& out, char* msg,
-              size_t msg_len);
 
 // Returns 0 or a negative psi_status; msg gets a description on error.
 int ingest(long long n, long long m, const long long* rp64_dev, const int* idx_dev,

@@ -2,20 +2,19 @@
 //
 // One sweep = two launches inside the CUDA-graph WHILE loop (psi_api.cu):
 //
-//  k_stream  persistent, edge-balanced gather-SpMV over the flagged edge stream
-//            (psi_internal.cuh).  Each warp owns a contiguous range of 256-edge chunks
-//            (balanced on edges + rows at ingest, so power-law row lengths do not matter,
-//            SURVEY §7) and works independently of the other warps: per chunk each lane
-//            holds 8 consecutive edge words (two 128-bit loads), issues 8 independent
-//            8-byte gathers of x_{t-1}, reduces them by the row-start flags in registers,
-//            and a warp segmented scan (shuffles) carries partial row sums across lanes and,
-//            through a register, across chunks.  Completed row sums go through a per-warp
-//            shared-memory slot array to a lane-parallel epilogue that writes
-//            x_t = a + g*S and accumulates Wt*|x_t - x_{t-1}| for eps_t (Eq. (15)).  The
-//            gathers of chunk c+1 and the edge words of chunk c+2 are in flight while chunk
-//            c is reduced.  No block barrier inside the loop.
-//  k_fix     finishes the rows that cross warp ranges (p_out of the first warp + p_in of
-//            the following ones, in warp order), then the LAST CTA to arrive reduces the
+//  k_tiles   persistent, edge-balanced gather-SpMV over the flagged edge stream
+//            (psi_internal.cuh).  Tile k = edges [k*kTile, (k+1)*kTile): every CTA does the
+//            same number of gathers whatever the power-law row lengths.  Per
+//            tile each thread loads 8 consecutive edge words (two 128-bit loads, prefetched
+//            one tile ahead), issues 8 independent 8-byte gathers of x_{t-1}, reduces its
+//            values by the row-start flags in registers, and a block-wide segmented scan
+//            (warp shuffles + one smem step) carries partial row sums across threads.
+//            Row sums land in shared memory; a row-parallel epilogue then writes
+//            x_t = a + g*S coalesced and accumulates Wt*|x_t - x_{t-1}| for eps_t (Eq. (15)).
+//            Rows that continue across tile boundaries leave two partials per tile
+//            (p_in: the row open at the tile start; p_out: the last row started in it).
+//  k_fix     finishes the rows cut by tile boundaries (p_out of the first tile + p_in of
+//            the following ones, in tile order), then the LAST CTA to arrive reduces the
 //            per-CTA eps partials in a fixed order, appends eps_t to the history, updates
 //            gap = ||B|| eps_t (Alg. 2), t += 1, and sets the graph's WHILE
 //            condition (gap > eps && t < max_iters): the stop rule of Eq. (16) / Alg. 2
@@ -24,7 +23,7 @@
 // The readout (Alg. 2) is the same pair of kernels with the epilogue
 // psi_j = (d_j + lambda_j S_j) / N.
 //
-// Determinism: no floating-point atomics; chunk -> warp assignment is static and every
+// Determinism: no floating-point atomics; tile -> CTA assignment is static and every
 // reduction has a fixed order, so two runs give bitwise identical psi and eps_t.
 #include "psi_internal.cuh"
 
@@ -98,166 +97,140 @@ __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 
-// Epilogue for one completed row r with S = sum of x_{t-1} over its followers.
-template <bool READOUT>
-__device__ __forceinline__ void row_epilogue(const SweepArgs& A, int r, double S,
-                                             const double* __restrict__ xs, double* __restrict__ xd,
-                                             unsigned hot_lim, unsigned long long pf,
-                                             unsigned long long pl, double& eps_acc) {
-  if (READOUT) {
-    A.psi[r] = (ld_stream(A.d + r, pf) + ld_stream(A.lam + r, pf) * S) / A.n_users;
-  } else {
-    const unsigned long long px = (unsigned)r < hot_lim ? pl : pf;
-    const double xn = fma(ld_stream(A.g + r, pf), S, ld_stream(A.a + r, pf));
-    eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - ld_hint(xs + r, px));
-    st_hint(xd + r, xn, px);
-  }
-}
+struct TileSmem {
+  double rowsum[kTile];       // S of the rows started in this tile (local row index)
+  double wv[kBlock / 32];     // warp aggregates of the segmented scan
+  int wf[kBlock / 32];
+  int wn[kBlock / 32];
+  double red[33];
+  int next_flag;              // does the edge after this tile start a row?
+};
 
-// Persistent warp-stream sweep: warp gw processes chunks [warp_chunk[gw], warp_chunk[gw+1]).
-// Software pipeline per warp: the gathers of chunk c+1 are in flight while chunk c is
-// reduced and its rows' epilogue runs; the edge words of chunk c+2 are prefetched.
 template <bool READOUT>
-__global__ void __launch_bounds__(kBlock, 4) k_stream(SweepArgs A) {
-  __shared__ double rowsum[kWarps][kChunk + 1];   // slot 0: row open at chunk start
-  __shared__ double red[33];
+__global__ void __launch_bounds__(kBlock, 4) k_tiles(SweepArgs A) {
+  __shared__ TileSmem sm;
   const long long t = A.st->iter;
   const double* __restrict__ xs = (t & 1) ? A.x1 : A.x0;    // x_{t-1}
   double* __restrict__ xd = (t & 1) ? A.x0 : A.x1;          // x_t
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gw = blockIdx.x * kWarps + warp;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long pf = pol_evict_first(), pl = pol_evict_last();
   const unsigned hot_lim = (unsigned)A.hot_lim;
-  double* rs = rowsum[warp];
+  const int ntiles = A.ntiles;
   double eps_acc = 0.0;
 
-  if (gw < A.nwarps) {
-    const int c_beg = A.warp_chunk[gw], c_end = A.warp_chunk[gw + 1];
-    int row = A.warp_row[gw];          // flags before the current chunk = next row to start
-    double carry = 0.0;                // partial of the open row (row - 1)
-    bool open_is_split = false;        // open row began before this warp's range
-    bool pending_first = true;         // no row flag seen yet in this range (warp-uniform)
-    bool has_pin = false;              // this lane closed the split-in row
-    double p_in = 0.0;
-    if (c_beg < c_end) {
-      const unsigned* base = A.edges + (size_t)c_beg * kChunk + lane * kEpt;
-      uint4 u0 = ld_stream4(base, pf), u1 = ld_stream4(base + 4, pf);
-      open_is_split = !(__shfl_sync(kFull, u0.x, 0) & kRowFlag);
-      // gathers of the first chunk
-      unsigned w[kEpt] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-      double v[kEpt];
-      unsigned fl = 0;
-#pragma unroll
-      for (int q = 0; q < kEpt; ++q) {
-        const unsigned lab = w[q] & kLabelMask;
-        fl |= (w[q] >> 31) << q;
-        v[q] = ld_hint(xs + lab, lab < hot_lim ? pl : pf);
-      }
-      if (c_beg + 1 < c_end) {
-        const unsigned* p = A.edges + (size_t)(c_beg + 1) * kChunk + lane * kEpt;
-        u0 = ld_stream4(p, pf);
-        u1 = ld_stream4(p + 4, pf);
-      }
-      for (int c = c_beg; c < c_end; ++c) {
-        // ---- issue chunk c+1's gathers and chunk c+2's edge words before reducing chunk c
-        double vn[kEpt];
-        unsigned fln = 0;
-        if (c + 1 < c_end) {
-          const unsigned wn[kEpt] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-#pragma unroll
-          for (int q = 0; q < kEpt; ++q) {
-            const unsigned lab = wn[q] & kLabelMask;
-            fln |= (wn[q] >> 31) << q;
-            vn[q] = ld_hint(xs + lab, lab < hot_lim ? pl : pf);
-          }
-          if (c + 2 < c_end) {
-            const unsigned* p = A.edges + (size_t)(c + 2) * kChunk + lane * kEpt;
-            u0 = ld_stream4(p, pf);
-            u1 = ld_stream4(p + 4, pf);
-          }
-        }
+  int k = blockIdx.x;
+  uint4 u0 = make_uint4(0, 0, 0, 0), u1 = u0;
+  if (k < ntiles) {
+    const unsigned* p = A.edges + (size_t)k * kTile + tid * kEpt;
+    u0 = ld_stream4(p, pf);
+    u1 = ld_stream4(p + 4, pf);
+  }
+  for (; k < ntiles; k += gridDim.x) {
+    const int f0 = __ldg(A.tile_row + k);
+    const int F = __ldg(A.tile_row + k + 1) - f0;      // rows started in this tile
+    const unsigned w[kEpt] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
 
-        // ---- lane-local reduction by row flags
-        const int nf = __popc(fl);
-        double run = 0.0;
+    // ---- 8 independent gathers of x_{t-1}
+    double v[kEpt];
+    unsigned fl = 0;
 #pragma unroll
-        for (int q = 0; q < kEpt; ++q) {
-          if ((fl >> q) & 1u) run = 0.0;
-          run += v[q];
-        }
-        // ---- warp segmented scan of (has flag, open-row partial) and of flag counts
-        int f_in = nf > 0, n_in = nf;
-        double v_in = run;
+    for (int q = 0; q < kEpt; ++q) {
+      const unsigned lab = w[q] & kLabelMask;
+      fl |= (w[q] >> 31) << q;
+      v[q] = ld_hint(xs + lab, lab < hot_lim ? pl : pf);
+    }
+    if (tid == 0)
+      sm.next_flag = (k + 1 >= ntiles) ? 1 : (int)(ld_stream(A.edges + (size_t)(k + 1) * kTile, pf) >> 31);
+    // ---- prefetch the next tile's edge words
+    const int kn = k + gridDim.x;
+    if (kn < ntiles) {
+      const unsigned* p = A.edges + (size_t)kn * kTile + tid * kEpt;
+      u0 = ld_stream4(p, pf);
+      u1 = ld_stream4(p + 4, pf);
+    }
+
+    // ---- thread-local reduction by row flags
+    const int nf = __popc(fl);
+    double head = 0.0, run = 0.0;
+    bool seen = false;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int n2 = __shfl_up_sync(kFull, n_in, o);
-          const double v2 = __shfl_up_sync(kFull, v_in, o);
-          const int f2 = __shfl_up_sync(kFull, f_in, o);
-          if (lane >= o) {
-            n_in += n2;
-            if (!f_in) v_in += v2;
-            f_in |= f2;
-          }
-        }
-        const double v_full = f_in ? v_in : carry + v_in;
-        const double v_prev = __shfl_up_sync(kFull, v_full, 1);
-        const int F = __shfl_sync(kFull, n_in, 31);          // rows started in this chunk
-        const int n_ex = n_in - nf;
-        // ---- emit completed rows: slot s <-> row (row - 1 + s)
-        int slot = n_ex;
-        run = lane == 0 ? carry : v_prev;
+    for (int q = 0; q < kEpt; ++q) {
+      if ((fl >> q) & 1u) {
+        if (!seen) head = run;
+        seen = true;
+        run = 0.0;
+      }
+      run += v[q];
+    }
+    // scan element: (has flag, partial of the row open at the thread's end)
+    int f_in = nf > 0;
+    double v_in = run;            // tail if a flag was seen, total otherwise
+    int n_in = nf;
 #pragma unroll
-        for (int q = 0; q < kEpt; ++q) {
-          if ((fl >> q) & 1u) {
-            if (slot == 0 && pending_first) {              // the range's first flag
-              if (open_is_split) { p_in = run; has_pin = true; }
-            } else {
-              rs[slot] = run;
-            }
-            ++slot;
-            run = 0.0;
-          }
-          run += v[q];
-        }
-        carry = __shfl_sync(kFull, v_full, 31);              // partial of the new open row
-        __syncwarp();
-        // ---- epilogue over the rows completed in this chunk (rows row-1 .. row+F-2)
-        const int s_lo = pending_first ? 1 : 0;        // slot 0 = previous warp's / split row
-        for (int s = s_lo + lane; s < F; s += 32)
-          row_epilogue<READOUT>(A, row - 1 + s, rs[s], xs, xd, hot_lim, pf, pl, eps_acc);
-        if (F > 0) pending_first = false;
-        row += F;
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < kEpt; ++q) v[q] = vn[q];
-        fl = fln;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n2 = __shfl_up_sync(kFull, n_in, o);
+      const double v2 = __shfl_up_sync(kFull, v_in, o);
+      const int f2 = __shfl_up_sync(kFull, f_in, o);
+      if (lane >= o) {
+        n_in += n2;
+        if (!f_in) v_in += v2;
+        f_in |= f2;
       }
     }
-    // ---- the open row at the end of the range: complete here, or split (k_fix)
-    const unsigned pin_lane = __ballot_sync(kFull, has_pin);
-    p_in = pin_lane ? __shfl_sync(kFull, p_in, __ffs(pin_lane) - 1) : 0.0;
-    const bool any_flag = !pending_first;
-    if (lane == 0) {
-      bool next_flag = true;
-      if (c_end < A.nchunks) next_flag = (ld_stream(A.edges + (size_t)c_end * kChunk, pf) & kRowFlag) != 0;
-      if (!any_flag) {
-        A.p_in[gw] = carry;                       // whole range inside one row
-        A.p_out[gw] = 0.0;
+    if (lane == 31) { sm.wv[warp] = v_in; sm.wf[warp] = f_in; sm.wn[warp] = n_in; }
+    __syncthreads();
+    const int next_flag = sm.next_flag;
+    int nP = 0, fP = 0;
+    double vP = 0.0;
+    for (int w2 = 0; w2 < warp; ++w2) {              // fold of earlier warps, fixed order
+      nP += sm.wn[w2];
+      vP = sm.wf[w2] ? sm.wv[w2] : vP + sm.wv[w2];
+      fP |= sm.wf[w2];
+    }
+    const double v_full = f_in ? v_in : vP + v_in;
+    const double v_prev = __shfl_up_sync(kFull, v_full, 1);
+    double carry = lane == 0 ? vP : v_prev;          // partial of the row open at thread start
+    const int n_ex = nP + n_in - nf;                 // flags before this thread in the tile
+
+    // ---- emit completed row sums
+    int row = n_ex - 1;                              // local index of the open row
+    run = carry;
+#pragma unroll
+    for (int q = 0; q < kEpt; ++q) {
+      if ((fl >> q) & 1u) {
+        if (row >= 0) sm.rowsum[row] = run;
+        else A.p_in[k] = run;                        // first flag of the tile ends row f0-1
+        ++row;
+        run = 0.0;
+      }
+      run += v[q];
+    }
+    if (tid == kBlock - 1) {                         // the tile's last open row
+      if (F == 0) { A.p_in[k] = run; A.p_out[k] = 0.0; }
+      else if (next_flag) { sm.rowsum[F - 1] = run; A.p_out[k] = 0.0; }
+      else A.p_out[k] = run;
+    }
+    __syncthreads();
+
+    // ---- epilogue over the rows completed in this tile (coalesced)
+    const int nrows = (F > 0 && !next_flag) ? F - 1 : F;
+    for (int i = tid; i < nrows; i += kBlock) {
+      const int r = f0 + i;
+      const double Sr = sm.rowsum[i];
+      if (READOUT) {
+        A.psi[r] = (ld_stream(A.d + r, pf) + ld_stream(A.lam + r, pf) * Sr) / A.n_users;
       } else {
-        A.p_in[gw] = p_in;
-        if (next_flag) {
-          A.p_out[gw] = 0.0;
-          if (c_beg < c_end) row_epilogue<READOUT>(A, row - 1, carry, xs, xd, hot_lim, pf, pl, eps_acc);
-        } else {
-          A.p_out[gw] = carry;
-        }
+        const unsigned long long px = (unsigned)r < hot_lim ? pl : pf;
+        const double xn = fma(ld_stream(A.g + r, pf), Sr, ld_stream(A.a + r, pf));
+        eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - ld_hint(xs + r, px));
+        st_hint(xd + r, xn, px);
       }
     }
   }
 
   if (!READOUT) {
-    const double tot = block_sum<kBlock>(eps_acc, red);
-    if (threadIdx.x == 0) A.eps_part1[blockIdx.x] = tot;
+    const double tot = block_sum<kBlock>(eps_acc, sm.red);
+    if (tid == 0) A.eps_part1[blockIdx.x] = tot;
   }
 }
 
@@ -338,16 +311,18 @@ __global__ void k_init(SweepArgs A, int n) {
 
 }  // namespace
 
-int sweep_grid() {
+int sweep_grid(int ntiles) {
   static int occ = -1, sms = 0;
   if (occ < 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stream<false>, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiles<false>, kBlock, 0);
     if (occ < 1) occ = 1;
   }
-  return sms * occ;
+  long long g = (long long)sms * occ;
+  if (g > ntiles) g = ntiles;
+  return g < 1 ? 1 : (int)g;
 }
 
 int fix_grid(int nsplit) {
@@ -360,7 +335,7 @@ int fix_grid(int nsplit) {
 }
 
 void* sweep_kernel_ptr(bool readout) {
-  return readout ? (void*)k_stream<true> : (void*)k_stream<false>;
+  return readout ? (void*)k_tiles<true> : (void*)k_tiles<false>;
 }
 void* fix_kernel_ptr(bool readout) {
   return readout ? (void*)k_fix<true> : (void*)k_fix<false>;
