@@ -74,6 +74,12 @@ typedef struct psi_info {
   int64_t grid;           /* persistent CTAs per sweep launch */
   int64_t device_bytes;   /* device memory held by the context */
   int64_t relabeled;      /* 1 if users were relabeled for locality at ingest */
+  int64_t block;          /* threads per sweep CTA (tile groups x 256) */
+  int64_t hot_smem;       /* hottest labels of x gathered from each CTA's shared-memory copy */
+  int64_t n_heavy;        /* heavy rows (labels [0, n_heavy)) served by the staged-segment kernel */
+  int64_t heavy_entries;  /* (heavy row, follower < heavy_labels) pairs summed from shared memory */
+  int64_t heavy_panels;   /* work panels of the staged-segment kernel */
+  int64_t heavy_labels;   /* H: labels of x staged through shared memory per sweep */
 } psi_info;
 
 /*
@@ -139,12 +145,14 @@ psi_status psi_get_residual_history(const psi_ctx* ctx, double* out, int64_t cap
                                     int64_t* len_out);
 
 /* psi_time_sweep -- measurement entry: runs `sweeps` sweeps of Eq. (14) from s_0 = c
- * (eps = 0) as direct stream launches and returns the average device time of the
- * sweep's two kernels, each bracketed by CUDA events on the context's stream:
- * *tiles_ms = merge-path gather + epilogue (k_tiles), *fix_ms = split rows + eps_t
- * reduction + stop rule (k_fix).  Leaves no psi (call psi_iterate afterwards).
- * PSI_E_INVALID_ARG if ctx is NULL or sweeps < 1. */
-psi_status psi_time_sweep(psi_ctx* ctx, int64_t sweeps, double* tiles_ms, double* fix_ms);
+ * (eps = 0) as direct stream launches and returns the average device time of each of the
+ * sweep's kernels, bracketed by CUDA events on the context's stream: *heavy_ms = staged
+ * shared-memory sums of the heavy rows (k_heavy; 0 if the graph has no heavy rows),
+ * *tiles_ms = edge-stream gather + epilogue (k_tiles), *fix_ms = split rows + eps_t
+ * reduction + stop rule (k_fix).  Any output pointer may be NULL.  Leaves no psi (call
+ * psi_iterate afterwards).  PSI_E_INVALID_ARG if ctx is NULL or sweeps < 1. */
+psi_status psi_time_sweep(psi_ctx* ctx, int64_t sweeps, double* heavy_ms, double* tiles_ms,
+                          double* fix_ms);
 
 /* psi_get_info -- sizes, norms and timings (see psi_info). */
 psi_status psi_get_info(const psi_ctx* ctx, psi_info* out);

@@ -57,7 +57,10 @@ class psi_info(ctypes.Structure):
                 ("iterate_ms", ctypes.c_double), ("last_iters", ctypes.c_int64),
                 ("last_gap", ctypes.c_double), ("num_tiles", ctypes.c_int64),
                 ("num_long_rows", ctypes.c_int64), ("grid", ctypes.c_int64),
-                ("device_bytes", ctypes.c_int64), ("relabeled", ctypes.c_int64)]
+                ("device_bytes", ctypes.c_int64), ("relabeled", ctypes.c_int64),
+                ("block", ctypes.c_int64), ("hot_smem", ctypes.c_int64),
+                ("n_heavy", ctypes.c_int64), ("heavy_entries", ctypes.c_int64),
+                ("heavy_panels", ctypes.c_int64), ("heavy_labels", ctypes.c_int64)]
 
 
 _lib = None
@@ -85,7 +88,8 @@ def load_library(build_if_stale: bool = True):
     lib.psi_get_series.argtypes = [vp, vp, ci]
     lib.psi_get_residual_history.argtypes = [vp, vp, i64, ctypes.POINTER(i64)]
     lib.psi_get_info.argtypes = [vp, ctypes.POINTER(psi_info)]
-    lib.psi_time_sweep.argtypes = [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl)]
+    lib.psi_time_sweep.argtypes = [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl),
+                                   ctypes.POINTER(dbl)]
     lib.psi_destroy.argtypes = [vp]
     lib.psi_destroy.restype = None
     lib.psi_last_error.restype = ctypes.c_char_p
@@ -187,12 +191,14 @@ class PsiGraph:
         return out
 
     def time_sweep(self, sweeps: int = 20):
-        """(k_tiles ms, k_fix ms): average per-launch device time over `sweeps` sweeps."""
-        a, b = ctypes.c_double(), ctypes.c_double()
-        st = self._lib.psi_time_sweep(self._ctx, int(sweeps), ctypes.byref(a), ctypes.byref(b))
+        """(k_heavy ms, k_tiles ms, k_fix ms): average per-launch device time over `sweeps`
+        sweeps (CUDA events on the context's stream around each launch)."""
+        h, a, b = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        st = self._lib.psi_time_sweep(self._ctx, int(sweeps), ctypes.byref(h), ctypes.byref(a),
+                                      ctypes.byref(b))
         if st != PSI_OK:
             raise PsiError(st, _err(self._lib))
-        return a.value, b.value
+        return h.value, a.value, b.value
 
     def info(self) -> dict:
         inf = psi_info()

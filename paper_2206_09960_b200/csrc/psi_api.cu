@@ -64,6 +64,7 @@ struct psi_ctx {
   LoopState* h_st = nullptr;     // pinned
   LoopParams* h_prm = nullptr;   // pinned
   int grid1 = 0, grid2 = 0;
+  TilesCfg tc{};                 // launch shape of k_tiles (sweep + readout)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -73,6 +74,9 @@ struct psi_ctx {
   double ingest_ms = 0, iterate_ms = 0;
   size_t device_bytes = 0;
   long long hot_lim = 0;         // x labels kept in L2 with evict_last (both buffers)
+  double* hhot = nullptr;        // [n_heavy] heavy rows' sums over followers < H (k_heavy)
+  int heavy_grid = 0;
+  size_t heavy_smem = 0;
 };
 
 namespace {
@@ -83,7 +87,8 @@ void free_ctx(psi_ctx* c) {
   if (c->graph) cudaGraphDestroy(c->graph);
   void* ptrs[] = {c->g.edges, c->g.tile_row, c->g.a0, c->g.a1, c->g.g, c->g.wt, c->g.d1,
                   c->g.lam, c->g.psi, c->g.old_of_new, c->g.split, c->x[0], c->x[1],
-                  c->p_in, c->p_out, c->eps_part1, c->eps_part2, c->history, c->st, c->prm};
+                  c->p_in, c->p_out, c->eps_part1, c->eps_part2, c->history, c->st, c->prm,
+                  c->hhot, c->g.h_ent, c->g.h_loff, c->g.h_prow, c->g.h_rslot, c->g.h_wslot};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -117,6 +122,20 @@ SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   A.eps_part1 = c->eps_part1;
   A.eps_part2 = c->eps_part2;
   A.grid1 = c->grid1;
+  A.hot_smem = c->tc.hot_smem;
+  A.l1_lim = c->tc.l1_lim;
+  A.single_lo = getenv("PSI_SINGLE_L1") && atoi(getenv("PSI_SINGLE_L1")) == 0 ? 0x7fffffff
+                                                                             : (int)c->g.single_lo;
+  A.st_last = getenv("PSI_ST_LAST") ? atoi(getenv("PSI_ST_LAST")) : 0;
+  A.n_heavy = (int)c->g.n_heavy;
+  A.hhot = c->hhot;
+  A.heavy.ent = c->g.h_ent;
+  A.heavy.loff = c->g.h_loff;
+  A.heavy.prow = c->g.h_prow;
+  A.heavy.rslot = c->g.h_rslot;
+  A.heavy.wslot = c->g.h_wslot;
+  A.heavy.npanels = c->g.npanels;
+  A.heavy.nseg = c->g.nseg;
   A.st = c->st;
   A.prm = c->prm;
   A.cond = cond;
@@ -125,12 +144,13 @@ SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
 }
 
 cudaError_t add_kernel(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode_t* dep, size_t ndep,
-                       void* fn, int grid, int block, SweepArgs* args, int* n_extra) {
+                       void* fn, int grid, int block, SweepArgs* args, int* n_extra,
+                       size_t smem = 0) {
   cudaKernelNodeParams p{};
   p.func = fn;
   p.gridDim = dim3(grid);
   p.blockDim = dim3(block);
-  p.sharedMemBytes = 0;
+  p.sharedMemBytes = (unsigned)smem;
   void* kp[2] = {args, n_extra};
   p.kernelParams = kp;
   return cudaGraphAddKernelNode(node, g, dep, ndep, &p);
@@ -155,19 +175,29 @@ psi_status build_graph_exec(psi_ctx* c) {
   cp.conditional.size = 1;
   API_CK(cudaGraphAddNode(&n_while, c->graph, &n_init, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
-  cudaGraphNode_t b1, b2;
-  API_CK(add_kernel(body, &b1, nullptr, 0, sweep_kernel_ptr(false), c->grid1, kBlock, &A, nullptr));
+  cudaGraphNode_t b0, b1, b2, n_r0;
+  const bool hv = c->g.n_heavy > 0;
+  if (hv)
+    API_CK(add_kernel(body, &b0, nullptr, 0, heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock, &A,
+                      nullptr, c->heavy_smem));
+  API_CK(add_kernel(body, &b1, hv ? &b0 : nullptr, hv ? 1 : 0, c->tc.sweep, c->grid1, c->tc.block,
+                    &A, nullptr, c->tc.smem));
   API_CK(add_kernel(body, &b2, &b1, 1, fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr));
 
-  API_CK(add_kernel(c->graph, &n_r1, &n_while, 1, sweep_kernel_ptr(true), c->grid1, kBlock, &A, nullptr));
+  if (hv)
+    API_CK(add_kernel(c->graph, &n_r0, &n_while, 1, heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock,
+                      &A, nullptr, c->heavy_smem));
+  API_CK(add_kernel(c->graph, &n_r1, hv ? &n_r0 : &n_while, 1, c->tc.readout, c->grid1,
+                    c->tc.block, &A, nullptr, c->tc.smem));
   API_CK(add_kernel(c->graph, &n_r2, &n_r1, 1, fix_kernel_ptr(true), c->grid2, kFixBlock, &A, nullptr));
   API_CK(cudaGraphInstantiate(&c->exec, c->graph, 0));
   return PSI_OK;
 }
 
-cudaError_t launch(void* fn, int grid, int block, SweepArgs* A, int* extra, cudaStream_t s) {
+cudaError_t launch(void* fn, int grid, int block, SweepArgs* A, int* extra, cudaStream_t s,
+                   size_t smem = 0) {
   void* kp[2] = {A, extra};
-  return cudaLaunchKernel(fn, dim3(grid), dim3(block), kp, 0, s);
+  return cudaLaunchKernel(fn, dim3(grid), dim3(block), kp, smem, s);
 }
 
 // Direct stream launches of the same kernels (no CUDA graph, no conditional node): used by
@@ -185,13 +215,19 @@ psi_status iterate_direct(psi_ctx* c) {
   const long long max_iters = c->h_prm->max_iters;
   bool cont = 1.0 > eps && max_iters > 0;
   while (cont) {
-    API_CK(launch(sweep_kernel_ptr(false), c->grid1, kBlock, &A, nullptr, c->stream));
+    if (c->g.n_heavy > 0)
+      API_CK(launch(heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock, &A, nullptr, c->stream,
+                    c->heavy_smem));
+    API_CK(launch(c->tc.sweep, c->grid1, c->tc.block, &A, nullptr, c->stream, c->tc.smem));
     API_CK(launch(fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr, c->stream));
     API_CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(LoopState), cudaMemcpyDeviceToHost, c->stream));
     API_CK(cudaStreamSynchronize(c->stream));
     cont = !(c->h_st->status & 1) && c->h_st->gap > eps && c->h_st->iter < max_iters;
   }
-  API_CK(launch(sweep_kernel_ptr(true), c->grid1, kBlock, &A, nullptr, c->stream));
+  if (c->g.n_heavy > 0)
+    API_CK(launch(heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock, &A, nullptr, c->stream,
+                  c->heavy_smem));
+  API_CK(launch(c->tc.readout, c->grid1, c->tc.block, &A, nullptr, c->stream, c->tc.smem));
   API_CK(launch(fix_kernel_ptr(true), c->grid2, kFixBlock, &A, nullptr, c->stream));
   return PSI_OK;
 }
@@ -317,7 +353,8 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
 
   // Iteration buffers.
-  c->grid1 = sweep_grid(c->g.ntiles);
+  c->tc = tiles_config(c->g.ntiles, n);
+  c->grid1 = c->tc.grid;
   {
     // Hot prefix of x kept in L2 (evict_last) in BOTH ping-pong buffers: PSI_HOT_MB per
     // buffer (default: a third of L2 each), never more than the users with >= 2 leaders.
@@ -334,6 +371,17 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
     if (fetch > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)fetch);
   }
   c->grid2 = fix_grid(c->g.nsplit);
+  if (c->g.n_heavy > 0) {
+    int dev = 0, sms = 0;
+    B_CK(cudaGetDevice(&dev));
+    B_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    c->heavy_grid = std::max(1, std::min(sms, c->g.npanels));
+    c->heavy_smem = heavy_smem_bytes(c->g.nseg);
+    B_CK(cudaFuncSetAttribute(heavy_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)c->heavy_smem));
+    B_CK(cudaMalloc(&c->hhot, (size_t)c->g.n_heavy * sizeof(double)));
+    B_CK(cudaMemsetAsync(c->hhot, 0, (size_t)c->g.n_heavy * sizeof(double), c->stream));
+  }
   B_CK(cudaMalloc(&c->x[0], (n + 1) * sizeof(double)));      // + sentinel x[n] = 0
   B_CK(cudaMalloc(&c->x[1], (n + 1) * sizeof(double)));
   B_CK(cudaMemsetAsync(c->x[0] + n, 0, sizeof(double), c->stream));
@@ -470,10 +518,17 @@ psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
   out->grid = c->grid1;
   out->device_bytes = (int64_t)c->device_bytes;
   out->relabeled = c->g.relabeled;
+  out->block = c->tc.block;
+  out->hot_smem = c->tc.hot_smem;
+  out->n_heavy = c->g.n_heavy;
+  out->heavy_entries = c->g.heavy_entries;
+  out->heavy_panels = c->g.npanels;
+  out->heavy_labels = (int64_t)c->g.nseg * kSeg;
   return PSI_OK;
 }
 
-psi_status psi_time_sweep(psi_ctx* c, int64_t sweeps, double* tiles_ms, double* fix_ms) {
+psi_status psi_time_sweep(psi_ctx* c, int64_t sweeps, double* heavy_ms, double* tiles_ms,
+                          double* fix_ms) {
   g_err.clear();
   if (!c || sweeps < 1) return fail(PSI_E_INVALID_ARG, "ctx NULL or sweeps < 1");
   psi_status hs = ensure_history(c, sweeps);
@@ -490,27 +545,34 @@ psi_status psi_time_sweep(psi_ctx* c, int64_t sweeps, double* tiles_ms, double* 
   int init_grid = (int)std::min<long long>((c->g.n_act + 255) / 256, 148LL * 8);
   if (init_grid < 1) init_grid = 1;
   API_CK(launch(init_kernel_ptr(), init_grid, 256, &A, &n_int, c->stream));
-  cudaEvent_t e[3];
+  cudaEvent_t e[4];
   for (auto& x : e) API_CK(cudaEventCreate(&x));
-  double t1 = 0, t2 = 0;
+  double t0 = 0, t1 = 0, t2 = 0;
   psi_status rc = PSI_OK;
+  const bool hv = c->g.n_heavy > 0;
   for (int64_t k = 0; k < sweeps && rc == PSI_OK; ++k) {
-    float a = 0, b = 0;
+    float a = 0, b = 0, d = 0;
     if (cudaEventRecord(e[0], c->stream) != cudaSuccess ||
-        launch(sweep_kernel_ptr(false), c->grid1, kBlock, &A, nullptr, c->stream) != cudaSuccess ||
+        (hv && launch(heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock, &A, nullptr, c->stream,
+                      c->heavy_smem) != cudaSuccess) ||
         cudaEventRecord(e[1], c->stream) != cudaSuccess ||
-        launch(fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr, c->stream) != cudaSuccess ||
+        launch(c->tc.sweep, c->grid1, c->tc.block, &A, nullptr, c->stream, c->tc.smem) != cudaSuccess ||
         cudaEventRecord(e[2], c->stream) != cudaSuccess ||
-        cudaEventSynchronize(e[2]) != cudaSuccess ||
-        cudaEventElapsedTime(&a, e[0], e[1]) != cudaSuccess ||
-        cudaEventElapsedTime(&b, e[1], e[2]) != cudaSuccess)
+        launch(fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr, c->stream) != cudaSuccess ||
+        cudaEventRecord(e[3], c->stream) != cudaSuccess ||
+        cudaEventSynchronize(e[3]) != cudaSuccess ||
+        cudaEventElapsedTime(&d, e[0], e[1]) != cudaSuccess ||
+        cudaEventElapsedTime(&a, e[1], e[2]) != cudaSuccess ||
+        cudaEventElapsedTime(&b, e[2], e[3]) != cudaSuccess)
       rc = fail(PSI_E_CUDA, "psi_time_sweep: %s", cudaGetErrorString(cudaGetLastError()));
+    t0 += d;
     t1 += a;
     t2 += b;
   }
   for (auto& x : e) cudaEventDestroy(x);
   if (rc != PSI_OK) return rc;
   c->have_psi = false;     // the iterate state is mid-solve: require a new psi_iterate
+  if (heavy_ms) *heavy_ms = hv ? t0 / sweeps : 0.0;
   if (tiles_ms) *tiles_ms = t1 / sweeps;
   if (fix_ms) *fix_ms = t2 / sweeps;
   return PSI_OK;

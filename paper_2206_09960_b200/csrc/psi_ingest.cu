@@ -34,8 +34,11 @@
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 namespace psi {
 namespace {
@@ -44,7 +47,7 @@ enum : int {
   F_RP0 = 1, F_RPN = 2, F_RPMONO = 4, F_RANGE = 8, F_SELF = 16, F_ORDER = 32, F_ACT = 64,
 };
 // user classes of the relabel
-enum : unsigned char { C_HOT = 0, C_SINGLE = 1, C_ROOT = 2, C_INACTIVE = 3 };
+enum : unsigned char { C_HOT = 0, C_SINGLE = 1, C_ROOT = 2, C_INACTIVE = 3, C_HEAVY = 4 };
 
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -201,8 +204,8 @@ __global__ void k_stage_keys(int stage, const unsigned char* cls, const int* nle
     const unsigned char c = cls[u];
     unsigned char f = 0;
     unsigned long long k = (unsigned long long)u;
-    if (stage == 0) {
-      f = c == C_HOT;
+    if (stage == 0 || stage == 5) {
+      f = c == (stage == 0 ? C_HOT : C_HEAVY);
       k |= (unsigned long long)(0x7fffffff - nlead[u]) << 32;
     } else if (stage == 1) {
       f = c == C_ROOT;
@@ -233,48 +236,141 @@ __global__ void k_assign(const unsigned long long* sel, long long cnt, int base,
   }
 }
 
-// warp per new active row r: #active followers, and K_r = sum of a_n over follower-less ones
+// warp per (old) user: number of followers that are active (have followers themselves)
+__global__ void k_active_count(const int* rp, const int* idx, const unsigned char* cls, int n,
+                               int* act) {
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(u, n) {
+    const int b = rp[u], e = rp[u + 1];
+    int c = 0;
+    for (int q = b + lane; q < e; q += 32) c += cls[idx[q]] != C_INACTIVE;
+    c = __reduce_add_sync(kFull, c);
+    if (lane == 0) act[u] = c;
+  }
+}
+
+// heavy rows: active users with >= min_act active followers; recount the classes
+__global__ void k_mark_heavy(const int* act, int n, int min_act, unsigned char* cls,
+                             unsigned long long* counts) {
+  GRID_STRIDE(u, n) {
+    unsigned char c = cls[u];
+    if (c != C_INACTIVE && act[u] >= min_act) cls[u] = c = C_HEAVY;
+    atomicAdd(counts + c, 1ull);
+  }
+}
+
+// warp per new active row r: #active followers in the edge stream (for heavy rows r <
+// n_heavy only those with label >= H; the others, hc[r], go to k_heavy), and
+// K_r = sum of a_n over follower-less followers
 __global__ void k_row_count(const int* rp, const int* idx, const int* old_of_new,
-                            const unsigned char* cls, const double* a_old, int n_act, int* cnt,
-                            double* K) {
+                            const unsigned char* cls, const int* new_of_old, const double* a_old,
+                            int n_act, int n_heavy, int H, int* cnt, long long* hc, double* K) {
   const int lane = threadIdx.x & 31;
   WARP_STRIDE(r, n_act) {
     const int o = old_of_new[r];
     const int b = rp[o], e = rp[o + 1];
-    int c = 0;
+    const bool heavy = r < n_heavy;
+    int c = 0, h = 0;
     double k = 0.0;
     for (int q = b + lane; q < e; q += 32) {
       const int v = idx[q];
-      if (cls[v] == C_INACTIVE) k += a_old[v]; else ++c;
+      if (cls[v] == C_INACTIVE) k += a_old[v];
+      else if (heavy && new_of_old[v] < H) ++h;
+      else ++c;
     }
     c = __reduce_add_sync(kFull, c);
+    h = __reduce_add_sync(kFull, h);
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) k += __shfl_xor_sync(kFull, k, s);
-    if (lane == 0) { cnt[r] = c > 0 ? c : 1; K[r] = k; }   // 0 -> one pseudo edge
+    if (lane == 0) {
+      cnt[r] = c > 0 ? c : 1;      // 0 -> one pseudo edge
+      K[r] = k;
+      if (heavy) hc[r] = h;
+    }
   }
 }
 
-// warp per new active row: write the active followers' new labels (unsorted, stable); a row
-// with no active follower gets one pseudo edge to the sentinel label n (x[n] = 0).
+// warp per new active row: write the active followers' new labels (unsorted, stable) to the
+// edge stream -- heavy rows: only labels >= H; their labels < H go to hot[hoff[r]...].  A row
+// with no stream follower gets one pseudo edge to the sentinel label n (x[n] = 0).
 __global__ void k_row_fill(const int* rp, const int* idx, const int* old_of_new,
                            const unsigned char* cls, const int* new_of_old, const int* rp_new,
-                           int n_act, int n, int* idx_new) {
+                           int n_act, int n, int n_heavy, int H, const long long* hoff,
+                           int* idx_new, int* hot) {
   const int lane = threadIdx.x & 31;
   WARP_STRIDE(r, n_act) {
     const int o = old_of_new[r];
     const int b = rp[o], e = rp[o + 1];
     const int start = rp_new[r];
+    const bool heavy = r < n_heavy;
     int out = start;
+    long long hout = heavy ? hoff[r] : 0;
     for (int q0 = b; q0 < e; q0 += 32) {
       const int q = q0 + lane;
       int v = -1;
       bool act = false;
       if (q < e) { v = idx[q]; act = cls[v] != C_INACTIVE; }
-      const unsigned mask = __ballot_sync(kFull, act);
-      if (act) idx_new[out + __popc(mask & ((1u << lane) - 1u))] = new_of_old[v];
-      out += __popc(mask);
+      const int nv = act ? new_of_old[v] : 0;
+      const bool is_hot = act && heavy && nv < H;
+      const bool is_str = act && !is_hot;
+      const unsigned m1 = __ballot_sync(kFull, is_str), m2 = __ballot_sync(kFull, is_hot);
+      const unsigned below = (1u << lane) - 1u;
+      if (is_str) idx_new[out + __popc(m1 & below)] = nv;
+      if (is_hot) hot[hout + __popc(m2 & below)] = nv;
+      out += __popc(m1);
+      hout += __popc(m2);
     }
     if (lane == 0 && out == start) idx_new[start] = n;
+  }
+}
+
+// warp per heavy row: entry keys (list << kEntBits) | (slot << kSegShift) | (label % kSeg);
+// list = (panel * kHeavyWarps + owner warp of the slot) * nseg + segment.  The i-th hot
+// follower of row r goes to slot rslot[r].x + i % rslot[r].y (round-robin virtual rows).
+__global__ void k_heavy_keys(const int* hot, const long long* hoff, const int2* rslot,
+                             const int* row_panel, const int* pslot_base, const unsigned char* slot_warp,
+                             int n_heavy, int nseg, unsigned long long* keys) {
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(r, n_heavy) {
+    const long long b = hoff[r], e = hoff[r + 1];
+    const int2 sn = rslot[r];
+    const int p = row_panel[r];
+    const int base = pslot_base[p];
+    for (long long q = b + lane; q < e; q += 32) {
+      const unsigned lab = (unsigned)hot[q];
+      const int slot = sn.x + (int)((q - b) % sn.y);
+      const unsigned long long list =
+          ((unsigned long long)p * kHeavyWarps + slot_warp[base + slot]) * nseg + (lab >> kSegShift);
+      keys[q] = (list << kEntBits) | ((unsigned long long)slot << kSegShift) | (lab & (kSeg - 1));
+    }
+  }
+}
+
+// first position of every list in the sorted keys (lower bound), lists 0..nlists
+__global__ void k_list_start(const unsigned long long* keys, long long nk, long long nlists,
+                             long long* lstart) {
+  GRID_STRIDE(L, nlists + 1) {
+    long long lo = 0, hi = nk;
+    while (lo < hi) {
+      const long long mid = (lo + hi) >> 1;
+      if ((long long)(keys[mid] >> kEntBits) < L) lo = mid + 1; else hi = mid;
+    }
+    lstart[L] = lo;
+  }
+}
+
+__global__ void k_list_padded(const long long* lstart, long long nlists, long long* plen) {
+  GRID_STRIDE(L, nlists) plen[L] = (lstart[L + 1] - lstart[L] + 7) & ~7ll;   // 32-byte lists
+}
+
+__global__ void k_fill_u32(unsigned* p, long long n, unsigned v) { GRID_STRIDE(i, n) p[i] = v; }
+
+__global__ void k_heavy_fill(const unsigned long long* keys, long long nk, const long long* lstart,
+                             const long long* loff, unsigned* ent) {
+  GRID_STRIDE(i, nk) {
+    const unsigned long long k = keys[i];
+    const long long L = (long long)(k >> kEntBits);
+    ent[loff[L] + (i - lstart[L])] = (unsigned)(k & ((1ull << kEntBits) - 1));
   }
 }
 
@@ -350,6 +446,12 @@ int grid_for(long long work, int block, int cap = 148 * 16) {
   return (int)g;
 }
 
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
 }  // namespace
 
 #define IG_CK(call)                                                                  \
@@ -361,6 +463,138 @@ int grid_for(long long work, int block, int cap = 148 * 16) {
       return e_ == cudaErrorMemoryAllocation ? PSI_E_OOM : PSI_E_CUDA;               \
     }                                                                                \
   } while (0)
+
+namespace {
+
+// Heavy-row plan (psi_heavy.cu): panels of <= kHeavySlots slots and ~e_panel hot entries,
+// virtual rows of <= vmax entries, contiguous slot ranges per consumer warp balanced by
+// entries; then the entry lists (panel, segment, warp) sorted by (slot, label).
+int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcnt, Tmp& hoff,
+                     cudaStream_t s, char* msg, size_t msg_len) {
+  const int nseg = out.nseg;
+  std::vector<long long> hc(NH);
+  IG_CK(cudaMemcpyAsync(hc.data(), hcnt.p, (size_t)NH * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  // hot followers of each heavy row sorted by label (the k_row_fill order is unsorted)
+  if (n_ent > 0) {
+    Tmp tmp2, seg_tmp;
+    IG_CK(tmp2.alloc((size_t)n_ent * sizeof(int)));
+    cub::DoubleBuffer<int> kb(hot.as<int>(), tmp2.as<int>());
+    size_t tb = 0;
+    IG_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, kb, (int)n_ent, NH, hoff.as<long long>(),
+                                             hoff.as<long long>() + 1, s));
+    IG_CK(seg_tmp.alloc(tb));
+    IG_CK(cub::DeviceSegmentedSort::SortKeys(seg_tmp.p, tb, kb, (int)n_ent, NH, hoff.as<long long>(),
+                                             hoff.as<long long>() + 1, s));
+    if (kb.Current() != hot.as<int>())
+      IG_CK(cudaMemcpyAsync(hot.p, kb.Current(), (size_t)n_ent * sizeof(int),
+                            cudaMemcpyDeviceToDevice, s));
+  }
+  IG_CK(cudaStreamSynchronize(s));
+
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long pps = std::max(1, env_int("PSI_HEAVY_PPS", kDefaultHeavyPPS));
+  const long long e_panel = std::max<long long>((n_ent + pps * sms - 1) / (pps * sms), 32768);
+  const long long vmax = std::max<long long>(e_panel / (2 * kHeavyWarps), 64);
+  std::vector<int> prow{0}, row_panel(NH), pslot_base{0}, wslot;
+  std::vector<int2> rslot(NH);
+  std::vector<unsigned char> slot_warp;
+  std::vector<long long> slot_w;
+  long long p_ent = 0;
+  auto close_panel = [&](int r_end) {
+    const int slots = (int)slot_w.size();
+    long long T = 0;
+    for (long long x : slot_w) T += x;
+    std::vector<int> ws(kHeavyWarps + 1, slots);
+    ws[0] = 0;
+    long long acc = 0;
+    int w = 1;
+    for (int k = 0; k < slots && w < kHeavyWarps; ++k) {
+      acc += slot_w[k];
+      while (w < kHeavyWarps && acc * kHeavyWarps >= T * w) ws[w++] = k + 1;
+    }
+    int owner = 0;
+    for (int k = 0; k < slots; ++k) {
+      while (owner + 1 < kHeavyWarps && ws[owner + 1] <= k) ++owner;
+      slot_warp.push_back((unsigned char)owner);
+    }
+    wslot.insert(wslot.end(), ws.begin(), ws.end());
+    prow.push_back(r_end);
+    pslot_base.push_back(pslot_base.back() + slots);
+    slot_w.clear();
+    p_ent = 0;
+  };
+  for (int r = 0; r < NH; ++r) {
+    long long nv = hc[r] > 0 ? (hc[r] + vmax - 1) / vmax : 0;
+    if (nv > kHeavySlots) nv = kHeavySlots;
+    if (r > prow.back() && ((long long)slot_w.size() + nv > kHeavySlots || p_ent + hc[r] > e_panel))
+      close_panel(r);
+    rslot[r] = make_int2((int)slot_w.size(), (int)nv);
+    row_panel[r] = (int)prow.size() - 1;
+    for (long long k = 0; k < nv; ++k) slot_w.push_back(hc[r] / nv + (k < hc[r] % nv ? 1 : 0));
+    p_ent += hc[r];
+  }
+  close_panel(NH);
+  const int npanels = (int)prow.size() - 1;
+  out.npanels = npanels;
+  out.heavy_entries = n_ent;
+
+  IG_CK(cudaMalloc(&out.h_prow, prow.size() * sizeof(int)));
+  IG_CK(cudaMalloc(&out.h_rslot, (size_t)NH * sizeof(int2)));
+  IG_CK(cudaMalloc(&out.h_wslot, wslot.size() * sizeof(int)));
+  IG_CK(cudaMemcpyAsync(out.h_prow, prow.data(), prow.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  IG_CK(cudaMemcpyAsync(out.h_rslot, rslot.data(), (size_t)NH * sizeof(int2), cudaMemcpyHostToDevice, s));
+  IG_CK(cudaMemcpyAsync(out.h_wslot, wslot.data(), wslot.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+
+  const long long nlists = (long long)npanels * nseg * kHeavyWarps;
+  IG_CK(cudaMalloc(&out.h_loff, (size_t)(nlists + 1) * sizeof(long long)));
+  Tmp keys, keys2, rpan, psb, sw, lstart, plen, scan_tmp, sort_tmp;
+  IG_CK(keys.alloc((size_t)std::max<long long>(n_ent, 1) * 8));
+  IG_CK(keys2.alloc((size_t)std::max<long long>(n_ent, 1) * 8));
+  IG_CK(rpan.alloc((size_t)NH * sizeof(int)));
+  IG_CK(psb.alloc(pslot_base.size() * sizeof(int)));
+  IG_CK(sw.alloc(std::max<size_t>(slot_warp.size(), 1)));
+  IG_CK(cudaMemcpyAsync(rpan.p, row_panel.data(), (size_t)NH * sizeof(int), cudaMemcpyHostToDevice, s));
+  IG_CK(cudaMemcpyAsync(psb.p, pslot_base.data(), pslot_base.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  if (!slot_warp.empty())
+    IG_CK(cudaMemcpyAsync(sw.p, slot_warp.data(), slot_warp.size(), cudaMemcpyHostToDevice, s));
+  k_heavy_keys<<<grid_for((long long)NH * 32, 256), 256, 0, s>>>(
+      hot.as<int>(), hoff.as<long long>(), out.h_rslot, rpan.as<int>(), psb.as<int>(),
+      sw.as<unsigned char>(), NH, nseg, keys.as<unsigned long long>());
+  int end_bit = kEntBits;
+  while ((1LL << (end_bit - kEntBits)) <= nlists) ++end_bit;
+  cub::DoubleBuffer<unsigned long long> kb(keys.as<unsigned long long>(), keys2.as<unsigned long long>());
+  if (n_ent > 0) {
+    size_t tb = 0;
+    IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, (int)n_ent, 0, end_bit, s));
+    IG_CK(sort_tmp.alloc(tb));
+    IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp.p, tb, kb, (int)n_ent, 0, end_bit, s));
+  }
+  IG_CK(lstart.alloc((size_t)(nlists + 1) * sizeof(long long)));
+  IG_CK(plen.alloc((size_t)(nlists + 1) * sizeof(long long)));
+  k_list_start<<<grid_for(nlists + 1, 256), 256, 0, s>>>(kb.Current(), n_ent, nlists,
+                                                        lstart.as<long long>());
+  IG_CK(cudaMemsetAsync(plen.as<long long>() + nlists, 0, sizeof(long long), s));
+  k_list_padded<<<grid_for(nlists, 256), 256, 0, s>>>(lstart.as<long long>(), nlists,
+                                                      plen.as<long long>());
+  size_t sb = 0;
+  IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, plen.as<long long>(), out.h_loff, nlists + 1, s));
+  IG_CK(scan_tmp.alloc(sb));
+  IG_CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, sb, plen.as<long long>(), out.h_loff, nlists + 1, s));
+  long long total = 0;
+  IG_CK(cudaMemcpyAsync(&total, out.h_loff + nlists, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  IG_CK(cudaStreamSynchronize(s));
+  IG_CK(cudaMalloc(&out.h_ent, (size_t)std::max<long long>(total, 4) * sizeof(unsigned)));
+  k_fill_u32<<<grid_for(total, 256), 256, 0, s>>>(out.h_ent, total, kNullEntry);
+  k_heavy_fill<<<grid_for(n_ent, 256), 256, 0, s>>>(kb.Current(), n_ent, lstart.as<long long>(),
+                                                   out.h_loff, out.h_ent);
+  IG_CK(cudaStreamSynchronize(s));
+  IG_CK(cudaGetLastError());
+  return PSI_OK;
+}
+
+}  // namespace
 
 int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
            const double* lam, const double* mu, cudaStream_t s, IngestOut& out, char* msg,
@@ -460,6 +694,33 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   out.n_f = out.n_act;
   out.n_hot = (long long)h[8 + C_HOT];
 
+  // heavy rows (psi_heavy.cu): active users with >= heavy_min active followers, labelled
+  // first; their followers with label < H = nseg * kSeg are summed by k_heavy from staged
+  // shared-memory segments.  Disabled for graphs smaller than one segment.
+  int nseg = env_int("PSI_HEAVY_SEGS", kDefaultHeavySegs);   // in units of kSeg labels
+  // on by default only where it measured faster (C5 yes, C4 no); PSI_HEAVY=1/0
+  // forces it on/off
+  const int heavy_env = env_int("PSI_HEAVY", -1);
+  if (heavy_env == 0 || (heavy_env < 0 && n < kDefaultHeavyMinN)) nseg = 0;
+  nseg = (int)std::min<long long>(std::min(nseg, kMaxHeavySegs), (n + 1) / kSeg);
+  if (nseg > 0) {
+    Tmp act;
+    IG_CK(act.alloc((size_t)n * sizeof(int)));
+    k_active_count<<<grid_for(n * 32, 256), 256, 0, s>>>(rp, idx_in, cls.as<unsigned char>(), N,
+                                                         act.as<int>());
+    IG_CK(cudaMemsetAsync(ccount, 0, 8 * sizeof(unsigned long long), s));
+    k_mark_heavy<<<grid_for(n, 256), 256, 0, s>>>(act.as<int>(), N,
+                                                  env_int("PSI_HEAVY_MIN", kDefaultHeavyMin),
+                                                  cls.as<unsigned char>(), ccount);
+    IG_CK(cudaMemcpyAsync(h + 8, ccount, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+    out.n_heavy = (long long)h[8 + C_HEAVY];
+    out.n_hot = (long long)h[8 + C_HOT] + out.n_heavy;
+  }
+  if (out.n_heavy == 0) nseg = 0;
+  out.nseg = nseg;
+  const int Hs = nseg * kSeg;                 // staged labels [0, Hs)
+
   IG_CK(key.alloc((size_t)n * 8));
   IG_CK(sel.alloc((size_t)n * 8));
   IG_CK(sorted.alloc((size_t)n * 8));
@@ -502,8 +763,10 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   };
   long long c = 0;
   int rc;
+  if (out.n_heavy > 0 && (rc = run_stage(5, true, &c)) != PSI_OK) return rc;  // heavy rows first
   if ((rc = run_stage(0, true, &c)) != PSI_OK) return rc;          // hot, by leader count
   if ((rc = run_stage(1, false, &c)) != PSI_OK) return rc;         // leaderless active
+  out.single_lo = base;                                            // single-leader users follow
   while (true) {                                                   // single-leader, by level
     if ((rc = run_stage(2, true, &c)) != PSI_OK) return rc;
     if (c == 0) break;
@@ -525,10 +788,30 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   IG_CK(K.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(double)));
   IG_CK(rp_new.alloc((size_t)(NA + 1) * sizeof(int)));
   IG_CK(cudaMemsetAsync(cntr.p, 0, (size_t)(NA + 1) * sizeof(int), s));
+  const int NH = (int)out.n_heavy;
+  Tmp hcnt, hoff;
+  IG_CK(hcnt.alloc((size_t)(NH + 1) * sizeof(long long)));
+  IG_CK(hoff.alloc((size_t)(NH + 1) * sizeof(long long)));
+  IG_CK(cudaMemsetAsync(hcnt.p, 0, (size_t)(NH + 1) * sizeof(long long), s));
   if (NA > 0)
     k_row_count<<<grid_for((long long)NA * 32, 256), 256, 0, s>>>(
-        rp, idx_in, out.old_of_new, cls.as<unsigned char>(), a_old.as<double>(), NA,
-        cntr.as<int>(), K.as<double>());
+        rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
+        a_old.as<double>(), NA, NH, Hs, cntr.as<int>(), hcnt.as<long long>(), K.as<double>());
+  long long n_hot_ent = 0;
+  if (NH > 0) {
+    Tmp scan_tmp;
+    size_t sb = 0;
+    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, hcnt.as<long long>(), hoff.as<long long>(),
+                                        NH + 1, s));
+    IG_CK(scan_tmp.alloc(sb));
+    IG_CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, sb, hcnt.as<long long>(), hoff.as<long long>(),
+                                        NH + 1, s));
+    IG_CK(cudaMemcpyAsync(&n_hot_ent, hoff.as<long long>() + NH, sizeof(long long),
+                          cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+  }
+  Tmp hot;
+  IG_CK(hot.alloc((size_t)(n_hot_ent > 0 ? n_hot_ent : 1) * sizeof(int)));
   {
     Tmp scan_tmp;
     size_t sb = 0;
@@ -550,7 +833,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     if (NA > 0)
       k_row_fill<<<grid_for((long long)NA * 32, 256), 256, 0, s>>>(
           rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
-          rp_new.as<int>(), NA, N, ed);
+          rp_new.as<int>(), NA, N, NH, Hs, hoff.as<long long>(), ed, hot.as<int>());
     if (m_act > 0) {
       cub::DoubleBuffer<int> kb(ed, idx2.as<int>());
       size_t tb = 0;
@@ -567,6 +850,12 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     }
     IG_CK(cudaStreamSynchronize(s));
   }
+  if (NH > 0) {
+    int rc2 = build_heavy_plan(out, NH, n_hot_ent, hot, hcnt, hoff, s, msg, msg_len);
+    if (rc2 != PSI_OK) return rc2;
+  }
+  hot.reset();
+
   const size_t na_b = (size_t)(NA > 0 ? NA : 1) * sizeof(double);
   IG_CK(cudaMalloc(&out.a0, (size_t)n * sizeof(double)));
   IG_CK(cudaMalloc(&out.wt, (size_t)n * sizeof(double)));

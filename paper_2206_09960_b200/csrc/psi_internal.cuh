@@ -28,6 +28,23 @@ constexpr int kEpt = 8;                  // edges per thread
 constexpr int kTile = kBlock * kEpt;     // 2048 edges per tile
 constexpr int kFixBlock = 256;           // threads per CTA of the split-row fix-up kernel
 constexpr unsigned kRowFlag = 0x80000000u;
+// staged-segment heavy-row kernel (psi_heavy.cu)
+constexpr int kSegShift = 12;
+constexpr int kSeg = 1 << kSegShift;     // labels of x per TMA-staged segment (32 KB)
+constexpr int kHeavySlots = 8192;        // slot sums per panel (+ a junk slot for padding)
+constexpr int kEntBits = 26;             // entry word: slot (14 bits) << kSegShift | offset
+constexpr unsigned kNullEntry = (unsigned)kHeavySlots << kSegShift;
+constexpr int kHeavyWarps = 16;          // consumer warps (+ 1 producer warp)
+constexpr int kHeavyStages = 4;          // TMA ring depth
+constexpr int kHeavyBlock = 32 * (kHeavyWarps + 1);
+constexpr int kDefaultHeavyMin = 64;     // rows with >= this many active followers are heavy
+constexpr long long kDefaultHeavyMinN = 1LL << 25;   // graphs below this many users skip it
+constexpr int kMaxHeavySegs = 512;       // shared-memory bound of the per-warp list offsets
+constexpr int kDefaultHeavySegs = 256;   // staged labels H = segs * kSeg (1 Mi labels, 8 MB)
+constexpr int kDefaultHeavyPPS = 1;      // heavy panels per SM (entry budget per panel)
+constexpr int kDefaultGroups = 4;        // tile groups (of kBlock threads) per sweep CTA
+constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA
+constexpr int kDefaultL1Hot = 16384;     // labels below this gather through L1 (evict_last)
 
 // Device-resident loop state (written by kernels, read back by the host once per iterate).
 struct LoopState {
@@ -36,6 +53,7 @@ struct LoopState {
   double eps_t;          // last epsilon_t
   unsigned int done;     // CTA arrival counter of the fix-up kernel
   int status;            // bit 0: non-finite epsilon_t
+  unsigned heavy_next;   // next panel of k_heavy to claim (reset by k_fix / k_init)
 };
 
 // Per-call parameters (host writes them before every graph launch).
@@ -45,6 +63,17 @@ struct LoopParams {
   double kappa;          // ||B|| for the selected norm
   double* history;       // epsilon_t, t = 1..T
   long long hist_cap;
+};
+
+// Device view of the heavy-row plan (built at ingest, psi_ingest.cu).
+struct HeavyPlan {
+  const unsigned* ent;       // entry words, lists (panel, segment, warp), 32-byte aligned
+  const long long* loff;     // [npanels * kHeavyWarps * nseg + 1] starts of lists (p, warp, s)
+  const int* prow;           // [npanels + 1] heavy rows of panel p: [prow[p], prow[p+1])
+  const int2* rslot;         // [n_heavy] (first slot, number of slots) of each heavy row
+  const int* wslot;          // [npanels * (kHeavyWarps + 1)] slot range of each warp
+  int npanels;
+  int nseg;                  // staged labels H = nseg * kSeg
 };
 
 // Everything one sweep / readout launch needs (passed by value; frozen in the graph).
@@ -65,7 +94,14 @@ struct SweepArgs {
   double n_users;            // N of psi = (...)/N
   int n_act;
   int hot_lim;               // labels < hot_lim: L2 evict_last for x gathers/stores
+  int hot_smem;              // labels < hot_smem: gathered from the CTA's shared-memory copy
+  int l1_lim;                // labels in [hot_smem, l1_lim): L1-allocating gathers
+  int st_last;               // 1: x_t stores below hot_lim are L2 evict_last (else evict_first)
+  int single_lo;             // labels >= single_lo: single-leader users, L1 evict_first gathers
   double* psi;               // readout output (relabelled order)
+  int n_heavy;               // rows [0, n_heavy) add hhot (their followers < H) to S
+  double* hhot;              // [n_heavy] written by k_heavy before k_tiles
+  HeavyPlan heavy;
   double* x0;                // ping-pong iterate buffers [n + 1], x[n] = 0 (sentinel)
   double* x1;
   double* eps_part1;         // per CTA of the tile kernel
@@ -78,10 +114,18 @@ struct SweepArgs {
 };
 
 // ---- launchers (psi_sweep.cu)
-int sweep_grid(int ntiles);          // persistent CTAs for the tile kernel
+struct TilesCfg {                    // launch shape of k_tiles (sweep and readout)
+  void* sweep;
+  void* readout;
+  int groups, grid, block;
+  size_t smem;                       // dynamic: groups x TileSmem + hot cache
+  int hot_smem, l1_lim;
+};
+TilesCfg tiles_config(int ntiles, long long n);
 int fix_grid(int nsplit);            // CTAs of the fix-up kernel
-void* sweep_kernel_ptr(bool readout);
 void* fix_kernel_ptr(bool readout);
+void* heavy_kernel_ptr();            // psi_heavy.cu
+size_t heavy_smem_bytes(int nseg);
 void* init_kernel_ptr();
 
 // ---- ingest (psi_ingest.cu)
@@ -102,6 +146,15 @@ struct IngestOut {
   int4* split = nullptr;
   int nsplit = 0;
   long long n_act = 0, m_act = 0, n_hot = 0, n_pseudo = 0;
+  long long single_lo = 0;    // first label of the single-leader users (gathered once, in order)
+  // heavy rows (labels [0, n_heavy)): followers < H served by k_heavy (HeavyPlan)
+  long long n_heavy = 0, heavy_entries = 0;
+  int nseg = 0, npanels = 0;
+  unsigned* h_ent = nullptr;
+  long long* h_loff = nullptr;
+  int* h_prow = nullptr;
+  int2* h_rslot = nullptr;
+  int* h_wslot = nullptr;
   int relabel_levels = 0;
   double kappa_row = 0, kappa_col = 0, rho_A = 0;
   long long n_f = 0, n_g = 0, n_leaderless = 0;

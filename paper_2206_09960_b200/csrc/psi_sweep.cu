@@ -27,6 +27,9 @@
 // reduction has a fixed order, so two runs give bitwise identical psi and eps_t.
 #include "psi_internal.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace psi {
 namespace {
 
@@ -70,6 +73,28 @@ __device__ __forceinline__ double ld_hint(const double* p, unsigned long long po
   asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ double ld_hint_na(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_l1first(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::evict_first.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_l1last(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+// named barrier over one 256-thread tile group of the CTA (id 0 is __syncthreads)
+__device__ __forceinline__ void group_bar(int id) {
+  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(kBlock) : "memory");
+}
 __device__ __forceinline__ void st_hint(double* p, double v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
 }
@@ -106,26 +131,42 @@ struct TileSmem {
   int next_flag;              // does the edge after this tile start a row?
 };
 
-template <bool READOUT>
-__global__ void __launch_bounds__(kBlock, 4) k_tiles(SweepArgs A) {
-  __shared__ TileSmem sm;
+// G tile groups of kBlock threads per CTA (named barriers 1..G); the CTA's shared hot
+// cache holds x_{t-1}[0, hot_smem): the most-gathered labels, read from
+// shared memory instead of L2.  Gathers of labels in [hot_smem, l1_lim) allocate in L1
+// (evict_last); all others bypass L1, so streaming cold gathers cannot evict them.
+template <bool READOUT, int G>
+__global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_tiles(SweepArgs A) {
+  extern __shared__ __align__(16) unsigned char dsm[];   // [G x TileSmem][hot cache]
+  TileSmem* smg = reinterpret_cast<TileSmem*>(dsm);
+  double* hot = reinterpret_cast<double*>(dsm + G * sizeof(TileSmem));
   const long long t = A.st->iter;
   const double* __restrict__ xs = (t & 1) ? A.x1 : A.x0;    // x_{t-1}
   double* __restrict__ xd = (t & 1) ? A.x0 : A.x1;          // x_t
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = G == 1 ? 0 : threadIdx.x / kBlock;
+  const int tid = threadIdx.x - grp * kBlock, lane = tid & 31, warp = tid >> 5;
+  TileSmem& sm = smg[grp];
   const unsigned long long pf = pol_evict_first(), pl = pol_evict_last();
   const unsigned hot_lim = (unsigned)A.hot_lim;
+  const unsigned hs = (unsigned)A.hot_smem;
+  const unsigned l1_lim = (unsigned)A.l1_lim;
+  const unsigned single_lo = (unsigned)A.single_lo;
   const int ntiles = A.ntiles;
+  const bool st_last = A.st_last;
   double eps_acc = 0.0;
 
-  int k = blockIdx.x;
+  for (unsigned i = threadIdx.x; i < hs; i += blockDim.x) hot[i] = __ldcg(xs + i);
+  __syncthreads();
+
+  const int stride = gridDim.x * G;
+  int k = blockIdx.x * G + grp;
   uint4 u0 = make_uint4(0, 0, 0, 0), u1 = u0;
   if (k < ntiles) {
     const unsigned* p = A.edges + (size_t)k * kTile + tid * kEpt;
     u0 = ld_stream4(p, pf);
     u1 = ld_stream4(p + 4, pf);
   }
-  for (; k < ntiles; k += gridDim.x) {
+  for (; k < ntiles; k += stride) {
     const int f0 = __ldg(A.tile_row + k);
     const int F = __ldg(A.tile_row + k + 1) - f0;      // rows started in this tile
     const unsigned w[kEpt] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
@@ -137,12 +178,15 @@ __global__ void __launch_bounds__(kBlock, 4) k_tiles(SweepArgs A) {
     for (int q = 0; q < kEpt; ++q) {
       const unsigned lab = w[q] & kLabelMask;
       fl |= (w[q] >> 31) << q;
-      v[q] = ld_hint(xs + lab, lab < hot_lim ? pl : pf);
+      if (lab < hs) v[q] = hot[lab];
+      else if (lab < l1_lim) v[q] = ld_l1last(xs + lab, pl);
+      else if (lab >= single_lo) v[q] = ld_l1first(xs + lab, pf);
+      else v[q] = ld_hint_na(xs + lab, lab < hot_lim ? pl : pf);
     }
     if (tid == 0)
       sm.next_flag = (k + 1 >= ntiles) ? 1 : (int)(ld_stream(A.edges + (size_t)(k + 1) * kTile, pf) >> 31);
     // ---- prefetch the next tile's edge words
-    const int kn = k + gridDim.x;
+    const int kn = k + stride;
     if (kn < ntiles) {
       const unsigned* p = A.edges + (size_t)kn * kTile + tid * kEpt;
       u0 = ld_stream4(p, pf);
@@ -151,15 +195,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_tiles(SweepArgs A) {
 
     // ---- thread-local reduction by row flags
     const int nf = __popc(fl);
-    double head = 0.0, run = 0.0;
-    bool seen = false;
+    double run = 0.0;
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {
-      if ((fl >> q) & 1u) {
-        if (!seen) head = run;
-        seen = true;
-        run = 0.0;
-      }
+      if ((fl >> q) & 1u) run = 0.0;
       run += v[q];
     }
     // scan element: (has flag, partial of the row open at the thread's end)
@@ -178,18 +217,17 @@ __global__ void __launch_bounds__(kBlock, 4) k_tiles(SweepArgs A) {
       }
     }
     if (lane == 31) { sm.wv[warp] = v_in; sm.wf[warp] = f_in; sm.wn[warp] = n_in; }
-    __syncthreads();
+    if (G == 1) __syncthreads(); else group_bar(1 + grp);
     const int next_flag = sm.next_flag;
-    int nP = 0, fP = 0;
+    int nP = 0;
     double vP = 0.0;
     for (int w2 = 0; w2 < warp; ++w2) {              // fold of earlier warps, fixed order
       nP += sm.wn[w2];
       vP = sm.wf[w2] ? sm.wv[w2] : vP + sm.wv[w2];
-      fP |= sm.wf[w2];
     }
     const double v_full = f_in ? v_in : vP + v_in;
     const double v_prev = __shfl_up_sync(kFull, v_full, 1);
-    double carry = lane == 0 ? vP : v_prev;          // partial of the row open at thread start
+    const double carry = lane == 0 ? vP : v_prev;    // partial of the row open at thread start
     const int n_ex = nP + n_in - nf;                 // flags before this thread in the tile
 
     // ---- emit completed row sums
@@ -210,27 +248,28 @@ __global__ void __launch_bounds__(kBlock, 4) k_tiles(SweepArgs A) {
       else if (next_flag) { sm.rowsum[F - 1] = run; A.p_out[k] = 0.0; }
       else A.p_out[k] = run;
     }
-    __syncthreads();
+    if (G == 1) __syncthreads(); else group_bar(1 + grp);
 
     // ---- epilogue over the rows completed in this tile (coalesced)
     const int nrows = (F > 0 && !next_flag) ? F - 1 : F;
     for (int i = tid; i < nrows; i += kBlock) {
       const int r = f0 + i;
-      const double Sr = sm.rowsum[i];
+      double Sr = sm.rowsum[i];
+      if (r < A.n_heavy) Sr += A.hhot[r];               // followers < H (k_heavy)
       if (READOUT) {
         A.psi[r] = (ld_stream(A.d + r, pf) + ld_stream(A.lam + r, pf) * Sr) / A.n_users;
       } else {
         const unsigned long long px = (unsigned)r < hot_lim ? pl : pf;
         const double xn = fma(ld_stream(A.g + r, pf), Sr, ld_stream(A.a + r, pf));
-        eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - ld_hint(xs + r, px));
-        st_hint(xd + r, xn, px);
+        eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - ld_hint_na(xs + r, px));
+        st_hint(xd + r, xn, st_last ? px : pf);
       }
     }
   }
 
   if (!READOUT) {
-    const double tot = block_sum<kBlock>(eps_acc, sm.red);
-    if (tid == 0) A.eps_part1[blockIdx.x] = tot;
+    const double tot = block_sum<kBlock * G>(eps_acc, smg[0].red);
+    if (threadIdx.x == 0) A.eps_part1[blockIdx.x] = tot;
   }
 }
 
@@ -244,11 +283,13 @@ __global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
   const int tid = threadIdx.x;
   double eps_acc = 0.0;
 
+  if (blockIdx.x == 0 && tid == 0) A.st->heavy_next = 0;   // k_heavy of this sweep is done
   for (int s = blockIdx.x * kFixBlock + tid; s < A.nsplit; s += gridDim.x * kFixBlock) {
     const int4 sp = A.split[s];
     const int r = sp.x;
     double S = A.p_out[sp.y];
     for (int k = sp.y + 1; k <= sp.z; ++k) S += A.p_in[k];
+    if (r < A.n_heavy) S += A.hhot[r];
     if (READOUT) {
       A.psi[r] = (A.d[r] + A.lam[r] * S) / A.n_users;
     } else {
@@ -304,6 +345,7 @@ __global__ void k_init(SweepArgs A, int n) {
     A.st->eps_t = 0.0;
     A.st->done = 0;
     A.st->status = 0;
+    A.st->heavy_next = 0;
     const LoopParams P = *A.prm;
     if (A.use_cond) cudaGraphSetConditional(A.cond, (1.0 > P.eps && P.max_iters > 0) ? 1u : 0u);
   }
@@ -311,18 +353,54 @@ __global__ void k_init(SweepArgs A, int n) {
 
 }  // namespace
 
-int sweep_grid(int ntiles) {
-  static int occ = -1, sms = 0;
-  if (occ < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiles<false>, kBlock, 0);
-    if (occ < 1) occ = 1;
-  }
+namespace {
+template <int G>
+TilesCfg cfg_for(int ntiles, long long n, int hot_req, int l1_req) {
+  int dev = 0, sms = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  TilesCfg c{};
+  c.groups = G;
+  c.block = kBlock * G;
+  const size_t fixed = G * sizeof(TileSmem);
+  long long hs = hot_req;
+  const long long cap = ((long long)optin - (long long)fixed - 1024) / 8;
+  if (hs > cap) hs = cap;
+  if (hs > n + 1) hs = n + 1;                         // labels 0..n (n = zero sentinel)
+  if (hs < 0) hs = 0;
+  c.hot_smem = (int)hs;
+  c.l1_lim = (int)std::max<long long>(hs, std::min<long long>(l1_req, n + 1));
+  c.smem = fixed + (size_t)hs * 8;
+  c.sweep = (void*)k_tiles<false, G>;
+  c.readout = (void*)k_tiles<true, G>;
+  cudaFuncSetAttribute(k_tiles<false, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  cudaFuncSetAttribute(k_tiles<true, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiles<false, G>, c.block, c.smem);
+  if (occ < 1) occ = 1;
   long long g = (long long)sms * occ;
-  if (g > ntiles) g = ntiles;
-  return g < 1 ? 1 : (int)g;
+  if (g * G > ntiles) g = (ntiles + G - 1) / G;
+  c.grid = g < 1 ? 1 : (int)g;
+  return c;
+}
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+}  // namespace
+
+// Launch shape of the sweep/readout kernel.  Defaults from the C5 measurements in
+// DESIGN.md §12; PSI_GROUPS / PSI_SMEM_HOT / PSI_L1_HOT override them (tuning only).
+TilesCfg tiles_config(int ntiles, long long n) {
+  const int G = env_int("PSI_GROUPS", kDefaultGroups);
+  const int hot = env_int("PSI_SMEM_HOT", kDefaultSmemHot);
+  const int l1 = env_int("PSI_L1_HOT", kDefaultL1Hot);
+  switch (G) {
+    case 1: return cfg_for<1>(ntiles, n, hot, l1);
+    case 2: return cfg_for<2>(ntiles, n, hot, l1);
+    default: return cfg_for<4>(ntiles, n, hot, l1);
+  }
 }
 
 int fix_grid(int nsplit) {
@@ -334,9 +412,6 @@ int fix_grid(int nsplit) {
   return g < 1 ? 1 : (int)g;
 }
 
-void* sweep_kernel_ptr(bool readout) {
-  return readout ? (void*)k_tiles<true> : (void*)k_tiles<false>;
-}
 void* fix_kernel_ptr(bool readout) {
   return readout ? (void*)k_fix<true> : (void*)k_fix<false>;
 }

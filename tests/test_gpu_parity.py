@@ -142,8 +142,12 @@ def test_random_small_graphs_fixed_count(gpu, seed):
                                atol=1e-13 * max(1.0, np.abs(ref.s).sum()))
 
 
-def test_long_rows_span_many_tiles(gpu):
-    """A hub followed by everybody (row longer than several 2048-item tiles) + a chain."""
+@pytest.mark.parametrize("heavy", ["0", "1"])
+def test_long_rows_span_many_tiles(gpu, heavy, monkeypatch):
+    """A hub followed by everybody (row longer than several 2048-item tiles) + a chain; with
+    the heavy-row kernel off the hub is a split row of the edge stream (k_fix), with it on
+    its followers below H come from staged shared memory."""
+    monkeypatch.setenv("PSI_HEAVY", heavy)
     n = 9000
     edges = [(i, 0) for i in range(1, n)] + [(0, 1)] + [(i, i + 1) for i in range(1, n - 1)]
     rp, f = psigen.csr_from_edges(n, edges)
@@ -152,7 +156,10 @@ def test_long_rows_span_many_tiles(gpu):
     ref = oracle.power_psi(rp, f, lam, mu, eps=1e-13)
     got = gpu_run(gpu, rp, f, lam, mu, 0.0, ref.iterations)
     assert oracle.max_rel_error(ref.psi, got["psi"]) <= TOL
-    assert got["info"]["num_long_rows"] >= 1
+    if heavy == "0":
+        assert got["info"]["num_long_rows"] >= 1 and got["info"]["n_heavy"] == 0
+    else:
+        assert got["info"]["n_heavy"] >= 1
 
 
 # ---------------------------------------------------------------- configs
@@ -223,3 +230,71 @@ def test_repeated_iterate_on_one_context(gpu):
         _, T3, _ = g.iterate(1e-9)
         p3 = g.get_psi().cpu().numpy()
     assert T2 > T1 == T3 and np.array_equal(p1, p3)
+
+
+# ------------------------------------------------ staged-segment heavy-row path (k_heavy)
+
+@pytest.mark.parametrize("env", [
+    {"PSI_HEAVY": "0"},                                     # edge-stream sweep only
+    {"PSI_HEAVY": "1", "PSI_HEAVY_MIN": "2", "PSI_HEAVY_SEGS": "3"},   # nearly every row heavy
+    {"PSI_HEAVY": "1", "PSI_HEAVY_MIN": "16"},              # default H, more heavy rows
+    {"PSI_HEAVY": "1"},                                     # library defaults, forced on
+])
+def test_heavy_rows_parity(gpu, env, monkeypatch):
+    """psi_build_graph reads the heavy-row knobs; every split of the work between k_heavy
+    (followers < H from TMA-staged shared memory) and k_tiles must give the oracle's psi."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w = psigen.make_config(5, scale=17)
+    ref, got = parity(gpu, w)
+    info = got["info"]
+    if env.get("PSI_HEAVY") == "0":
+        assert info["n_heavy"] == 0
+    else:
+        assert info["n_heavy"] > 0 and info["heavy_entries"] > 0 and info["heavy_panels"] > 0
+
+
+def test_heavy_hub_many_slots(gpu, monkeypatch):
+    """A hub followed by nearly everyone is spread over many slots (virtual rows) and
+    warps; its psi must still match the oracle (and the readout path too)."""
+    monkeypatch.setenv("PSI_HEAVY", "1")
+    monkeypatch.setenv("PSI_HEAVY_MIN", "8")
+    rng = np.random.default_rng(7)
+    n = 40_000
+    src = rng.integers(0, n, 400_000)
+    dst = rng.integers(0, n, 400_000)
+    keep = src != dst
+    edges = np.stack([src[keep], dst[keep]], 1)
+    hub = np.stack([np.arange(1, n), np.zeros(n - 1, dtype=np.int64)], 1)   # all follow user 0
+    rp, f = psigen.csr_from_edges(n, np.concatenate([edges, hub]))
+    lam = rng.uniform(0.05, 1.0, n)
+    mu = rng.uniform(0.05, 1.0, n)
+    ref = oracle.power_psi(rp, f, lam, mu, eps=1e-11)
+    got = gpu_run(gpu, rp, f, lam, mu, 0.0, ref.iterations)
+    assert got["info"]["n_heavy"] > 0
+    assert oracle.max_rel_error(ref.psi, got["psi"]) <= TOL
+    check_topk(ref.psi, got["psi"])
+
+
+def test_heavy_rows_deterministic(gpu, monkeypatch):
+    """k_heavy claims panels dynamically; each panel's sums have a fixed order, so psi and
+    the eps history must be bitwise identical run to run."""
+    monkeypatch.setenv("PSI_HEAVY", "1")
+    monkeypatch.setenv("PSI_HEAVY_MIN", "8")
+    w = psigen.make_config(4, scale=17)
+    a = gpu_run(gpu, w.row_ptr, w.followers, w.lam, w.mu, w.eps)
+    b = gpu_run(gpu, w.row_ptr, w.followers, w.lam, w.mu, w.eps)
+    assert a["info"]["n_heavy"] > 0
+    assert np.array_equal(a["psi"], b["psi"]) and np.array_equal(a["hist"], b["hist"])
+
+
+# ------------------------------------------------ BASELINE.json full sizes (bench launch config)
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_size_parity(gpu, cfg):
+    """Configs 4 (R-MAT s24, 273M edges) and 5 (R-MAT s26, 1.1e9 edges) at full size with the
+    library defaults bench.py times: every psi entry against the fp64 oracle at the oracle's
+    T*, the same top-k, and the eps-mode stop within one sweep of T*."""
+    w = psigen.make_config(cfg)
+    parity(gpu, w, full=True)

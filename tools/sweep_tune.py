@@ -31,12 +31,13 @@ def main():
             os.environ[k] = v
         with psi.PsiGraph(*dev) as g:
             g.time_sweep(3)
-            a, b = g.time_sweep(args.sweeps)
+            hv, a, b = g.time_sweep(args.sweeps)
             st, T, gap = g.iterate(w.eps)
             inf = g.info()
         byt = 4 * w.m + 4 * (w.n + 1) + 8 * inf["n_g"] + 32 * inf["n_f"]
-        print(f"[{s}] k_tiles {a:.3f} ms  k_fix {b:.3f} ms  sweep {a + b:.3f} ms  "
-              f"{byt / (a + b) / 1e6:.0f} GB/s  T={T} solve {inf['iterate_ms']:.2f} ms  "
+        print(f"[{s}] k_heavy {hv:.3f} ms  k_tiles {a:.3f} ms  k_fix {b:.3f} ms  sweep {hv + a + b:.3f} ms  "
+              f"{byt / (hv + a + b) / 1e6:.0f} GB/s  T={T} solve {inf['iterate_ms']:.2f} ms  "
+              f"heavy rows {inf['n_heavy']} entries {inf['heavy_entries']} panels {inf['heavy_panels']}  "
               f"ingest {inf['ingest_ms']:.0f} ms", flush=True)
 
 
