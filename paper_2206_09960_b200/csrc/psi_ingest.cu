@@ -35,6 +35,7 @@
 #include <cub/iterator/counting_input_iterator.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -106,36 +107,134 @@ __global__ void k_check_activity(const double* lam, const double* mu, long long 
 
 // ------------------------------------------------------------------ 2.-4. normalisers
 
-// leader (row) of every edge, a copy of the follower, and #leaders of every follower
-__global__ void k_expand(const int* rp, const int* idx, int n, int* leader_of_edge,
-                         int* follower_copy, int* n_leaders) {
-  const int lane = threadIdx.x & 31;
-  WARP_STRIDE(row, n) {
+// leader (row) of every edge: thread per short row, warp per long row (see kShort)
+__global__ void k_expand_short(const int* rp, int n, int* leader_of_edge) {
+  GRID_STRIDE(row, n) {
     const int b = rp[row], e = rp[row + 1];
-    for (int q = b + lane; q < e; q += 32) {
-      const int v = idx[q];
-      leader_of_edge[q] = (int)row;
-      follower_copy[q] = v;
-      atomicAdd(n_leaders + v, 1);
+    if (e - b > 32) continue;
+    for (int q = b; q < e; ++q) leader_of_edge[q] = (int)row;
+  }
+}
+__global__ void k_expand_long(const int* list, int nlist, const int* rp, int* leader_of_edge) {
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(i, nlist) {
+    const int row = list[i];
+    const int b = rp[row], e = rp[row + 1];
+    for (int q = b + lane; q < e; q += 32) leader_of_edge[q] = row;
+  }
+}
+
+// loff[u] = first sorted pair with follower >= u (u = 0..n); nlead[u] = loff[u+1] - loff[u]
+__global__ void k_lower_bounds(const unsigned* keys, int m, int n, int* loff, int* nlead) {
+  GRID_STRIDE(u, n + 1) {
+    int lo = 0, hi = m;
+    while (lo < hi) {
+      const int mid = (int)(((unsigned)lo + (unsigned)hi) >> 1);
+      if (keys[mid] < (unsigned)u) lo = mid + 1; else hi = mid;
+    }
+    loff[u] = lo;
+  }
+}
+__global__ void k_diff(const int* loff, int n, int* nlead) { GRID_STRIDE(u, n) nlead[u] = loff[u + 1] - loff[u]; }
+
+// Segments (a user's leaders, a leader's followers) follow the power law: most are a few
+// entries long, a few are huge.  Every per-segment pass below therefore runs as a thread
+// per short segment (<= kShort entries, summed sequentially) plus a warp per long segment
+// (a compacted list; fixed shuffle tree) -- both deterministic -- instead of a warp per
+// segment that leaves most lanes idle.
+constexpr int kShort = 32;
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(kFull, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// (lambda, mu) interleaved: one 16-byte gather per leader instead of two 8-byte ones
+__global__ void k_pack_activity(const double* lam, const double* mu, long long n, double2* lm) {
+  GRID_STRIDE(i, n) lm[i] = make_double2(lam[i], mu[i]);
+}
+
+__global__ void k_long_flags(const int* off, const int* perm, int n, int thr, unsigned char* flag) {
+  GRID_STRIDE(r, n) {
+    const int o = perm ? perm[r] : (int)r;
+    flag[r] = (off[o + 1] - off[o]) > thr;
+  }
+}
+
+// constants of user u from its newsfeed sums (reading R5); returns the row sums
+// of B and A (for ||B||_row and rho_A), -1 for a leaderless user
+__device__ __forceinline__ void norm_finish(int u, double W, double L, double M, int first,
+                                            const double2* lm, double* a, double* g, double* wt,
+                                            double* d, int* first_leader, double& rowB,
+                                            double& rowA) {
+  const double2 own = lm[u];
+  const double w = own.x + own.y;
+  const double c = own.y / w;
+  d[u] = own.x / w;
+  const double W_t = W > 0.0 ? W : 1.0;            // R5: leaderless slot holds s_j
+  wt[u] = W_t;
+  a[u] = c / W_t;
+  g[u] = own.y / W_t;
+  first_leader[u] = first;
+  rowB = W > 0.0 ? L / W : -1.0;
+  rowA = W > 0.0 ? M / W : -1.0;
+}
+
+// thread per user with <= kShort leaders: W_n, Lambda_n, M_n summed in leader order
+__global__ void k_norm_short(const int* loff, const int* leaders, const double2* lm, int n,
+                             double* a, double* g, double* wt, double* d, int* first_leader,
+                             unsigned long long* kmax, unsigned long long* cnt) {
+  const int lane = threadIdx.x & 31;
+  for (long long base = blockIdx.x * (long long)blockDim.x; base < n;
+       base += (long long)gridDim.x * blockDim.x) {
+    const long long u = base + threadIdx.x;
+    double rowB = -1.0, rowA = -1.0;
+    bool leaderless = false;
+    if (u < n) {
+      const int b = loff[u], e = loff[u + 1];
+      if (e - b <= kShort) {
+        double W = 0.0, L = 0.0, M = 0.0;
+        for (int q = b; q < e; ++q) {
+          const double2 v = lm[leaders[q]];
+          W += v.x + v.y;
+          L += v.x;
+          M += v.y;
+        }
+        norm_finish((int)u, W, L, M, e > b ? leaders[b] : -1, lm, a, g, wt, d, first_leader,
+                    rowB, rowA);
+        leaderless = e == b;
+      }
+    }
+    // one atomic per warp (negative doubles never win: kmax starts at +0.0)
+    const unsigned long long mb = warp_max_u64(rowB > 0.0 ? dbits(rowB) : 0ull);
+    const unsigned long long ma = warp_max_u64(rowA > 0.0 ? dbits(rowA) : 0ull);
+    const unsigned nl = __popc(__ballot_sync(kFull, leaderless));
+    if (lane == 0) {
+      if (mb) atomicMax(kmax + 0, mb);
+      if (ma) atomicMax(kmax + 1, ma);
+      if (nl) atomicAdd(cnt + 0, (unsigned long long)nl);
     }
   }
 }
 
-// warp per user n: W_n, Lambda_n, M_n over its leaders (ascending, fixed tree), then constants.
-__global__ void k_normalisers(const int* loff, const int* leaders, const double* lam,
-                              const double* mu, int n, double* a, double* g, double* wt,
-                              double* d, int* first_leader, unsigned long long* kmax,
-                              unsigned long long* cnt) {
+// warp per listed user with > kShort leaders (fixed shuffle tree)
+__global__ void k_norm_long(const int* list, int nlist, const int* loff, const int* leaders,
+                            const double2* lm, double* a, double* g, double* wt, double* d,
+                            int* first_leader, unsigned long long* kmax) {
   const int lane = threadIdx.x & 31;
-  WARP_STRIDE(u, n) {
+  WARP_STRIDE(i, nlist) {
+    const int u = list[i];
     const int b = loff[u], e = loff[u + 1];
     double W = 0.0, L = 0.0, M = 0.0;
     for (int q = b + lane; q < e; q += 32) {
-      const int l = leaders[q];
-      const double ll = lam[l], mm = mu[l];
-      W += ll + mm;
-      L += ll;
-      M += mm;
+      const double2 v = lm[leaders[q]];
+      W += v.x + v.y;
+      L += v.x;
+      M += v.y;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -144,36 +243,46 @@ __global__ void k_normalisers(const int* loff, const int* leaders, const double*
       M += __shfl_xor_sync(kFull, M, o);
     }
     if (lane == 0) {
-      const double lu = lam[u], mu_u = mu[u];
-      const double w = lu + mu_u;
-      const double c = mu_u / w;
-      d[u] = lu / w;
-      const double W_t = W > 0.0 ? W : 1.0;            // R5: leaderless slot holds s_j
-      wt[u] = W_t;
-      a[u] = c / W_t;
-      g[u] = mu_u / W_t;
-      first_leader[u] = e > b ? leaders[b] : -1;
-      if (W > 0.0) {
-        atomicMax(kmax + 0, dbits(L / W));             // row sum of B
-        atomicMax(kmax + 1, dbits(M / W));             // row sum of A
-      } else {
-        atomicAdd(cnt + 0, 1ull);                      // leaderless
-      }
+      double rowB, rowA;
+      norm_finish(u, W, L, M, leaders[b], lm, a, g, wt, d, first_leader, rowB, rowA);
+      atomicMax(kmax + 0, dbits(rowB));
+      atomicMax(kmax + 1, dbits(rowA));
     }
   }
 }
 
-// warp per leader i: column sum of B = lambda_i sum_{j in F(i)} 1/W_j.
-__global__ void k_kappa_col(const int* rp, const int* idx, const double* wt, const double* lam,
-                            int n, unsigned long long* kmax) {
+// column sums of B = lambda_i sum_{j in F(i)} 1/W_j: thread per short leader row ...
+__global__ void k_kappa_col_short(const int* rp, const int* idx, const double* wt,
+                                  const double* lam, int n, unsigned long long* kmax) {
+  for (long long base = blockIdx.x * (long long)blockDim.x; base < n;
+       base += (long long)gridDim.x * blockDim.x) {
+    const long long i = base + threadIdx.x;
+    unsigned long long m = 0;
+    if (i < n) {
+      const int b = rp[i], e = rp[i + 1];
+      if (e > b && e - b <= kShort) {
+        double s = 0.0;
+        for (int q = b; q < e; ++q) s += 1.0 / wt[idx[q]];
+        m = dbits(lam[i] * s);
+      }
+    }
+    m = warp_max_u64(m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(kmax + 2, m);
+  }
+}
+
+// ... and a warp per long one
+__global__ void k_kappa_col_long(const int* list, int nlist, const int* rp, const int* idx,
+                                 const double* wt, const double* lam, unsigned long long* kmax) {
   const int lane = threadIdx.x & 31;
-  WARP_STRIDE(i, n) {
+  WARP_STRIDE(k, nlist) {
+    const int i = list[k];
     const int b = rp[i], e = rp[i + 1];
     double s = 0.0;
     for (int q = b + lane; q < e; q += 32) s += 1.0 / wt[idx[q]];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-    if (lane == 0 && e > b) atomicMax(kmax + 2, dbits(lam[i] * s));
+    if (lane == 0) atomicMax(kmax + 2, dbits(lam[i] * s));
   }
 }
 
@@ -259,23 +368,48 @@ __global__ void k_mark_heavy(const int* act, int n, int min_act, unsigned char* 
   }
 }
 
-// warp per new active row r: #active followers in the edge stream (for heavy rows r <
-// n_heavy only those with label >= H; the others, hc[r], go to k_heavy), and
-// K_r = sum of a_n over follower-less followers
-__global__ void k_row_count(const int* rp, const int* idx, const int* old_of_new,
-                            const unsigned char* cls, const int* new_of_old, const double* a_old,
-                            int n_act, int n_heavy, int H, int* cnt, long long* hc, double* K) {
+// new active row r: #active followers in the edge stream (for heavy rows r < n_heavy only
+// those with label >= H; the others, hc[r], go to k_heavy), and K_r = sum of a_n over
+// follower-less followers.  Thread per short row / warp per long row (see kShort).
+struct RowCountArgs {
+  const int* rp; const int* idx; const int* old_of_new; const unsigned char* cls;
+  const int* new_of_old; const double* a_old; int n_act, n_heavy, H;
+  int* cnt; long long* hc; double* K;
+};
+
+__global__ void k_row_count_short(RowCountArgs R) {
+  GRID_STRIDE(r, R.n_act) {
+    const int o = R.old_of_new[r];
+    const int b = R.rp[o], e = R.rp[o + 1];
+    if (e - b > kShort) continue;
+    const bool heavy = r < R.n_heavy;
+    int c = 0, h = 0;
+    double k = 0.0;
+    for (int q = b; q < e; ++q) {
+      const int v = R.idx[q];
+      if (R.cls[v] == C_INACTIVE) k += R.a_old[v];
+      else if (heavy && R.new_of_old[v] < R.H) ++h;
+      else ++c;
+    }
+    R.cnt[r] = c > 0 ? c : 1;      // 0 -> one pseudo edge
+    R.K[r] = k;
+    if (heavy) R.hc[r] = h;
+  }
+}
+
+__global__ void k_row_count_long(RowCountArgs R, const int* list, int nlist) {
   const int lane = threadIdx.x & 31;
-  WARP_STRIDE(r, n_act) {
-    const int o = old_of_new[r];
-    const int b = rp[o], e = rp[o + 1];
-    const bool heavy = r < n_heavy;
+  WARP_STRIDE(i, nlist) {
+    const int r = list[i];
+    const int o = R.old_of_new[r];
+    const int b = R.rp[o], e = R.rp[o + 1];
+    const bool heavy = r < R.n_heavy;
     int c = 0, h = 0;
     double k = 0.0;
     for (int q = b + lane; q < e; q += 32) {
-      const int v = idx[q];
-      if (cls[v] == C_INACTIVE) k += a_old[v];
-      else if (heavy && new_of_old[v] < H) ++h;
+      const int v = R.idx[q];
+      if (R.cls[v] == C_INACTIVE) k += R.a_old[v];
+      else if (heavy && R.new_of_old[v] < R.H) ++h;
       else ++c;
     }
     c = __reduce_add_sync(kFull, c);
@@ -283,44 +417,69 @@ __global__ void k_row_count(const int* rp, const int* idx, const int* old_of_new
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) k += __shfl_xor_sync(kFull, k, s);
     if (lane == 0) {
-      cnt[r] = c > 0 ? c : 1;      // 0 -> one pseudo edge
-      K[r] = k;
-      if (heavy) hc[r] = h;
+      R.cnt[r] = c > 0 ? c : 1;
+      R.K[r] = k;
+      if (heavy) R.hc[r] = h;
     }
   }
 }
 
-// warp per new active row: write the active followers' new labels (unsorted, stable) to the
-// edge stream -- heavy rows: only labels >= H; their labels < H go to hot[hoff[r]...].  A row
-// with no stream follower gets one pseudo edge to the sentinel label n (x[n] = 0).
-__global__ void k_row_fill(const int* rp, const int* idx, const int* old_of_new,
-                           const unsigned char* cls, const int* new_of_old, const int* rp_new,
-                           int n_act, int n, int n_heavy, int H, const long long* hoff,
-                           int* idx_new, int* hot) {
-  const int lane = threadIdx.x & 31;
-  WARP_STRIDE(r, n_act) {
-    const int o = old_of_new[r];
-    const int b = rp[o], e = rp[o + 1];
-    const int start = rp_new[r];
-    const bool heavy = r < n_heavy;
+// write the active followers' new labels in input order to the edge stream -- heavy rows:
+// only labels >= H; their labels < H go to hot[hoff[r]...].  A row with no stream follower
+// gets one pseudo edge to the sentinel label n (x[n] = 0).  Thread per short row / warp
+// per long row (ballot compaction keeps the input order).
+struct RowFillArgs {
+  const int* rp; const int* idx; const int* old_of_new; const unsigned char* cls;
+  const int* new_of_old; const int* rp_new; int n_act, n, n_heavy, H;
+  const long long* hoff; int* idx_new; int* hot;
+};
+
+__global__ void k_row_fill_short(RowFillArgs R) {
+  GRID_STRIDE(r, R.n_act) {
+    const int o = R.old_of_new[r];
+    const int b = R.rp[o], e = R.rp[o + 1];
+    if (e - b > kShort) continue;
+    const bool heavy = r < R.n_heavy;
+    const int start = R.rp_new[r];
     int out = start;
-    long long hout = heavy ? hoff[r] : 0;
+    long long hout = heavy ? R.hoff[r] : 0;
+    for (int q = b; q < e; ++q) {
+      const int v = R.idx[q];
+      if (R.cls[v] == C_INACTIVE) continue;
+      const int nv = R.new_of_old[v];
+      if (heavy && nv < R.H) R.hot[hout++] = nv;
+      else R.idx_new[out++] = nv;
+    }
+    if (out == start) R.idx_new[start] = R.n;
+  }
+}
+
+__global__ void k_row_fill_long(RowFillArgs R, const int* list, int nlist) {
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(i, nlist) {
+    const int r = list[i];
+    const int o = R.old_of_new[r];
+    const int b = R.rp[o], e = R.rp[o + 1];
+    const int start = R.rp_new[r];
+    const bool heavy = r < R.n_heavy;
+    int out = start;
+    long long hout = heavy ? R.hoff[r] : 0;
     for (int q0 = b; q0 < e; q0 += 32) {
       const int q = q0 + lane;
       int v = -1;
       bool act = false;
-      if (q < e) { v = idx[q]; act = cls[v] != C_INACTIVE; }
-      const int nv = act ? new_of_old[v] : 0;
-      const bool is_hot = act && heavy && nv < H;
+      if (q < e) { v = R.idx[q]; act = R.cls[v] != C_INACTIVE; }
+      const int nv = act ? R.new_of_old[v] : 0;
+      const bool is_hot = act && heavy && nv < R.H;
       const bool is_str = act && !is_hot;
       const unsigned m1 = __ballot_sync(kFull, is_str), m2 = __ballot_sync(kFull, is_hot);
       const unsigned below = (1u << lane) - 1u;
-      if (is_str) idx_new[out + __popc(m1 & below)] = nv;
-      if (is_hot) hot[hout + __popc(m2 & below)] = nv;
+      if (is_str) R.idx_new[out + __popc(m1 & below)] = nv;
+      if (is_hot) R.hot[hout + __popc(m2 & below)] = nv;
       out += __popc(m1);
       hout += __popc(m2);
     }
-    if (lane == 0 && out == start) idx_new[start] = n;
+    if (lane == 0 && out == start) R.idx_new[start] = R.n;
   }
 }
 
@@ -431,11 +590,18 @@ __global__ void k_split_fill(const int* rows, long long ns, const int* rp, int4*
 
 // ------------------------------------------------------------------ host helpers
 
-struct Tmp {  // RAII device buffer for temporaries
+// RAII device buffer for temporaries, stream-ordered (cudaMallocAsync from the device's
+// default pool; psi_build_graph raises the pool's release threshold so repeated ingests
+// reuse the memory instead of re-mapping it)
+thread_local cudaStream_t g_tmp_stream = nullptr;
+struct Tmp {
   void* p = nullptr;
   ~Tmp() { reset(); }
-  void reset() { if (p) cudaFree(p); p = nullptr; }
-  cudaError_t alloc(size_t bytes) { reset(); return cudaMalloc(&p, bytes ? bytes : 16); }
+  void reset() { if (p) cudaFreeAsync(p, g_tmp_stream); p = nullptr; }
+  cudaError_t alloc(size_t bytes) {
+    reset();
+    return cudaMallocAsync(&p, bytes ? bytes : 16, g_tmp_stream);
+  }
   template <class T> T* as() const { return (T*)p; }
 };
 
@@ -446,6 +612,50 @@ int grid_for(long long work, int block, int cap = 148 * 16) {
   return (int)g;
 }
 
+
+// indices r in [0, n) whose segment off[perm[r]] .. off[perm[r]+1] (perm = identity if NULL)
+// is longer than thr; returns the count (stream-synchronising)
+long long long_segments(const int* off, const int* perm, int n, int thr, cudaStream_t s,
+                        Tmp& list) {
+  Tmp flag, cnt, tmp;
+  if (flag.alloc((size_t)std::max(n, 1)) != cudaSuccess || cnt.alloc(sizeof(long long)) != cudaSuccess ||
+      list.alloc((size_t)std::max(n, 1) * sizeof(int)) != cudaSuccess)
+    return -1;
+  k_long_flags<<<grid_for(n, 256), 256, 0, s>>>(off, perm, n, thr, flag.as<unsigned char>());
+  cub::CountingInputIterator<int> it(0);
+  size_t tb = 0;
+  cub::DeviceSelect::Flagged(nullptr, tb, it, flag.as<unsigned char>(), list.as<int>(),
+                             cnt.as<long long>(), n, s);
+  if (tmp.alloc(tb) != cudaSuccess) return -1;
+  cub::DeviceSelect::Flagged(tmp.p, tb, it, flag.as<unsigned char>(), list.as<int>(),
+                             cnt.as<long long>(), n, s);
+  long long h = 0;
+  if (cudaMemcpyAsync(&h, cnt.p, sizeof(long long), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return -1;
+  return h;
+}
+
+// PSI_TRACE=1: per-phase wall time of the ingest on stderr (syncs the stream at each mark)
+struct Trace {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::chrono::steady_clock::time_point t0, last;
+  explicit Trace(cudaStream_t st) : s(st) {
+    const char* e = getenv("PSI_TRACE");
+    on = e && *e == '1';
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[psi ingest] %-28s %9.2f ms  (total %9.2f ms)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(),
+            std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
 
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
@@ -474,21 +684,8 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   const int nseg = out.nseg;
   std::vector<long long> hc(NH);
   IG_CK(cudaMemcpyAsync(hc.data(), hcnt.p, (size_t)NH * sizeof(long long), cudaMemcpyDeviceToHost, s));
-  // hot followers of each heavy row sorted by label (the k_row_fill order is unsorted)
-  if (n_ent > 0) {
-    Tmp tmp2, seg_tmp;
-    IG_CK(tmp2.alloc((size_t)n_ent * sizeof(int)));
-    cub::DoubleBuffer<int> kb(hot.as<int>(), tmp2.as<int>());
-    size_t tb = 0;
-    IG_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, kb, (int)n_ent, NH, hoff.as<long long>(),
-                                             hoff.as<long long>() + 1, s));
-    IG_CK(seg_tmp.alloc(tb));
-    IG_CK(cub::DeviceSegmentedSort::SortKeys(seg_tmp.p, tb, kb, (int)n_ent, NH, hoff.as<long long>(),
-                                             hoff.as<long long>() + 1, s));
-    if (kb.Current() != hot.as<int>())
-      IG_CK(cudaMemcpyAsync(hot.p, kb.Current(), (size_t)n_ent * sizeof(int),
-                            cudaMemcpyDeviceToDevice, s));
-  }
+  // the hot followers of each row stay in input order: the entries are sorted by
+  // (list, slot, label) below, and the round-robin virtual-row split only needs a fixed order
   IG_CK(cudaStreamSynchronize(s));
 
   int dev = 0, sms = 148;
@@ -605,6 +802,16 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   IG_CK(cudaMemsetAsync(flags.p, 0, sizeof(int), s));
   int hflags = 0;
 
+  Trace tr(s);
+  g_tmp_stream = s;
+  {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long keep = 64ull << 30;         // ingest temporaries stay reserved
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   // ---- 1. validation
   k_check_rowptr<<<grid_for(n, 256), 256, 0, s>>>(rp64, n, m, flags.as<int>());
   k_check_activity<<<grid_for(n, 256), 256, 0, s>>>(lam, mu, n, flags.as<int>());
@@ -633,6 +840,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     return PSI_E_ACTIVITY;
   }
 
+  tr.mark("validate");
   // ---- 2.-4. transpose, normalisers, constants (old labels)
   Tmp a_old, g_old, wt_old, d_old, first_leader, nlead, red;
   IG_CK(a_old.alloc((size_t)n * sizeof(double)));
@@ -656,24 +864,51 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     IG_CK(leader_s.alloc((size_t)m * sizeof(int)));
     IG_CK(follower_s.alloc((size_t)m * sizeof(int)));
     IG_CK(loff.alloc((size_t)(n + 1) * sizeof(int)));
-    k_expand<<<grid_for(n * 32, 256), 256, 0, s>>>(rp, idx_in, N, leader_e.as<int>(),
-                                                   follower_e.as<int>(), nlead.as<int>());
+    // (follower, leader) pairs in input order: keys = a copy of the input followers, values
+    // = the row (leader) of every edge; a stable radix sort by follower is the transpose
+    if (m > 0)
+      IG_CK(cudaMemcpyAsync(follower_e.p, idx_in, (size_t)m * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    k_expand_short<<<grid_for(n, 256), 256, 0, s>>>(rp, N, leader_e.as<int>());
+    {
+      Tmp longl;
+      const long long nl = long_segments(rp, nullptr, N, kShort, s, longl);
+      if (nl < 0) IG_CK(cudaErrorMemoryAllocation);
+      if (nl > 0)
+        k_expand_long<<<grid_for(nl * 32, 256), 256, 0, s>>>(longl.as<int>(), (int)nl, rp,
+                                                             leader_e.as<int>());
+    }
     cub::DoubleBuffer<unsigned> keys((unsigned*)follower_e.p, (unsigned*)follower_s.p);
     cub::DoubleBuffer<int> vals(leader_e.as<int>(), leader_s.as<int>());
     size_t tb = 0;
     IG_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, Mm, 0, end_bit, s));
     IG_CK(sort_tmp.alloc(tb));
     IG_CK(cub::DeviceRadixSort::SortPairs(sort_tmp.p, tb, keys, vals, Mm, 0, end_bit, s));
-    size_t sb = 0;
-    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, nlead.as<int>(), loff.as<int>(), N + 1, s));
-    IG_CK(scan_tmp.alloc(sb));
-    IG_CK(cub::DeviceScan::ExclusiveSum(scan_tmp.p, sb, nlead.as<int>(), loff.as<int>(), N + 1, s));
-    k_normalisers<<<grid_for(n * 32, 256), 256, 0, s>>>(
-        loff.as<int>(), vals.Current(), lam, mu, N, a_old.as<double>(), g_old.as<double>(),
+    // leaders of user u = sorted pairs [loff[u], loff[u+1]) (lower bounds); #leaders
+    k_lower_bounds<<<grid_for(n + 1, 256), 256, 0, s>>>(keys.Current(), Mm, N, loff.as<int>(),
+                                                        nlead.as<int>());
+    k_diff<<<grid_for(n, 256), 256, 0, s>>>(loff.as<int>(), N, nlead.as<int>());
+    Tmp lm, longu;
+    IG_CK(lm.alloc((size_t)n * sizeof(double2)));
+    k_pack_activity<<<grid_for(n, 256), 256, 0, s>>>(lam, mu, n, lm.as<double2>());
+    k_norm_short<<<grid_for(n, 256), 256, 0, s>>>(
+        loff.as<int>(), vals.Current(), lm.as<double2>(), N, a_old.as<double>(), g_old.as<double>(),
         wt_old.as<double>(), d_old.as<double>(), first_leader.as<int>(), kmax, cnt);
-    k_kappa_col<<<grid_for(n * 32, 256), 256, 0, s>>>(rp, idx_in, wt_old.as<double>(), lam, N, kmax);
+    long long nlong = long_segments(loff.as<int>(), nullptr, N, kShort, s, longu);
+    if (nlong < 0) IG_CK(cudaErrorMemoryAllocation);
+    if (nlong > 0)
+      k_norm_long<<<grid_for(nlong * 32, 256), 256, 0, s>>>(
+          longu.as<int>(), (int)nlong, loff.as<int>(), vals.Current(), lm.as<double2>(),
+          a_old.as<double>(), g_old.as<double>(), wt_old.as<double>(), d_old.as<double>(),
+          first_leader.as<int>(), kmax);
+    k_kappa_col_short<<<grid_for(n, 256), 256, 0, s>>>(rp, idx_in, wt_old.as<double>(), lam, N, kmax);
+    nlong = long_segments(rp, nullptr, N, kShort, s, longu);
+    if (nlong < 0) IG_CK(cudaErrorMemoryAllocation);
+    if (nlong > 0)
+      k_kappa_col_long<<<grid_for(nlong * 32, 256), 256, 0, s>>>(longu.as<int>(), (int)nlong, rp,
+                                                                 idx_in, wt_old.as<double>(), lam, kmax);
   }
 
+  tr.mark("transpose+normalisers");
   // ---- 5. relabel
   Tmp cls, new_of_old, key, sel, flag8, nsel, stage_tmp, sort_tmp2, sorted;
   IG_CK(cls.alloc((size_t)n));
@@ -781,6 +1016,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   out.relabel_levels = levels;
   key.reset(); sel.reset(); sorted.reset(); flag8.reset(); stage_tmp.reset(); sort_tmp2.reset();
 
+  tr.mark("relabel");
   // ---- 6. relabelled edge stream over active rows, folded constants
   const int NA = (int)out.n_act;
   Tmp cntr, K, rp_new;
@@ -793,10 +1029,18 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   IG_CK(hcnt.alloc((size_t)(NH + 1) * sizeof(long long)));
   IG_CK(hoff.alloc((size_t)(NH + 1) * sizeof(long long)));
   IG_CK(cudaMemsetAsync(hcnt.p, 0, (size_t)(NH + 1) * sizeof(long long), s));
-  if (NA > 0)
-    k_row_count<<<grid_for((long long)NA * 32, 256), 256, 0, s>>>(
-        rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
-        a_old.as<double>(), NA, NH, Hs, cntr.as<int>(), hcnt.as<long long>(), K.as<double>());
+  Tmp longr;
+  long long nlongr = 0;
+  if (NA > 0) {
+    nlongr = long_segments(rp, out.old_of_new, NA, kShort, s, longr);
+    if (nlongr < 0) IG_CK(cudaErrorMemoryAllocation);
+    RowCountArgs R{rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
+                   a_old.as<double>(), NA, NH, Hs, cntr.as<int>(), hcnt.as<long long>(),
+                   K.as<double>()};
+    k_row_count_short<<<grid_for(NA, 256), 256, 0, s>>>(R);
+    if (nlongr > 0)
+      k_row_count_long<<<grid_for(nlongr * 32, 256), 256, 0, s>>>(R, longr.as<int>(), (int)nlongr);
+  }
   long long n_hot_ent = 0;
   if (NH > 0) {
     Tmp scan_tmp;
@@ -826,36 +1070,31 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   out.ntiles = (int)(((long long)m_act + kTile - 1) / kTile);
   const long long m_pad = (long long)out.ntiles * kTile;
   {
-    Tmp idx2, seg_tmp;
     IG_CK(cudaMalloc(&out.edges, (size_t)(m_pad > 0 ? m_pad : 4) * sizeof(unsigned)));
-    IG_CK(idx2.alloc((size_t)(m_act > 0 ? m_act : 1) * sizeof(int)));
     int* ed = (int*)out.edges;
-    if (NA > 0)
-      k_row_fill<<<grid_for((long long)NA * 32, 256), 256, 0, s>>>(
-          rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
-          rp_new.as<int>(), NA, N, NH, Hs, hoff.as<long long>(), ed, hot.as<int>());
+    if (NA > 0) {
+      RowFillArgs R{rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
+                    rp_new.as<int>(), NA, N, NH, Hs, hoff.as<long long>(), ed, hot.as<int>()};
+      k_row_fill_short<<<grid_for(NA, 256), 256, 0, s>>>(R);
+      if (nlongr > 0)
+        k_row_fill_long<<<grid_for(nlongr * 32, 256), 256, 0, s>>>(R, longr.as<int>(), (int)nlongr);
+    }
+    // rows keep their followers in input order: the sweep's sums have a fixed order either
+    // way, and a per-row sort bought nothing measurable
     if (m_act > 0) {
-      cub::DoubleBuffer<int> kb(ed, idx2.as<int>());
-      size_t tb = 0;
-      IG_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, kb, m_act, NA, rp_new.as<int>(),
-                                               rp_new.as<int>() + 1, s));
-      IG_CK(seg_tmp.alloc(tb));
-      IG_CK(cub::DeviceSegmentedSort::SortKeys(seg_tmp.p, tb, kb, m_act, NA, rp_new.as<int>(),
-                                               rp_new.as<int>() + 1, s));
-      if (kb.Current() != ed)
-        IG_CK(cudaMemcpyAsync(ed, kb.Current(), (size_t)m_act * sizeof(int),
-                              cudaMemcpyDeviceToDevice, s));
       k_flag_rows<<<grid_for(NA, 256), 256, 0, s>>>(rp_new.as<int>(), NA, m_act, m_pad, N,
                                                     out.edges);
     }
     IG_CK(cudaStreamSynchronize(s));
   }
+  tr.mark("edge stream");
   if (NH > 0) {
     int rc2 = build_heavy_plan(out, NH, n_hot_ent, hot, hcnt, hoff, s, msg, msg_len);
     if (rc2 != PSI_OK) return rc2;
   }
   hot.reset();
 
+  tr.mark("heavy plan");
   const size_t na_b = (size_t)(NA > 0 ? NA : 1) * sizeof(double);
   IG_CK(cudaMalloc(&out.a0, (size_t)n * sizeof(double)));
   IG_CK(cudaMalloc(&out.wt, (size_t)n * sizeof(double)));
@@ -870,6 +1109,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
       out.lam, out.psi);
   out.relabeled = 1;
 
+  tr.mark("vectors");
   // ---- 7. edge tiles: first row of every tile, rows spanning tiles
   IG_CK(cudaMalloc(&out.tile_row, (size_t)(out.ntiles + 1) * sizeof(int)));
   k_tile_rows<<<grid_for(out.ntiles + 1, 256), 256, 0, s>>>(rp_new.as<int>(), NA, out.ntiles,
@@ -901,6 +1141,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     IG_CK(cudaStreamSynchronize(s));
   }
   IG_CK(cudaGetLastError());
+  tr.mark("tiles");
   return PSI_OK;
 }
 
