@@ -302,6 +302,19 @@ def run_ours(args, ws, rank, local):
 
     # ---- per-launch device time of the sweep kernels: CUDA events on the library's stream
     # around every k_tiles / k_fix launch (psi_time_sweep, direct launches, 20 sweeps)
+    # ---- PageRank power method (Eq. (22)) on the same ingested graph:
+    # the paper's "as fast as PageRank" comparison (Table IV), alpha = 0.85, same eps
+    pr_T, pr_ms = None, []
+    for i in range(3):
+        e0.record(stream)
+        _, pr_T, _ = g.pagerank(0.85, eps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i > 0:
+            pr_ms.append(e0.elapsed_time(e1))
+    pr_ms = statistics.median(pr_ms)
+    g.iterate(eps)   # leave the context at the psi solution
+
     g.time_sweep(3)
     heavy_ms, tiles_ms, fix_ms = g.time_sweep(20)
     sweep_ms = heavy_ms + tiles_ms + fix_ms
@@ -359,6 +372,10 @@ def run_ours(args, ws, rank, local):
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                    "what": "psi_build_graph(pinned host CSR) + psi_iterate(eps) + psi_get_psi(host)"},
            "roofline": roof, "clocks": clk.summary(),
+           "pagerank": {"what": "psi_pagerank: PageRank power method, Eq. (22), alpha = 0.85, "
+                                "same graph, eps and kernels (SURVEY 8(f) row 1)",
+                        "time_to_eps_ms": round(pr_ms, 3), "iterations_T": pr_T,
+                        "gteps": round(float(m) * pr_T / (pr_ms * 1e-3) / 1e9, 2)},
            "graph_info": {k: info[k] for k in ("n_f", "n_g", "n_leaderless", "kappa_row", "kappa_col",
                                                "rho_A", "num_tiles", "num_long_rows", "grid", "block", "hot_smem",
                                                "n_heavy", "heavy_entries", "heavy_panels", "heavy_labels",

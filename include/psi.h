@@ -139,10 +139,30 @@ psi_status psi_get_psi(const psi_ctx* ctx, double* out, int mem_kind);
 psi_status psi_get_series(const psi_ctx* ctx, double* out, int mem_kind);
 
 /* psi_get_residual_history -- raw epsilon_t = ||s_t - s_{t-1}||_1 for t = 1..T
- * (Eq. (15), NOT multiplied by ||B||) into host buffer `out` of capacity `cap`;
- * *len_out = T (the copy is truncated to min(T, cap, 2^24)).  PSI_E_STATE as above. */
+ * (Eq. (15), NOT multiplied by ||B||) of the most recent psi_iterate -- or ||pi_t - pi_{t-1}||_1
+ * if psi_pagerank ran last -- into host buffer `out` of capacity `cap`; *len_out = T (the
+ * copy is truncated to min(T, cap, 2^24)).  PSI_E_STATE if neither has run. */
 psi_status psi_get_residual_history(const psi_ctx* ctx, double* out, int64_t cap,
                                     int64_t* len_out);
+
+/*
+ * psi_pagerank -- the PageRank power method of PAPER.md Eq. (22) on the same
+ * graph and kernels (the paper's speed baseline, Table IV):
+ *     pi_0 = (1/N) 1,   pi_t^T = alpha pi_{t-1}^T W + (1 - alpha)/N 1^T,
+ * W = D_out^{-1} L, the walk from a follower to its leaders: (pi^T W)_i =
+ * sum_{j in F(i)} pi_j / |L(j)|; leaderless users' rows are zero (reading R5).  Stops when
+ * ||pi_t - pi_{t-1}||_1 <= eps (the pi-tolerance; the first test always passes)
+ * or at T = max_iters (PSI_NOT_CONVERGED, pi valid).  eps = 0 runs exactly max_iters sweeps
+ * unless an exact fp fixed point is reached.  alpha in [0, 1).  Blocks until done; the
+ * result is read with psi_get_pagerank.  Overwrites the iterate buffers (psi_get_series needs
+ * a new psi_iterate), not psi.  Errors: PSI_E_INVALID_ARG, PSI_E_NUMERIC, PSI_E_OOM, PSI_E_CUDA.
+ */
+psi_status psi_pagerank(psi_ctx* ctx, double alpha, double eps, int64_t max_iters,
+                        int64_t* iters_out, double* last_gap_out);
+
+/* psi_get_pagerank -- copy pi[n] of the last successful psi_pagerank (original labels) to a
+ * host or device buffer of n doubles.  PSI_E_STATE if psi_pagerank has not succeeded. */
+psi_status psi_get_pagerank(const psi_ctx* ctx, double* out, int mem_kind);
 
 /* psi_time_sweep -- measurement entry: runs `sweeps` sweeps of Eq. (14) from s_0 = c
  * (eps = 0) as direct stream launches and returns the average device time of each of the

@@ -39,8 +39,8 @@ _STATUS_NAMES = {0: "PSI_OK", 1: "PSI_NOT_CONVERGED", -1: "PSI_E_INVALID_ARG", -
                  -7: "PSI_E_NUMERIC"}
 
 EXPORTED = ["psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
-            "psi_get_residual_history", "psi_time_sweep", "psi_get_info", "psi_destroy",
-            "psi_last_error"]
+            "psi_get_residual_history", "psi_time_sweep", "psi_get_info", "psi_pagerank",
+            "psi_get_pagerank", "psi_destroy", "psi_last_error"]
 
 
 class PsiError(RuntimeError):
@@ -86,6 +86,8 @@ def load_library(build_if_stale: bool = True):
     lib.psi_iterate.argtypes = [vp, dbl, i64, ci, ctypes.POINTER(i64), ctypes.POINTER(dbl)]
     lib.psi_get_psi.argtypes = [vp, vp, ci]
     lib.psi_get_series.argtypes = [vp, vp, ci]
+    lib.psi_pagerank.argtypes = [vp, dbl, dbl, i64, ctypes.POINTER(i64), ctypes.POINTER(dbl)]
+    lib.psi_get_pagerank.argtypes = [vp, vp, ci]
     lib.psi_get_residual_history.argtypes = [vp, vp, i64, ctypes.POINTER(i64)]
     lib.psi_get_info.argtypes = [vp, ctypes.POINTER(psi_info)]
     lib.psi_time_sweep.argtypes = [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl),
@@ -94,7 +96,8 @@ def load_library(build_if_stale: bool = True):
     lib.psi_destroy.restype = None
     lib.psi_last_error.restype = ctypes.c_char_p
     for f in ("psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
-              "psi_get_residual_history", "psi_get_info", "psi_time_sweep"):
+              "psi_get_residual_history", "psi_get_info", "psi_time_sweep", "psi_pagerank",
+              "psi_get_pagerank"):
         getattr(lib, f).restype = ci
     _lib = lib
     return lib
@@ -176,6 +179,20 @@ class PsiGraph:
     def get_series(self, out=None, device: bool = True):
         """s_T[n] (Eq. (13)-(14)) in original labels."""
         return self._get(self._lib.psi_get_series, out, device)
+
+    def pagerank(self, alpha: float = 0.85, eps: float = 1e-9, max_iters: int = 100_000):
+        """PageRank power method, Eq. (22), on this graph: returns (status, T, gap_T)."""
+        T = ctypes.c_int64()
+        gap = ctypes.c_double()
+        st = self._lib.psi_pagerank(self._ctx, float(alpha), float(eps), int(max_iters),
+                                    ctypes.byref(T), ctypes.byref(gap))
+        if st < 0:
+            raise PsiError(st, _err(self._lib))
+        return st, T.value, gap.value
+
+    def get_pagerank(self, out=None, device: bool = True):
+        """pi[n] of the last pagerank() in the caller's original labels (torch.float64)."""
+        return self._get(self._lib.psi_get_pagerank, out, device)
 
     def get_residual_history(self) -> np.ndarray:
         n = ctypes.c_int64()

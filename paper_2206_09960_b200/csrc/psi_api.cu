@@ -74,6 +74,13 @@ struct psi_ctx {
   double ingest_ms = 0, iterate_ms = 0;
   size_t device_bytes = 0;
   long long hot_lim = 0;         // x labels kept in L2 with evict_last (both buffers)
+  PrBuffers pr;                  // PageRank constants and result (allocated on first use)
+  cudaGraph_t pr_graph = nullptr;
+  cudaGraphExec_t pr_exec = nullptr;
+  bool have_pr = false;          // psi_get_pagerank valid
+  bool series_ok = false;        // x holds the psi iterate s_T / Wt (no PageRank run since)
+  long long pr_T = 0;
+  double pr_alpha = 0.0;
   double* hhot = nullptr;        // [n_heavy] heavy rows' sums over followers < H (k_heavy)
   int heavy_grid = 0;
   size_t heavy_smem = 0;
@@ -85,6 +92,11 @@ void free_ctx(psi_ctx* c) {
   if (!c) return;
   if (c->exec) cudaGraphExecDestroy(c->exec);
   if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->pr_exec) cudaGraphExecDestroy(c->pr_exec);
+  if (c->pr_graph) cudaGraphDestroy(c->pr_graph);
+  for (void* p : {(void*)c->pr.a, (void*)c->pr.a_first, (void*)c->pr.g, (void*)c->pr.dt,
+                  (void*)c->pr.x0, (void*)c->pr.pi, (void*)c->g.nlead, (void*)c->g.kinv})
+    if (p) cudaFree(p);
   void* ptrs[] = {c->g.edges, c->g.tile_row, c->g.a0, c->g.a1, c->g.g, c->g.wt, c->g.d1,
                   c->g.lam, c->g.psi, c->g.old_of_new, c->g.split, c->x[0], c->x[1],
                   c->p_in, c->p_out, c->eps_part1, c->eps_part2, c->history, c->st, c->prm,
@@ -156,24 +168,37 @@ cudaError_t add_kernel(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode
   return cudaGraphAddKernelNode(node, g, dep, ndep, &p);
 }
 
-psi_status build_graph_exec(psi_ctx* c) {
-  API_CK(cudaGraphCreate(&c->graph, 0));
+// The PageRank variant of the sweep arguments: the same kernels with Eq. (22)'s constants.
+void pagerank_args(const psi_ctx* c, SweepArgs& A) {
+  A.a0 = c->pr.x0;
+  A.a = c->pr.a;
+  A.a_first = c->pr.a_first;
+  A.g = c->pr.g;
+  A.wt = c->pr.dt;
+}
+
+// Power-psi:  k_init -> WHILE { sweep } -> readout.   PageRank: k_init -> WHILE { sweep }.
+psi_status build_graph_exec(psi_ctx* c, bool pagerank = false) {
+  cudaGraph_t& graph = pagerank ? c->pr_graph : c->graph;
+  cudaGraphExec_t& exec = pagerank ? c->pr_exec : c->exec;
+  API_CK(cudaGraphCreate(&graph, 0));
   cudaGraphConditionalHandle cond;
-  API_CK(cudaGraphConditionalHandleCreate(&cond, c->graph, 0, cudaGraphCondAssignDefault));
+  API_CK(cudaGraphConditionalHandleCreate(&cond, graph, 0, cudaGraphCondAssignDefault));
   SweepArgs A = make_args(c, cond);
+  if (pagerank) pagerank_args(c, A);
   int n_int = (int)c->n;
 
   cudaGraphNode_t n_init, n_while, n_r1, n_r2;
   int init_grid = (int)std::min<long long>((c->n + 255) / 256, 148LL * 8);
   if (init_grid < 1) init_grid = 1;
-  API_CK(add_kernel(c->graph, &n_init, nullptr, 0, init_kernel_ptr(), init_grid, 256, &A, &n_int));
+  API_CK(add_kernel(graph, &n_init, nullptr, 0, init_kernel_ptr(), init_grid, 256, &A, &n_int));
 
   cudaGraphNodeParams cp{};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = cond;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
-  API_CK(cudaGraphAddNode(&n_while, c->graph, &n_init, 1, &cp));
+  API_CK(cudaGraphAddNode(&n_while, graph, &n_init, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   cudaGraphNode_t b0, b1, b2, n_r0;
   const bool hv = c->g.n_heavy > 0;
@@ -184,13 +209,15 @@ psi_status build_graph_exec(psi_ctx* c) {
                     &A, nullptr, c->tc.smem));
   API_CK(add_kernel(body, &b2, &b1, 1, fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr));
 
-  if (hv)
-    API_CK(add_kernel(c->graph, &n_r0, &n_while, 1, heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock,
-                      &A, nullptr, c->heavy_smem));
-  API_CK(add_kernel(c->graph, &n_r1, hv ? &n_r0 : &n_while, 1, c->tc.readout, c->grid1,
-                    c->tc.block, &A, nullptr, c->tc.smem));
-  API_CK(add_kernel(c->graph, &n_r2, &n_r1, 1, fix_kernel_ptr(true), c->grid2, kFixBlock, &A, nullptr));
-  API_CK(cudaGraphInstantiate(&c->exec, c->graph, 0));
+  if (!pagerank) {
+    if (hv)
+      API_CK(add_kernel(graph, &n_r0, &n_while, 1, heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock,
+                        &A, nullptr, c->heavy_smem));
+    API_CK(add_kernel(graph, &n_r1, hv ? &n_r0 : &n_while, 1, c->tc.readout, c->grid1,
+                      c->tc.block, &A, nullptr, c->tc.smem));
+    API_CK(add_kernel(graph, &n_r2, &n_r1, 1, fix_kernel_ptr(true), c->grid2, kFixBlock, &A, nullptr));
+  }
+  API_CK(cudaGraphInstantiate(&exec, graph, 0));
   return PSI_OK;
 }
 
@@ -204,8 +231,9 @@ cudaError_t launch(void* fn, int grid, int block, SweepArgs* A, int* extra, cuda
 // psi_time_sweep and, with PSI_GRAPH=0, by psi_iterate (profilers cannot see kernel nodes
 // of graphs with conditional nodes).  The stop rule is evaluated on the host after every
 // sweep from the device LoopState, exactly as the graph's WHILE condition does.
-psi_status iterate_direct(psi_ctx* c) {
+psi_status iterate_direct(psi_ctx* c, bool pagerank = false) {
   SweepArgs A = make_args(c, 0);
+  if (pagerank) pagerank_args(c, A);
   A.use_cond = 0;
   int n_int = (int)c->n;
   int init_grid = (int)std::min<long long>((c->g.n_act + 255) / 256, 148LL * 8);
@@ -213,7 +241,7 @@ psi_status iterate_direct(psi_ctx* c) {
   API_CK(launch(init_kernel_ptr(), init_grid, 256, &A, &n_int, c->stream));
   const double eps = c->h_prm->eps;
   const long long max_iters = c->h_prm->max_iters;
-  bool cont = 1.0 > eps && max_iters > 0;
+  bool cont = c->h_prm->gap0 > eps && max_iters > 0;
   while (cont) {
     if (c->g.n_heavy > 0)
       API_CK(launch(heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock, &A, nullptr, c->stream,
@@ -224,6 +252,7 @@ psi_status iterate_direct(psi_ctx* c) {
     API_CK(cudaStreamSynchronize(c->stream));
     cont = !(c->h_st->status & 1) && c->h_st->gap > eps && c->h_st->iter < max_iters;
   }
+  if (pagerank) return PSI_OK;
   if (c->g.n_heavy > 0)
     API_CK(launch(heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock, &A, nullptr, c->stream,
                   c->heavy_smem));
@@ -434,8 +463,11 @@ psi_status psi_iterate(psi_ctx* c, double eps, int64_t max_iters, int norm, int6
   c->h_prm->kappa = kappa;
   c->h_prm->history = c->history;
   c->h_prm->hist_cap = c->hist_cap;
+  c->h_prm->gap0 = 1.0;                               // Alg. 2 line 4
+  c->h_prm->eps1_extra = 0.0;
   API_CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(LoopParams), cudaMemcpyHostToDevice, c->stream));
   API_CK(cudaEventRecord(c->ev0, c->stream));
+  c->series_ok = false;
   if (use_graph()) {
     API_CK(cudaGraphLaunch(c->exec, c->stream));
   } else {
@@ -455,6 +487,7 @@ psi_status psi_iterate(psi_ctx* c, double eps, int64_t max_iters, int norm, int6
   if (c->h_st->status & 1)
     return fail(PSI_E_NUMERIC, "epsilon_t became non-finite at t = %lld", c->last_T);
   c->have_psi = true;
+  c->series_ok = true;
   if (c->last_gap > eps) {
     fail(PSI_NOT_CONVERGED, "not converged: gap %.3e > eps %.3e after %lld sweeps",
          c->last_gap, eps, c->last_T);
@@ -477,7 +510,8 @@ psi_status psi_get_series(const psi_ctx* c, double* out, int mem_kind) {
   if (!c || !out) return fail(PSI_E_INVALID_ARG, "NULL argument");
   if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
     return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
-  if (!c->have_psi) return fail(PSI_E_STATE, "no successful psi_iterate on this context");
+  if (!c->have_psi || !c->series_ok)
+    return fail(PSI_E_STATE, "no psi_iterate since the last psi_pagerank / psi_time_sweep");
   // s_T = Wt * x_T (kernel state, psi_internal.cuh)
   return copy_out(c, c->x[c->last_T & 1], c->g.wt, out, mem_kind);
 }
@@ -485,7 +519,8 @@ psi_status psi_get_series(const psi_ctx* c, double* out, int mem_kind) {
 psi_status psi_get_residual_history(const psi_ctx* c, double* out, int64_t cap, int64_t* len_out) {
   g_err.clear();
   if (!c || (cap > 0 && !out)) return fail(PSI_E_INVALID_ARG, "NULL argument");
-  if (!c->have_psi) return fail(PSI_E_STATE, "no successful psi_iterate on this context");
+  if (!c->have_psi && !c->have_pr)
+    return fail(PSI_E_STATE, "no successful psi_iterate / psi_pagerank on this context");
   if (len_out) *len_out = c->last_T;
   long long k = c->last_T;
   if (k > cap) k = cap;
@@ -538,7 +573,10 @@ psi_status psi_time_sweep(psi_ctx* c, int64_t sweeps, double* heavy_ms, double* 
   c->h_prm->kappa = c->g.kappa_row;
   c->h_prm->history = c->history;
   c->h_prm->hist_cap = c->hist_cap;
+  c->h_prm->gap0 = 1.0;
+  c->h_prm->eps1_extra = 0.0;
   API_CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(LoopParams), cudaMemcpyHostToDevice, c->stream));
+  c->series_ok = false;
   SweepArgs A = make_args(c, 0);
   A.use_cond = 0;
   int n_int = (int)c->n;
@@ -576,6 +614,82 @@ psi_status psi_time_sweep(psi_ctx* c, int64_t sweeps, double* heavy_ms, double* 
   if (tiles_ms) *tiles_ms = t1 / sweeps;
   if (fix_ms) *fix_ms = t2 / sweeps;
   return PSI_OK;
+}
+
+psi_status psi_pagerank(psi_ctx* c, double alpha, double eps, int64_t max_iters,
+                        int64_t* iters_out, double* last_gap_out) {
+  g_err.clear();
+  if (!c) return fail(PSI_E_INVALID_ARG, "ctx is NULL");
+  if (!(alpha >= 0.0 && alpha < 1.0)) return fail(PSI_E_INVALID_ARG, "alpha must be in [0, 1)");
+  if (!(eps >= 0.0)) return fail(PSI_E_INVALID_ARG, "eps must be >= 0 (got %g)", eps);
+  if (max_iters < 0) return fail(PSI_E_INVALID_ARG, "max_iters must be >= 0");
+  const long long n = c->n, na = std::max<long long>(c->g.n_act, 1);
+  if (!c->pr.a) {
+    API_CK(cudaMalloc(&c->pr.a, na * sizeof(double)));
+    API_CK(cudaMalloc(&c->pr.a_first, na * sizeof(double)));
+    API_CK(cudaMalloc(&c->pr.g, na * sizeof(double)));
+    API_CK(cudaMalloc(&c->pr.dt, n * sizeof(double)));
+    API_CK(cudaMalloc(&c->pr.x0, n * sizeof(double)));
+    API_CK(cudaMalloc(&c->pr.pi, n * sizeof(double)));
+    c->device_bytes += (3 * na + 3 * n) * sizeof(double);
+  }
+  c->have_pr = false;
+  API_CK(pagerank_prep(c->g, n, alpha, c->pr, c->stream));
+  psi_status hs = ensure_history(c, max_iters);
+  if (hs != PSI_OK) return hs;
+  c->h_prm->eps = eps;
+  c->h_prm->max_iters = max_iters;
+  c->h_prm->kappa = 1.0;                              // stop on ||pi_t - pi_{t-1}||_1 itself
+  c->h_prm->history = c->history;
+  c->h_prm->hist_cap = c->hist_cap;
+  c->h_prm->gap0 = INFINITY;                          // the oracle's first test always passes
+  // follower-less users are not swept; in the first sweep each one's pi moves by alpha/N
+  c->h_prm->eps1_extra = (double)(c->n - c->g.n_act) * alpha / (double)c->n;
+  API_CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(LoopParams), cudaMemcpyHostToDevice, c->stream));
+  c->series_ok = false;
+  API_CK(cudaEventRecord(c->ev0, c->stream));
+  if (use_graph()) {
+    if (!c->pr_exec) {
+      psi_status gs = build_graph_exec(c, true);
+      if (gs != PSI_OK) return gs;
+    }
+    API_CK(cudaGraphLaunch(c->pr_exec, c->stream));
+  } else {
+    psi_status ds = iterate_direct(c, true);
+    if (ds != PSI_OK) return ds;
+  }
+  API_CK(cudaEventRecord(c->ev1, c->stream));
+  API_CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(LoopState), cudaMemcpyDeviceToHost, c->stream));
+  API_CK(cudaStreamSynchronize(c->stream));
+  float ms = 0;
+  API_CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  c->iterate_ms = ms;
+  const long long T = c->h_st->iter;
+  const double gap = c->h_st->gap;
+  c->last_T = T;
+  c->last_gap = gap;
+  if (iters_out) *iters_out = T;
+  if (last_gap_out) *last_gap_out = gap;
+  if (c->h_st->status & 1) return fail(PSI_E_NUMERIC, "||pi_t - pi_(t-1)|| became non-finite at t = %lld", T);
+  API_CK(pagerank_readout(c->g, n, alpha, (T & 1) ? c->x[1] : c->x[0], T, c->pr, c->stream));
+  API_CK(cudaStreamSynchronize(c->stream));
+  c->pr_T = T;
+  c->pr_alpha = alpha;
+  c->have_pr = true;
+  if (gap > eps) {
+    fail(PSI_NOT_CONVERGED, "not converged: gap %.3e > eps %.3e after %lld sweeps", gap, eps, T);
+    return PSI_NOT_CONVERGED;
+  }
+  return PSI_OK;
+}
+
+psi_status psi_get_pagerank(const psi_ctx* c, double* out, int mem_kind) {
+  g_err.clear();
+  if (!c || !out) return fail(PSI_E_INVALID_ARG, "NULL argument");
+  if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
+    return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
+  if (!c->have_pr) return fail(PSI_E_STATE, "no successful psi_pagerank on this context");
+  return copy_out(c, c->pr.pi, nullptr, out, mem_kind);
 }
 
 void psi_destroy(psi_ctx* c) { free_ctx(c); }

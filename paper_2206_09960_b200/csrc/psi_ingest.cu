@@ -373,8 +373,8 @@ __global__ void k_mark_heavy(const int* act, int n, int min_act, unsigned char* 
 // follower-less followers.  Thread per short row / warp per long row (see kShort).
 struct RowCountArgs {
   const int* rp; const int* idx; const int* old_of_new; const unsigned char* cls;
-  const int* new_of_old; const double* a_old; int n_act, n_heavy, H;
-  int* cnt; long long* hc; double* K;
+  const int* new_of_old; const double* a_old; const int* nlead; int n_act, n_heavy, H;
+  int* cnt; long long* hc; double* K; double* Kinv;
 };
 
 __global__ void k_row_count_short(RowCountArgs R) {
@@ -384,15 +384,18 @@ __global__ void k_row_count_short(RowCountArgs R) {
     if (e - b > kShort) continue;
     const bool heavy = r < R.n_heavy;
     int c = 0, h = 0;
-    double k = 0.0;
+    double k = 0.0, ki = 0.0;
     for (int q = b; q < e; ++q) {
       const int v = R.idx[q];
-      if (R.cls[v] == C_INACTIVE) k += R.a_old[v];
-      else if (heavy && R.new_of_old[v] < R.H) ++h;
+      if (R.cls[v] == C_INACTIVE) {
+        k += R.a_old[v];
+        ki += 1.0 / (double)max(R.nlead[v], 1);
+      } else if (heavy && R.new_of_old[v] < R.H) ++h;
       else ++c;
     }
     R.cnt[r] = c > 0 ? c : 1;      // 0 -> one pseudo edge
     R.K[r] = k;
+    R.Kinv[r] = ki;
     if (heavy) R.hc[r] = h;
   }
 }
@@ -405,20 +408,26 @@ __global__ void k_row_count_long(RowCountArgs R, const int* list, int nlist) {
     const int b = R.rp[o], e = R.rp[o + 1];
     const bool heavy = r < R.n_heavy;
     int c = 0, h = 0;
-    double k = 0.0;
+    double k = 0.0, ki = 0.0;
     for (int q = b + lane; q < e; q += 32) {
       const int v = R.idx[q];
-      if (R.cls[v] == C_INACTIVE) k += R.a_old[v];
-      else if (heavy && R.new_of_old[v] < R.H) ++h;
+      if (R.cls[v] == C_INACTIVE) {
+        k += R.a_old[v];
+        ki += 1.0 / (double)max(R.nlead[v], 1);
+      } else if (heavy && R.new_of_old[v] < R.H) ++h;
       else ++c;
     }
     c = __reduce_add_sync(kFull, c);
     h = __reduce_add_sync(kFull, h);
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) k += __shfl_xor_sync(kFull, k, s);
+    for (int s = 16; s > 0; s >>= 1) {
+      k += __shfl_xor_sync(kFull, k, s);
+      ki += __shfl_xor_sync(kFull, ki, s);
+    }
     if (lane == 0) {
       R.cnt[r] = c > 0 ? c : 1;
       R.K[r] = k;
+      R.Kinv[r] = ki;
       if (heavy) R.hc[r] = h;
     }
   }
@@ -543,11 +552,13 @@ __global__ void k_flag_rows(const int* rp_new, int n_act, long long m_act, long 
 __global__ void k_permute_vectors(const int* old_of_new, int n, int n_act, const double* a_old,
                                   const double* g_old, const double* wt_old, const double* d_old,
                                   const double* lam, const double* K, double n_users,
-                                  double* a0, double* a1, double* g1, double* wt_new, double* d1,
-                                  double* lam1, double* psi) {
+                                  const int* nlead_old, double* a0, double* a1, double* g1,
+                                  double* wt_new, double* d1, double* lam1, double* psi,
+                                  int* nlead_new) {
   GRID_STRIDE(r, n) {
     const int o = old_of_new[r];
     a0[r] = a_old[o];
+    nlead_new[r] = nlead_old[o];
     wt_new[r] = wt_old[o];
     if (r < n_act) {
       const double k = K[r];
@@ -1020,6 +1031,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   // ---- 6. relabelled edge stream over active rows, folded constants
   const int NA = (int)out.n_act;
   Tmp cntr, K, rp_new;
+  IG_CK(cudaMalloc(&out.kinv, (size_t)(NA > 0 ? NA : 1) * sizeof(double)));
   IG_CK(cntr.alloc((size_t)(NA + 1) * sizeof(int)));
   IG_CK(K.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(double)));
   IG_CK(rp_new.alloc((size_t)(NA + 1) * sizeof(int)));
@@ -1035,8 +1047,8 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     nlongr = long_segments(rp, out.old_of_new, NA, kShort, s, longr);
     if (nlongr < 0) IG_CK(cudaErrorMemoryAllocation);
     RowCountArgs R{rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
-                   a_old.as<double>(), NA, NH, Hs, cntr.as<int>(), hcnt.as<long long>(),
-                   K.as<double>()};
+                   a_old.as<double>(), nlead.as<int>(), NA, NH, Hs, cntr.as<int>(),
+                   hcnt.as<long long>(), K.as<double>(), out.kinv};
     k_row_count_short<<<grid_for(NA, 256), 256, 0, s>>>(R);
     if (nlongr > 0)
       k_row_count_long<<<grid_for(nlongr * 32, 256), 256, 0, s>>>(R, longr.as<int>(), (int)nlongr);
@@ -1103,10 +1115,11 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   IG_CK(cudaMalloc(&out.g, na_b));
   IG_CK(cudaMalloc(&out.d1, na_b));
   IG_CK(cudaMalloc(&out.lam, na_b));
+  IG_CK(cudaMalloc(&out.nlead, (size_t)n * sizeof(int)));
   k_permute_vectors<<<grid_for(n, 256), 256, 0, s>>>(
       out.old_of_new, N, NA, a_old.as<double>(), g_old.as<double>(), wt_old.as<double>(),
-      d_old.as<double>(), lam, K.as<double>(), (double)n, out.a0, out.a1, out.g, out.wt, out.d1,
-      out.lam, out.psi);
+      d_old.as<double>(), lam, K.as<double>(), (double)n, nlead.as<int>(), out.a0, out.a1, out.g,
+      out.wt, out.d1, out.lam, out.psi, out.nlead);
   out.relabeled = 1;
 
   tr.mark("vectors");

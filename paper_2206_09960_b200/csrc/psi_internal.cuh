@@ -63,6 +63,8 @@ struct LoopParams {
   double kappa;          // ||B|| for the selected norm
   double* history;       // epsilon_t, t = 1..T
   long long hist_cap;
+  double gap0;           // gap before the first sweep: 1 (Alg. 2 line 4) or +inf (PageRank)
+  double eps1_extra;     // added to eps_1: PageRank's follower-less users move 1/N -> (1-alpha)/N
 };
 
 // Device view of the heavy-row plan (built at ingest, psi_ingest.cu).
@@ -87,6 +89,7 @@ struct SweepArgs {
   double* p_out;             // per tile: partial of the last row started in it, if it continues
   const double* a0;          // x_0 (init)                       [n_act]
   const double* a;           // sweep constant a + g K           [n_act]
+  const double* a_first;     // constant of the first sweep if different (PageRank), else NULL
   const double* g;           //                                  [n_act]
   const double* wt;          // Wt                               [n]
   const double* d;           // readout constant d + lambda K    [n_act]
@@ -142,6 +145,8 @@ struct IngestOut {
   double* lam = nullptr;      // [n_act]
   double* psi = nullptr;      // [n]     readout buffer; [n_act, n) prefilled with d/N
   int* old_of_new = nullptr;  // [n]
+  int* nlead = nullptr;       // [n]     #leaders |L(j)| (PageRank out-degree), new labels
+  double* kinv = nullptr;     // [n_act] sum over follower-less followers n of 1/max(|L(n)|, 1)
   int ntiles = 0;
   int4* split = nullptr;
   int nsplit = 0;
@@ -160,6 +165,20 @@ struct IngestOut {
   long long n_f = 0, n_g = 0, n_leaderless = 0;
   int relabeled = 0;
 };
+
+// ---- PageRank (psi_pagerank.cu): constants of Eq. (22) in the sweep's kernel state
+struct PrBuffers {
+  double* a = nullptr;        // [n_act] sweep constant (t >= 2)
+  double* a_first = nullptr;  // [n_act] sweep constant of the first sweep
+  double* g = nullptr;        // [n_act] alpha / Dt
+  double* dt = nullptr;       // [n]     Dt = max(|L(j)|, 1): pi = Dt x
+  double* x0 = nullptr;       // [n]     x_0 = 1 / (N Dt)
+  double* pi = nullptr;       // [n]     result, relabelled order
+};
+cudaError_t pagerank_prep(const IngestOut& G, long long n, double alpha, const PrBuffers& B,
+                          cudaStream_t s);
+cudaError_t pagerank_readout(const IngestOut& G, long long n, double alpha, const double* xT,
+                             long long T, const PrBuffers& B, cudaStream_t s);
 
 // Returns 0 or a negative psi_status; msg gets a description on error.
 int ingest(long long n, long long m, const long long* rp64_dev, const int* idx_dev,

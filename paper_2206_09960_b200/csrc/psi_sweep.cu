@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_t
   const unsigned single_lo = (unsigned)A.single_lo;
   const int ntiles = A.ntiles;
   const bool st_last = A.st_last;
+  const double* __restrict__ acon = (t == 0 && A.a_first) ? A.a_first : A.a;
   double eps_acc = 0.0;
 
   for (unsigned i = threadIdx.x; i < hs; i += blockDim.x) hot[i] = __ldcg(xs + i);
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_t
         A.psi[r] = (ld_stream(A.d + r, pf) + ld_stream(A.lam + r, pf) * Sr) / A.n_users;
       } else {
         const unsigned long long px = (unsigned)r < hot_lim ? pl : pf;
-        const double xn = fma(ld_stream(A.g + r, pf), Sr, ld_stream(A.a + r, pf));
+        const double xn = fma(ld_stream(A.g + r, pf), Sr, ld_stream(acon + r, pf));
         eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - ld_hint_na(xs + r, px));
         st_hint(xd + r, xn, st_last ? px : pf);
       }
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
     if (READOUT) {
       A.psi[r] = (A.d[r] + A.lam[r] * S) / A.n_users;
     } else {
-      const double xn = fma(A.g[r], S, A.a[r]);
+      const double xn = fma(A.g[r], S, ((t == 0 && A.a_first) ? A.a_first : A.a)[r]);
       eps_acc += A.wt[r] * fabs(xn - xs[r]);
       xd[r] = xn;
     }
@@ -319,8 +320,8 @@ __global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
   for (int q = tid; q < (int)gridDim.x; q += kFixBlock) v += __ldcg(A.eps_part2 + q);
   const double e2 = block_sum<kFixBlock>(v, red);
   if (tid == 0) {
-    const double eps_t = e1 + e2;
     const LoopParams P = *A.prm;
+    const double eps_t = e1 + e2 + (t == 0 ? P.eps1_extra : 0.0);
     if (t < P.hist_cap) P.history[t] = eps_t;
     const double gap = P.kappa * eps_t;
     const bool bad = !isfinite(eps_t);
@@ -341,13 +342,13 @@ __global__ void k_init(SweepArgs A, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n_act; i += stride) A.x0[i] = A.a0[i];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.st->iter = 0;
-    A.st->gap = 1.0;
+    A.st->gap = A.prm->gap0;
     A.st->eps_t = 0.0;
     A.st->done = 0;
     A.st->status = 0;
     A.st->heavy_next = 0;
     const LoopParams P = *A.prm;
-    if (A.use_cond) cudaGraphSetConditional(A.cond, (1.0 > P.eps && P.max_iters > 0) ? 1u : 0u);
+    if (A.use_cond) cudaGraphSetConditional(A.cond, (P.gap0 > P.eps && P.max_iters > 0) ? 1u : 0u);
   }
 }
 
