@@ -72,54 +72,73 @@ __device__ __forceinline__ void ld_stream8(const unsigned* p, unsigned (&w)[8]) 
 // One warp's pass over one list (panel, warp, segment) chunk: 8 entries per lane, gathers
 // from the staged segment, runs of equal slots summed in registers and across lanes (a
 // segmented scan), each finished run added once to its slot sum (owned by this warp).
+// predicated shared-memory read-modify-write (no branch: runs end at data-dependent lanes)
+__device__ __forceinline__ void sadd_if(bool p, const double* base, unsigned idx, double v) {
+  asm volatile(
+      "{\n"
+      ".reg .pred q;\n"
+      ".reg .f64 t;\n"
+      "setp.ne.u32 q, %0, 0;\n"
+      "@q ld.shared.f64 t, [%1];\n"
+      "@q add.rn.f64 t, t, %2;\n"
+      "@q st.shared.f64 [%1], t;\n"
+      "}\n" :: "r"((unsigned)p), "r"(smem_u32(base) + idx * 8u), "d"(v) : "memory");
+}
+
+// One warp's pass over one chunk of a list (panel, warp, segment): 8 entries per lane,
+// gathers from the staged segment, runs of equal slots summed in registers (inclusive run
+// sums) and across lanes (a segmented scan), each finished run added once to its slot sum
+// (owned by this warp) -- branch-free.
 __device__ __forceinline__ void process_chunk(const unsigned (&w)[8], const double* seg,
                                               double* rowsum, int lane, double& carry,
                                               unsigned& carry_slot) {
   unsigned sl[8];
-  double v[8];
+  double acc[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     sl[k] = w[k] >> kSegShift;
-    v[k] = seg[w[k] & (kSeg - 1)];
+    acc[k] = seg[w[k] & (kSeg - 1)];
   }
-  // per-lane runs: emit the internal ones, keep head (first run) and tail (last run)
-  double head = v[0], run = v[0];
   bool single = true;
 #pragma unroll
   for (int k = 1; k < 8; ++k) {
-    if (sl[k] != sl[k - 1]) {
-      if (single) head = run;
-      else rowsum[sl[k - 1]] += run;                  // a run wholly inside this lane
-      single = false;
-      run = 0.0;
-    }
-    run += v[k];
+    const bool same = sl[k] == sl[k - 1];
+    acc[k] = same ? acc[k - 1] + acc[k] : acc[k];
+    single = single && same;
   }
   // lane-crossing runs: the open value leaving lane l is
   //   out_l = (single_l && cont_l) ? out_{l-1} + run_l : run_l,   out_{-1} = carry
-  // = a segmented inclusive scan of run with resets f_l = !(single_l && cont_l).
+  // = a segmented inclusive scan of the lane's tail run with resets f_l = !(single_l && cont_l).
   const unsigned prev_last = __shfl_up_sync(kFull, sl[7], 1);
   const bool cont = lane == 0 ? (sl[0] == carry_slot) : (sl[0] == prev_last);
   // the run carried from the previous chunk ended at the chunk boundary
-  if (lane == 0 && !cont && carry_slot != kHeavySlots) rowsum[carry_slot] += carry;
+  sadd_if(lane == 0 && !cont && carry_slot != kHeavySlots, rowsum, carry_slot, carry);
   int f = !(single && cont);
-  double val = run;
+  double val = acc[7];
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const double v2 = __shfl_up_sync(kFull, val, o);
     const int f2 = __shfl_up_sync(kFull, f, o);
     if (lane >= o) {
-      if (!f) val += v2;
+      val = f ? val : val + v2;
       f |= f2;
     }
   }
   const double out = f ? val : val + carry;          // chain reaching back to the carry
   double in = __shfl_up_sync(kFull, out, 1);
   if (lane == 0) in = carry;
-  if (!single) rowsum[sl[0]] += (cont ? in : 0.0) + head;   // the head run ends here
+  // runs ending inside the lane; the first one (head) continues a run from earlier lanes
+  // when cont
+  bool head = true;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    const bool b = sl[k] != sl[k + 1];
+    sadd_if(b, rowsum, sl[k], acc[k] + ((head && cont) ? in : 0.0));
+    head = head && !b;
+  }
   // the tail run ends at the lane boundary when the next lane starts another slot
   const bool next_cont = __shfl_down_sync(kFull, cont, 1);
-  if (lane < 31 && !next_cont) rowsum[sl[7]] += out;
+  sadd_if(lane < 31 && !next_cont, rowsum, sl[7], out);
   carry = __shfl_sync(kFull, out, 31);
   carry_slot = __shfl_sync(kFull, sl[7], 31);
   __syncwarp();

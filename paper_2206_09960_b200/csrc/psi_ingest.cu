@@ -943,7 +943,9 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   // heavy rows (psi_heavy.cu): active users with >= heavy_min active followers, labelled
   // first; their followers with label < H = nseg * kSeg are summed by k_heavy from staged
   // shared-memory segments.  Disabled for graphs smaller than one segment.
-  int nseg = env_int("PSI_HEAVY_SEGS", kDefaultHeavySegs);   // in units of kSeg labels
+  long long h_default = kMinHeavyLabels;
+  while (h_default * 2 <= n / 32 && h_default < kMaxHeavyLabels) h_default *= 2;
+  int nseg = env_int("PSI_HEAVY_LABELS", (int)h_default) / kSeg;
   // on by default only where it measured faster (C5 yes, C4 no); PSI_HEAVY=1/0
   // forces it on/off
   const int heavy_env = env_int("PSI_HEAVY", -1);

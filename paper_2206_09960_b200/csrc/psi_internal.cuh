@@ -29,18 +29,20 @@ constexpr int kTile = kBlock * kEpt;     // 2048 edges per tile
 constexpr int kFixBlock = 256;           // threads per CTA of the split-row fix-up kernel
 constexpr unsigned kRowFlag = 0x80000000u;
 // staged-segment heavy-row kernel (psi_heavy.cu)
-constexpr int kSegShift = 12;
-constexpr int kSeg = 1 << kSegShift;     // labels of x per TMA-staged segment (32 KB)
+constexpr int kSegShift = 13;
+constexpr int kSeg = 1 << kSegShift;     // labels of x per TMA-staged segment (64 KB)
 constexpr int kHeavySlots = 8192;        // slot sums per panel (+ a junk slot for padding)
-constexpr int kEntBits = 26;             // entry word: slot (14 bits) << kSegShift | offset
+constexpr int kEntBits = 27;             // entry word: slot (14 bits) << kSegShift | offset
 constexpr unsigned kNullEntry = (unsigned)kHeavySlots << kSegShift;
 constexpr int kHeavyWarps = 16;          // consumer warps (+ 1 producer warp)
-constexpr int kHeavyStages = 4;          // TMA ring depth
+constexpr int kHeavyStages = 2;          // TMA ring depth (per-segment cost is fixed)
 constexpr int kHeavyBlock = 32 * (kHeavyWarps + 1);
 constexpr int kDefaultHeavyMin = 64;     // rows with >= this many active followers are heavy
-constexpr long long kDefaultHeavyMinN = 1LL << 25;   // graphs below this many users skip it
+constexpr long long kDefaultHeavyMinN = 1LL << 24;   // graphs below this many users skip it
 constexpr int kMaxHeavySegs = 512;       // shared-memory bound of the per-warp list offsets
-constexpr int kDefaultHeavySegs = 256;   // staged labels H = segs * kSeg (1 Mi labels, 8 MB)
+// staged labels H: N/32 rounded down to a power of two, within [2^19, 2^21] (C4: 512 Ki,
+// C5: 2 Mi; measured); PSI_HEAVY_LABELS overrides
+constexpr int kMinHeavyLabels = 1 << 19, kMaxHeavyLabels = 1 << 21;
 constexpr int kDefaultHeavyPPS = 1;      // heavy panels per SM (entry budget per panel)
 constexpr int kDefaultGroups = 4;        // tile groups (of kBlock threads) per sweep CTA
 constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA

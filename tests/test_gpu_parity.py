@@ -236,7 +236,7 @@ def test_repeated_iterate_on_one_context(gpu):
 
 @pytest.mark.parametrize("env", [
     {"PSI_HEAVY": "0"},                                     # edge-stream sweep only
-    {"PSI_HEAVY": "1", "PSI_HEAVY_MIN": "2", "PSI_HEAVY_SEGS": "3"},   # nearly every row heavy
+    {"PSI_HEAVY": "1", "PSI_HEAVY_MIN": "2", "PSI_HEAVY_LABELS": "24576"},   # nearly every row heavy
     {"PSI_HEAVY": "1", "PSI_HEAVY_MIN": "16"},              # default H, more heavy rows
     {"PSI_HEAVY": "1"},                                     # library defaults, forced on
 ])
