@@ -40,9 +40,9 @@ constexpr int kHeavyBlock = 32 * (kHeavyWarps + 1);
 constexpr int kDefaultHeavyMin = 64;     // rows with >= this many active followers are heavy
 constexpr long long kDefaultHeavyMinN = 1LL << 24;   // graphs below this many users skip it
 constexpr int kMaxHeavySegs = 512;       // shared-memory bound of the per-warp list offsets
-// staged labels H: N/32 rounded down to a power of two, within [2^19, 2^21] (C4: 512 Ki,
-// C5: 2 Mi; measured); PSI_HEAVY_LABELS overrides
-constexpr int kMinHeavyLabels = 1 << 19, kMaxHeavyLabels = 1 << 21;
+// staged labels H: N/32 rounded down to a power of two, within [2^19, 2^20] (C4: 512 Ki,
+// C5: 1 Mi; measured); PSI_HEAVY_LABELS overrides
+constexpr int kMinHeavyLabels = 1 << 19, kMaxHeavyLabels = 1 << 20;
 constexpr int kDefaultHeavyPPS = 1;      // heavy panels per SM (entry budget per panel)
 constexpr int kDefaultGroups = 4;        // tile groups (of kBlock threads) per sweep CTA
 constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA
