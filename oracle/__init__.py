@@ -33,10 +33,12 @@ from .power_psi import power_psi, PowerPsiResult
 from .nsystems import psi_nsystems
 from .exact import psi_exact, dense_A_B
 from .pagerank import pagerank_power
+from .power_nf import power_nf, psi_power_nf, PowerNFResult
 from .metrics import relative_error, max_rel_error, top_k
 
 __all__ = [
     "build_operator", "leader_sets", "norm_of_B", "power_psi", "PowerPsiResult",
-    "psi_nsystems", "psi_exact", "dense_A_B", "pagerank_power",
+    "psi_nsystems", "psi_exact", "dense_A_B", "pagerank_power", "power_nf", "psi_power_nf",
+    "PowerNFResult",
     "relative_error", "max_rel_error", "top_k",
 ]

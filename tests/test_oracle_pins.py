@@ -324,3 +324,58 @@ def test_metrics_pins():
     assert oracle.relative_error([3.0, 4.0], [0.0, 0.0]) == 1.0      # ||x||/||x||
     assert oracle.max_rel_error([0.0, 2.0], [0.0, 2.2]) == pytest.approx(0.1)
     assert list(oracle.top_k([0.1, 0.3, 0.3, 0.2], 3)) == [1, 2, 3]  # ties by label
+
+
+# ------------------------------------------------------- Alg. 1 Power-NF
+
+@pytest.mark.parametrize("name", ["chain", "mutual"])
+def test_power_nf_spec_fixtures(name):
+    """SPEC S:290-292 worked examples: per-origin p_i, q_i of Alg. 1 + Eq. (7)."""
+    from oracle.power_nf import power_nf
+    case = _gold("spec_examples.json")[name]
+    rp, f, lam, mu = _graph(case)
+    r = power_nf(rp, f, lam, mu, origin=case["power_nf_origin"], eps=1e-15)
+    assert r.converged
+    np.testing.assert_allclose(r.p, case["p"], atol=1e-14)
+    np.testing.assert_allclose(r.q, case["q"], atol=1e-14)
+
+
+def test_power_nf_edgeless_and_first_iterate():
+    """b_i = 0 when nobody follows i: p = 0, q = d_i e_i; Alg. 1 line 1 (p <- b_i) with eps >= 1."""
+    from oracle.power_nf import power_nf
+    case = _gold("spec_examples.json")["edgeless"]
+    rp, f, lam, mu = _graph(case)
+    r = power_nf(rp, f, lam, mu, origin=2, eps=1e-12)
+    assert np.all(r.p == 0)
+    np.testing.assert_allclose(r.q, [0, 0, lam[2] / (lam[2] + mu[2])])
+    rng = np.random.default_rng(9)
+    rp, f, lam, mu = random_graph(rng, 20, 0.2)
+    A, B, c, d = oracle.dense_A_B(rp, f, lam, mu)
+    r = power_nf(rp, f, lam, mu, origin=3, eps=1.0)
+    assert r.iterations == 0 and np.array_equal(r.p, B[:, 3])
+    r = power_nf(rp, f, lam, mu, origin=3, eps=0.0, max_iters=2)   # p_2 = A(A b + b) + b
+    np.testing.assert_allclose(r.p, A @ (A @ B[:, 3] + B[:, 3]) + B[:, 3], rtol=1e-14)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_power_nf_converges_to_balance_equations(seed):
+    """Alg. 1's fixed point is the solution of Eqs. (4)-(5) and (2)-(3) built from the leader
+    sets (oracle.nsystems, independent of A, B); psi via N runs of Alg. 1 = Eq. (1) brute force
+    = Alg. 2 (P:209-259)."""
+    from oracle.power_nf import power_nf, psi_power_nf
+    rng = np.random.default_rng(2000 + seed)
+    n = int(rng.integers(8, 30))
+    rp, f, lam, mu = random_graph(rng, n, float(rng.uniform(0.08, 0.3)))
+    for i in (0, n // 2, n - 1):
+        p_ex, q_ex = newsfeed_wall(rp, f, lam, mu, i)
+        r = power_nf(rp, f, lam, mu, origin=i, eps=0.0, max_iters=3000)
+        np.testing.assert_allclose(r.p, p_ex, rtol=1e-11, atol=1e-15)
+        np.testing.assert_allclose(r.q, q_ex, rtol=1e-11, atol=1e-15)
+        # p_t = sum_{tau<=t} A^tau b_i is non-decreasing (A, b >= 0)
+        r2 = power_nf(rp, f, lam, mu, origin=i, eps=0.0, max_iters=5)
+        r3 = power_nf(rp, f, lam, mu, origin=i, eps=0.0, max_iters=6)
+        assert np.all(r3.p >= r2.p)
+    psi, Ts = psi_power_nf(rp, f, lam, mu, eps=1e-14)
+    np.testing.assert_allclose(psi, oracle.psi_nsystems(rp, f, lam, mu), rtol=1e-10, atol=1e-16)
+    np.testing.assert_allclose(psi, oracle.power_psi(rp, f, lam, mu, eps=1e-15).psi, rtol=1e-10,
+                               atol=1e-16)
