@@ -164,6 +164,36 @@ psi_status psi_pagerank(psi_ctx* ctx, double alpha, double eps, int64_t max_iter
  * host or device buffer of n doubles.  PSI_E_STATE if psi_pagerank has not succeeded. */
 psi_status psi_get_pagerank(const psi_ctx* ctx, double* out, int mem_kind);
 
+/*
+ * psi_power_nf -- Alg. 1 "Power-NF" for `k` origins:
+ * per origin i (caller labels), p_i <- b_i; p_i <- A p_i + b_i until ||p_i - p_old||_1 <= eps
+ * (gap_0 = 1, so eps >= 1 gives T = 0 and p_i = b_i) or T = max_iters; then the wall vector
+ * q_i = C p_i + d_i (Eq. (7)).  A, b_i, C, d_i as in P:171-175 (the column
+ * products: a pull over the leaders L(j)).  Runs batches of 32 origins on the GPU; each
+ * origin stops on its own test, exactly as Alg. 1.
+ *   origins   host int32[k], each in [0, n)
+ *   p_out     NULL or k x n doubles, origin-major (p_out[c*n + j] = p_{origins[c]}^(j))
+ *   q_out     NULL or k x n doubles, same layout, the wall shares q
+ *   mem_kind  whether p_out / q_out are host or device buffers (caller-owned)
+ *   iters_out NULL or host int64[k]: T of each origin
+ * Available for graphs with <= 2^27 edges (the N systems cost N x T x M work; the leader
+ * lists are kept only then), else PSI_E_STATE.  Returns PSI_OK, PSI_NOT_CONVERGED (some
+ * origin hit max_iters; outputs valid), PSI_E_INVALID_ARG, PSI_E_OOM, PSI_E_CUDA.
+ */
+psi_status psi_power_nf(psi_ctx* ctx, const int32_t* origins, int64_t k, double eps,
+                        int64_t max_iters, double* p_out, double* q_out, int mem_kind,
+                        int64_t* iters_out);
+
+/*
+ * psi_nsystems -- the psi-score by its original definition: Alg. 1 for every origin i, then
+ * psi_i = (1/N) sum_n q_i^(n) (Eq. (1); "applied N times") -- the paper's
+ * Power-NF baseline of Tables III-IV.  psi_out: n doubles (caller labels), host or device per
+ * mem_kind.  *matvecs_out (may be NULL) = sum over origins of T_i (the A-products).
+ * Same limits and return codes as psi_power_nf.
+ */
+psi_status psi_nsystems(psi_ctx* ctx, double eps, int64_t max_iters, double* psi_out,
+                        int mem_kind, int64_t* matvecs_out);
+
 /* psi_time_sweep -- measurement entry: runs `sweeps` sweeps of Eq. (14) from s_0 = c
  * (eps = 0) as direct stream launches and returns the average device time of each of the
  * sweep's kernels, bracketed by CUDA events on the context's stream: *heavy_ms = staged

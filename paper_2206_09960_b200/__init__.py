@@ -40,7 +40,7 @@ _STATUS_NAMES = {0: "PSI_OK", 1: "PSI_NOT_CONVERGED", -1: "PSI_E_INVALID_ARG", -
 
 EXPORTED = ["psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
             "psi_get_residual_history", "psi_time_sweep", "psi_get_info", "psi_pagerank",
-            "psi_get_pagerank", "psi_destroy", "psi_last_error"]
+            "psi_get_pagerank", "psi_power_nf", "psi_nsystems", "psi_destroy", "psi_last_error"]
 
 
 class PsiError(RuntimeError):
@@ -88,6 +88,8 @@ def load_library(build_if_stale: bool = True):
     lib.psi_get_series.argtypes = [vp, vp, ci]
     lib.psi_pagerank.argtypes = [vp, dbl, dbl, i64, ctypes.POINTER(i64), ctypes.POINTER(dbl)]
     lib.psi_get_pagerank.argtypes = [vp, vp, ci]
+    lib.psi_power_nf.argtypes = [vp, vp, i64, dbl, i64, vp, vp, ci, vp]
+    lib.psi_nsystems.argtypes = [vp, dbl, i64, vp, ci, ctypes.POINTER(i64)]
     lib.psi_get_residual_history.argtypes = [vp, vp, i64, ctypes.POINTER(i64)]
     lib.psi_get_info.argtypes = [vp, ctypes.POINTER(psi_info)]
     lib.psi_time_sweep.argtypes = [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl),
@@ -97,7 +99,7 @@ def load_library(build_if_stale: bool = True):
     lib.psi_last_error.restype = ctypes.c_char_p
     for f in ("psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
               "psi_get_residual_history", "psi_get_info", "psi_time_sweep", "psi_pagerank",
-              "psi_get_pagerank"):
+              "psi_get_pagerank", "psi_power_nf", "psi_nsystems"):
         getattr(lib, f).restype = ci
     _lib = lib
     return lib
@@ -193,6 +195,32 @@ class PsiGraph:
     def get_pagerank(self, out=None, device: bool = True):
         """pi[n] of the last pagerank() in the caller's original labels (torch.float64)."""
         return self._get(self._lib.psi_get_pagerank, out, device)
+
+    def power_nf(self, origins, eps: float = 1e-9, max_iters: int = 100_000):
+        """Alg. 1 for the given origins: returns (status, p, q, iters) with p, q torch.float64
+        (k, n) on the device (origin-major) and iters a numpy int64 array."""
+        import torch
+        org = np.ascontiguousarray(np.asarray(origins, dtype=np.int32).ravel())
+        k = org.size
+        p = torch.empty((k, self.n), dtype=torch.float64, device="cuda")
+        q = torch.empty((k, self.n), dtype=torch.float64, device="cuda")
+        iters = np.zeros(k, dtype=np.int64)
+        st = self._lib.psi_power_nf(self._ctx, org.ctypes.data, k, float(eps), int(max_iters),
+                                    p.data_ptr(), q.data_ptr(), PSI_MEM_DEVICE, iters.ctypes.data)
+        if st < 0:
+            raise PsiError(st, _err(self._lib))
+        return st, p, q, iters
+
+    def nsystems(self, eps: float = 1e-9, max_iters: int = 100_000):
+        """psi by Alg. 1 for every origin + Eq. (1): returns (status, psi on device, matvecs)."""
+        import torch
+        out = torch.empty(self.n, dtype=torch.float64, device="cuda")
+        mv = ctypes.c_int64()
+        st = self._lib.psi_nsystems(self._ctx, float(eps), int(max_iters), out.data_ptr(),
+                                    PSI_MEM_DEVICE, ctypes.byref(mv))
+        if st < 0:
+            raise PsiError(st, _err(self._lib))
+        return st, out, mv.value
 
     def get_residual_history(self) -> np.ndarray:
         n = ctypes.c_int64()

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libpsi.so")
-SOURCES = ["psi_api.cu", "psi_ingest.cu", "psi_sweep.cu", "psi_heavy.cu", "psi_pagerank.cu"]
+SOURCES = ["psi_api.cu", "psi_ingest.cu", "psi_sweep.cu", "psi_heavy.cu", "psi_pagerank.cu", "psi_powernf.cu"]
 DEPS = SOURCES + ["psi_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 using namespace psi;
 
@@ -95,7 +96,9 @@ void free_ctx(psi_ctx* c) {
   if (c->pr_exec) cudaGraphExecDestroy(c->pr_exec);
   if (c->pr_graph) cudaGraphDestroy(c->pr_graph);
   for (void* p : {(void*)c->pr.a, (void*)c->pr.a_first, (void*)c->pr.g, (void*)c->pr.dt,
-                  (void*)c->pr.x0, (void*)c->pr.pi, (void*)c->g.nlead, (void*)c->g.kinv})
+                  (void*)c->pr.x0, (void*)c->pr.pi, (void*)c->g.nlead, (void*)c->g.kinv,
+                  (void*)c->g.nf_loff, (void*)c->g.nf_leaders, (void*)c->g.nf_wt,
+                  (void*)c->g.nf_lm})
     if (p) cudaFree(p);
   void* ptrs[] = {c->g.edges, c->g.tile_row, c->g.a0, c->g.a1, c->g.g, c->g.wt, c->g.d1,
                   c->g.lam, c->g.psi, c->g.old_of_new, c->g.split, c->x[0], c->x[1],
@@ -690,6 +693,179 @@ psi_status psi_get_pagerank(const psi_ctx* c, double* out, int mem_kind) {
     return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
   if (!c->have_pr) return fail(PSI_E_STATE, "no successful psi_pagerank on this context");
   return copy_out(c, c->pr.pi, nullptr, out, mem_kind);
+}
+
+}  // extern "C"
+
+namespace {
+
+// Run Alg. 1 for `k` origins in batches of kNfK; psi_dev (k entries) and/or the origin-major
+// p/q columns (device pointers) are filled; iters (host, k) receives each origin's T.
+psi_status power_nf_run(psi_ctx* c, const int32_t* origins, long long k, double eps,
+                        long long max_iters, double* psi_dev, double* p_dev, double* q_dev,
+                        long long* iters, bool* all_converged, long long* sweeps_total) {
+  if (!c->g.nf_loff)
+    return fail(PSI_E_STATE, "Power-NF keeps the leader lists only for graphs with <= %lld edges "
+                             "(N systems cost N x T x M work)", kPowerNfMaxEdges);
+  const long long n = c->n;
+  NfWork w;
+  NfArgs a{};
+  int* d_origin = nullptr;
+  unsigned char* d_frozen = nullptr;
+  long long* d_iters = nullptr;
+  double* d_gap = nullptr;
+  psi_status rc = PSI_OK;
+  auto cleanup = [&]() {
+    for (void* p : {(void*)w.P[0], (void*)w.P[1], (void*)w.part, (void*)w.active, (void*)d_origin,
+                    (void*)d_frozen, (void*)d_iters, (void*)d_gap})
+      if (p) cudaFree(p);
+    if (w.h_active) cudaFreeHost(w.h_active);
+  };
+#define NF_CK(call)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      rc = fail(e_ == cudaErrorMemoryAllocation ? PSI_E_OOM : PSI_E_CUDA, "%s: %s", #call, \
+                cudaGetErrorString(e_));                                                   \
+      cleanup();                                                                           \
+      return rc;                                                                           \
+    }                                                                                      \
+  } while (0)
+  NF_CK(cudaMalloc(&w.P[0], (size_t)n * kNfK * sizeof(double)));
+  NF_CK(cudaMalloc(&w.P[1], (size_t)n * kNfK * sizeof(double)));
+  NF_CK(cudaMalloc(&w.part, power_nf_part_elems(n) * sizeof(double)));
+  NF_CK(cudaMalloc(&w.active, sizeof(unsigned)));
+  NF_CK(cudaHostAlloc(&w.h_active, sizeof(unsigned), cudaHostAllocDefault));
+  NF_CK(cudaMalloc(&d_origin, kNfK * sizeof(int)));
+  NF_CK(cudaMalloc(&d_frozen, kNfK));
+  NF_CK(cudaMalloc(&d_iters, kNfK * sizeof(long long)));
+  NF_CK(cudaMalloc(&d_gap, kNfK * sizeof(double)));
+  a.n = n;
+  a.loff = c->g.nf_loff;
+  a.leaders = c->g.nf_leaders;
+  a.lm = c->g.nf_lm;
+  a.wt = c->g.nf_wt;
+  a.origin = d_origin;
+  a.frozen = d_frozen;
+  a.iters = d_iters;
+  a.gap = d_gap;
+  *all_converged = true;
+  long long sweeps = 0;
+  for (long long b0 = 0; b0 < k; b0 += kNfK) {
+    const int kb = (int)std::min<long long>(kNfK, k - b0);
+    int h_origin[kNfK];
+    unsigned char h_frozen[kNfK];
+    for (int j = 0; j < kNfK; ++j) {
+      h_origin[j] = j < kb ? origins[b0 + j] : -1;
+      h_frozen[j] = j < kb ? 0 : 1;
+    }
+    NF_CK(cudaMemcpyAsync(d_origin, h_origin, sizeof(h_origin), cudaMemcpyHostToDevice, c->stream));
+    NF_CK(cudaMemcpyAsync(d_frozen, h_frozen, sizeof(h_frozen), cudaMemcpyHostToDevice, c->stream));
+    int cur = 0;
+    long long sw = 0;
+    NF_CK(power_nf_batch(a, w, eps, max_iters, psi_dev ? psi_dev + b0 : nullptr, c->stream, &cur, &sw));
+    if (p_dev || q_dev)
+      NF_CK(power_nf_columns(a, w, cur, kb, p_dev ? p_dev + b0 * n : nullptr,
+                             q_dev ? q_dev + b0 * n : nullptr, c->stream));
+    long long h_iters[kNfK];
+    double h_gap[kNfK];
+    NF_CK(cudaMemcpyAsync(h_iters, d_iters, sizeof(h_iters), cudaMemcpyDeviceToHost, c->stream));
+    NF_CK(cudaMemcpyAsync(h_gap, d_gap, sizeof(h_gap), cudaMemcpyDeviceToHost, c->stream));
+    NF_CK(cudaStreamSynchronize(c->stream));
+    for (int j = 0; j < kb; ++j) {
+      if (iters) iters[b0 + j] = h_iters[j];
+      sweeps += h_iters[j];
+      if (h_iters[j] >= max_iters && h_iters[j] > 0 && h_gap[j] > eps) *all_converged = false;
+    }
+  }
+#undef NF_CK
+  cleanup();
+  if (sweeps_total) *sweeps_total = sweeps;
+  return PSI_OK;
+}
+
+psi_status check_nf_args(const psi_ctx* c, double eps, int64_t max_iters) {
+  if (!c) return fail(PSI_E_INVALID_ARG, "ctx is NULL");
+  if (!(eps >= 0.0)) return fail(PSI_E_INVALID_ARG, "eps must be >= 0 (got %g)", eps);
+  if (max_iters < 0) return fail(PSI_E_INVALID_ARG, "max_iters must be >= 0");
+  return PSI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+psi_status psi_power_nf(psi_ctx* c, const int32_t* origins, int64_t k, double eps,
+                        int64_t max_iters, double* p_out, double* q_out, int mem_kind,
+                        int64_t* iters_out) {
+  g_err.clear();
+  psi_status st = check_nf_args(c, eps, max_iters);
+  if (st != PSI_OK) return st;
+  if (k < 1 || !origins) return fail(PSI_E_INVALID_ARG, "need k >= 1 origins");
+  if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
+    return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
+  for (int64_t j = 0; j < k; ++j)
+    if (origins[j] < 0 || origins[j] >= c->n)
+      return fail(PSI_E_INVALID_ARG, "origin %d outside [0, n)", origins[j]);
+  const size_t bytes = (size_t)k * c->n * sizeof(double);
+  double *p_dev = p_out, *q_dev = q_out;
+  if (mem_kind == PSI_MEM_HOST) {
+    p_dev = q_dev = nullptr;
+    if (p_out) API_CK(cudaMalloc(&p_dev, bytes));
+    if (q_out && cudaMalloc(&q_dev, bytes) != cudaSuccess) {
+      if (p_dev) cudaFree(p_dev);
+      return fail(PSI_E_OOM, "cudaMalloc of the q columns failed");
+    }
+  }
+  std::vector<long long> iters(k);
+  bool conv = true;
+  st = power_nf_run(c, origins, k, eps, max_iters, nullptr, p_dev, q_dev, iters.data(), &conv,
+                    nullptr);
+  if (st == PSI_OK && mem_kind == PSI_MEM_HOST) {
+    if (p_out && cudaMemcpyAsync(p_out, p_dev, bytes, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      st = fail(PSI_E_CUDA, "copy of p failed");
+    if (q_out && cudaMemcpyAsync(q_out, q_dev, bytes, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+      st = fail(PSI_E_CUDA, "copy of q failed");
+    cudaStreamSynchronize(c->stream);
+  }
+  if (mem_kind == PSI_MEM_HOST) {
+    if (p_dev) cudaFree(p_dev);
+    if (q_dev) cudaFree(q_dev);
+  }
+  if (st != PSI_OK) return st;
+  if (iters_out)
+    for (int64_t j = 0; j < k; ++j) iters_out[j] = iters[j];
+  if (!conv) return fail(PSI_NOT_CONVERGED, "some origin reached max_iters with gap > eps");
+  return PSI_OK;
+}
+
+psi_status psi_nsystems(psi_ctx* c, double eps, int64_t max_iters, double* psi_out, int mem_kind,
+                        int64_t* matvecs_out) {
+  g_err.clear();
+  psi_status st = check_nf_args(c, eps, max_iters);
+  if (st != PSI_OK) return st;
+  if (!psi_out) return fail(PSI_E_INVALID_ARG, "psi_out is NULL");
+  if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
+    return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
+  const long long n = c->n;
+  double* psi_dev = psi_out;
+  if (mem_kind == PSI_MEM_HOST) API_CK(cudaMalloc(&psi_dev, (size_t)n * sizeof(double)));
+  std::vector<int32_t> all(n);
+  for (long long i = 0; i < n; ++i) all[i] = (int32_t)i;
+  bool conv = true;
+  long long sweeps = 0;
+  st = power_nf_run(c, all.data(), n, eps, max_iters, psi_dev, nullptr, nullptr, nullptr, &conv,
+                    &sweeps);
+  if (st == PSI_OK && mem_kind == PSI_MEM_HOST &&
+      (cudaMemcpyAsync(psi_out, psi_dev, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream) != cudaSuccess ||
+       cudaStreamSynchronize(c->stream) != cudaSuccess))
+    st = fail(PSI_E_CUDA, "copy of psi failed");
+  if (mem_kind == PSI_MEM_HOST) cudaFree(psi_dev);
+  if (st != PSI_OK) return st;
+  if (matvecs_out) *matvecs_out = sweeps;
+  if (!conv) return fail(PSI_NOT_CONVERGED, "some origin reached max_iters with gap > eps");
+  return PSI_OK;
 }
 
 void psi_destroy(psi_ctx* c) { free_ctx(c); }

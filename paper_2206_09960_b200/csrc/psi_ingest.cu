@@ -905,6 +905,16 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
         loff.as<int>(), vals.Current(), lm.as<double2>(), N, a_old.as<double>(), g_old.as<double>(),
         wt_old.as<double>(), d_old.as<double>(), first_leader.as<int>(), kmax, cnt);
     long long nlong = long_segments(loff.as<int>(), nullptr, N, kShort, s, longu);
+    if (m <= kPowerNfMaxEdges) {       // keep the leader lists for Power-NF (psi_powernf.cu)
+      IG_CK(cudaMalloc(&out.nf_loff, (size_t)(n + 1) * sizeof(int)));
+      IG_CK(cudaMalloc(&out.nf_leaders, (size_t)std::max<long long>(m, 1) * sizeof(int)));
+      IG_CK(cudaMalloc(&out.nf_lm, (size_t)n * sizeof(double2)));
+      IG_CK(cudaMemcpyAsync(out.nf_loff, loff.p, (size_t)(n + 1) * sizeof(int), cudaMemcpyDeviceToDevice, s));
+      if (m > 0)
+        IG_CK(cudaMemcpyAsync(out.nf_leaders, vals.Current(), (size_t)m * sizeof(int),
+                              cudaMemcpyDeviceToDevice, s));
+      IG_CK(cudaMemcpyAsync(out.nf_lm, lm.p, (size_t)n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    }
     if (nlong < 0) IG_CK(cudaErrorMemoryAllocation);
     if (nlong > 0)
       k_norm_long<<<grid_for(nlong * 32, 256), 256, 0, s>>>(
@@ -919,6 +929,10 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
                                                                  idx_in, wt_old.as<double>(), lam, kmax);
   }
 
+  if (out.nf_loff) {
+    IG_CK(cudaMalloc(&out.nf_wt, (size_t)n * sizeof(double)));
+    IG_CK(cudaMemcpyAsync(out.nf_wt, wt_old.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
   tr.mark("transpose+normalisers");
   // ---- 5. relabel
   Tmp cls, new_of_old, key, sel, flag8, nsel, stage_tmp, sort_tmp2, sorted;

@@ -149,6 +149,11 @@ struct IngestOut {
   int* old_of_new = nullptr;  // [n]
   int* nlead = nullptr;       // [n]     #leaders |L(j)| (PageRank out-degree), new labels
   double* kinv = nullptr;     // [n_act] sum over follower-less followers n of 1/max(|L(n)|, 1)
+  // Power-NF (caller labels; kept when m <= kPowerNfMaxEdges, else nf_loff == nullptr)
+  int* nf_loff = nullptr;
+  int* nf_leaders = nullptr;
+  double* nf_wt = nullptr;
+  double2* nf_lm = nullptr;
   int ntiles = 0;
   int4* split = nullptr;
   int nsplit = 0;
@@ -167,6 +172,32 @@ struct IngestOut {
   long long n_f = 0, n_g = 0, n_leaderless = 0;
   int relabeled = 0;
 };
+
+// ---- Power-NF (psi_powernf.cu): Alg. 1 for a batch of kNfK origins, caller labels
+constexpr int kNfK = 32;                         // origins per batch (one lane each)
+constexpr long long kPowerNfMaxEdges = 1LL << 27;  // graphs up to this size keep L(j) for it
+struct NfArgs {
+  long long n;
+  const int* loff;       // [n+1] leaders of user j: leaders[loff[j] .. loff[j+1])
+  const int* leaders;    // [m]   ascending per user
+  const double2* lm;     // [n]   (lambda, mu)
+  const double* wt;      // [n]   Wt = W, or 1 if leaderless
+  const int* origin;     // [kNfK] origin of each column, -1 = unused
+  unsigned char* frozen; // [kNfK] column stopped (Alg. 1 loop left)
+  long long* iters;      // [kNfK] T of each column
+  double* gap;           // [kNfK] last ||p - p_old||_1
+};
+struct NfWork {
+  double* P[2] = {nullptr, nullptr};  // [n * kNfK] row-major ping-pong
+  double* part = nullptr;             // per-CTA column partials
+  unsigned* active = nullptr;         // device: columns still iterating
+  unsigned* h_active = nullptr;       // pinned host copy
+};
+cudaError_t power_nf_batch(const NfArgs& a, NfWork& w, double eps, long long max_iters,
+                           double* psi_dev, cudaStream_t s, int* cur_out, long long* sweeps);
+cudaError_t power_nf_columns(const NfArgs& a, const NfWork& w, int cur, int k, double* p_out,
+                             double* q_out, cudaStream_t s);
+size_t power_nf_part_elems(long long n);
 
 // ---- PageRank (psi_pagerank.cu): constants of Eq. (22) in the sweep's kernel state
 struct PrBuffers {
