@@ -99,13 +99,13 @@ void free_ctx(psi_ctx* c) {
                   (void*)c->pr.x0, (void*)c->pr.pi, (void*)c->g.nlead, (void*)c->g.kinv,
                   (void*)c->g.nf_loff, (void*)c->g.nf_leaders, (void*)c->g.nf_wt,
                   (void*)c->g.nf_lm})
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, c->stream);
   void* ptrs[] = {c->g.edges, c->g.tile_row, c->g.a0, c->g.a1, c->g.g, c->g.wt, c->g.d1,
                   c->g.lam, c->g.psi, c->g.old_of_new, c->g.split, c->x[0], c->x[1],
                   c->p_in, c->p_out, c->eps_part1, c->eps_part2, c->history, c->st, c->prm,
                   c->hhot, c->g.h_ent, c->g.h_loff, c->g.h_prow, c->g.h_rslot, c->g.h_wslot};
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, c->stream);
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_prm) cudaFreeHost(c->h_prm);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -275,12 +275,12 @@ psi_status ensure_history(psi_ctx* c, long long need) {
   if (need < 1) need = 1;
   if (c->history && c->hist_cap >= need) return PSI_OK;
   if (c->history) {
-    cudaFree(c->history);
+    cudaFreeAsync(c->history, c->stream);
     c->device_bytes -= c->hist_cap * sizeof(double);
     c->history = nullptr;
   }
   long long cap = need < 1024 ? 1024 : need;
-  API_CK(cudaMalloc(&c->history, cap * sizeof(double)));
+  API_CK(cudaMallocAsync(&c->history, cap * sizeof(double), c->stream));
   c->hist_cap = cap;
   c->device_bytes += cap * sizeof(double);
   return PSI_OK;
@@ -340,6 +340,18 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
     return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
 
+  {
+    // every device buffer is stream-ordered (cudaMallocAsync from the device's default pool);
+    // the pool keeps freed memory reserved (release threshold: unlimited) so build / destroy
+    // cycles reuse it instead of re-mapping it.  PSI_POOL_KEEP_GB caps what stays reserved.
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      unsigned long long keep = ~0ull;
+      if (const char* e = getenv("PSI_POOL_KEEP_GB")) keep = (unsigned long long)atoll(e) << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   psi_ctx* c = new psi_ctx;
   c->n = n;
   c->m = m;
@@ -363,12 +375,16 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   const double* lam_d = lambda;
   const double* mu_d = mu;
   void* staged[4] = {nullptr, nullptr, nullptr, nullptr};
-  struct Free4 { void** p; ~Free4() { for (int i = 0; i < 4; ++i) if (p[i]) cudaFree(p[i]); } } f4{staged};
+  struct Free4 {
+    void** p;
+    cudaStream_t s;
+    ~Free4() { for (int i = 0; i < 4; ++i) if (p[i]) cudaFreeAsync(p[i], s); }
+  } f4{staged, c->stream};
   if (mem_kind == PSI_MEM_HOST) {
-    B_CK(cudaMalloc(&staged[0], (n + 1) * sizeof(long long)));
-    B_CK(cudaMalloc(&staged[1], (m > 0 ? m : 1) * sizeof(int)));
-    B_CK(cudaMalloc(&staged[2], n * sizeof(double)));
-    B_CK(cudaMalloc(&staged[3], n * sizeof(double)));
+    B_CK(cudaMallocAsync(&staged[0], (n + 1) * sizeof(long long), c->stream));
+    B_CK(cudaMallocAsync(&staged[1], (m > 0 ? m : 1) * sizeof(int), c->stream));
+    B_CK(cudaMallocAsync(&staged[2], n * sizeof(double), c->stream));
+    B_CK(cudaMallocAsync(&staged[3], n * sizeof(double), c->stream));
     B_CK(cudaMemcpyAsync(staged[0], row_ptr, (n + 1) * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
     if (m > 0)
       B_CK(cudaMemcpyAsync(staged[1], followers, m * sizeof(int), cudaMemcpyHostToDevice, c->stream));
@@ -411,19 +427,19 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
     c->heavy_smem = heavy_smem_bytes(c->g.nseg);
     B_CK(cudaFuncSetAttribute(heavy_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)c->heavy_smem));
-    B_CK(cudaMalloc(&c->hhot, (size_t)c->g.n_heavy * sizeof(double)));
+    B_CK(cudaMallocAsync(&c->hhot, (size_t)c->g.n_heavy * sizeof(double), c->stream));
     B_CK(cudaMemsetAsync(c->hhot, 0, (size_t)c->g.n_heavy * sizeof(double), c->stream));
   }
-  B_CK(cudaMalloc(&c->x[0], (n + 1) * sizeof(double)));      // + sentinel x[n] = 0
-  B_CK(cudaMalloc(&c->x[1], (n + 1) * sizeof(double)));
+  B_CK(cudaMallocAsync(&c->x[0], (n + 1) * sizeof(double), c->stream));      // + sentinel x[n] = 0
+  B_CK(cudaMallocAsync(&c->x[1], (n + 1) * sizeof(double), c->stream));
   B_CK(cudaMemsetAsync(c->x[0] + n, 0, sizeof(double), c->stream));
   B_CK(cudaMemsetAsync(c->x[1] + n, 0, sizeof(double), c->stream));
-  B_CK(cudaMalloc(&c->p_in, (c->g.ntiles + 1) * sizeof(double)));
-  B_CK(cudaMalloc(&c->p_out, (c->g.ntiles + 1) * sizeof(double)));
-  B_CK(cudaMalloc(&c->eps_part1, c->grid1 * sizeof(double)));
-  B_CK(cudaMalloc(&c->eps_part2, c->grid2 * sizeof(double)));
-  B_CK(cudaMalloc(&c->st, sizeof(LoopState)));
-  B_CK(cudaMalloc(&c->prm, sizeof(LoopParams)));
+  B_CK(cudaMallocAsync(&c->p_in, (c->g.ntiles + 1) * sizeof(double), c->stream));
+  B_CK(cudaMallocAsync(&c->p_out, (c->g.ntiles + 1) * sizeof(double), c->stream));
+  B_CK(cudaMallocAsync(&c->eps_part1, c->grid1 * sizeof(double), c->stream));
+  B_CK(cudaMallocAsync(&c->eps_part2, c->grid2 * sizeof(double), c->stream));
+  B_CK(cudaMallocAsync(&c->st, sizeof(LoopState), c->stream));
+  B_CK(cudaMallocAsync(&c->prm, sizeof(LoopParams), c->stream));
   B_CK(cudaMemsetAsync(c->st, 0, sizeof(LoopState), c->stream));
   // Follower-less users keep x = a0 in both buffers for ever (they are never written).
   B_CK(cudaMemcpyAsync(c->x[0], c->g.a0, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -628,12 +644,12 @@ psi_status psi_pagerank(psi_ctx* c, double alpha, double eps, int64_t max_iters,
   if (max_iters < 0) return fail(PSI_E_INVALID_ARG, "max_iters must be >= 0");
   const long long n = c->n, na = std::max<long long>(c->g.n_act, 1);
   if (!c->pr.a) {
-    API_CK(cudaMalloc(&c->pr.a, na * sizeof(double)));
-    API_CK(cudaMalloc(&c->pr.a_first, na * sizeof(double)));
-    API_CK(cudaMalloc(&c->pr.g, na * sizeof(double)));
-    API_CK(cudaMalloc(&c->pr.dt, n * sizeof(double)));
-    API_CK(cudaMalloc(&c->pr.x0, n * sizeof(double)));
-    API_CK(cudaMalloc(&c->pr.pi, n * sizeof(double)));
+    API_CK(cudaMallocAsync(&c->pr.a, na * sizeof(double), c->stream));
+    API_CK(cudaMallocAsync(&c->pr.a_first, na * sizeof(double), c->stream));
+    API_CK(cudaMallocAsync(&c->pr.g, na * sizeof(double), c->stream));
+    API_CK(cudaMallocAsync(&c->pr.dt, n * sizeof(double), c->stream));
+    API_CK(cudaMallocAsync(&c->pr.x0, n * sizeof(double), c->stream));
+    API_CK(cudaMallocAsync(&c->pr.pi, n * sizeof(double), c->stream));
     c->device_bytes += (3 * na + 3 * n) * sizeof(double);
   }
   c->have_pr = false;
@@ -718,7 +734,7 @@ psi_status power_nf_run(psi_ctx* c, const int32_t* origins, long long k, double 
   auto cleanup = [&]() {
     for (void* p : {(void*)w.P[0], (void*)w.P[1], (void*)w.part, (void*)w.active, (void*)d_origin,
                     (void*)d_frozen, (void*)d_iters, (void*)d_gap})
-      if (p) cudaFree(p);
+      if (p) cudaFreeAsync(p, c->stream);
     if (w.h_active) cudaFreeHost(w.h_active);
   };
 #define NF_CK(call)                                                                        \
@@ -731,15 +747,15 @@ psi_status power_nf_run(psi_ctx* c, const int32_t* origins, long long k, double 
       return rc;                                                                           \
     }                                                                                      \
   } while (0)
-  NF_CK(cudaMalloc(&w.P[0], (size_t)n * kNfK * sizeof(double)));
-  NF_CK(cudaMalloc(&w.P[1], (size_t)n * kNfK * sizeof(double)));
-  NF_CK(cudaMalloc(&w.part, power_nf_part_elems(n) * sizeof(double)));
-  NF_CK(cudaMalloc(&w.active, sizeof(unsigned)));
+  NF_CK(cudaMallocAsync(&w.P[0], (size_t)n * kNfK * sizeof(double), c->stream));
+  NF_CK(cudaMallocAsync(&w.P[1], (size_t)n * kNfK * sizeof(double), c->stream));
+  NF_CK(cudaMallocAsync(&w.part, power_nf_part_elems(n) * sizeof(double), c->stream));
+  NF_CK(cudaMallocAsync(&w.active, sizeof(unsigned), c->stream));
   NF_CK(cudaHostAlloc(&w.h_active, sizeof(unsigned), cudaHostAllocDefault));
-  NF_CK(cudaMalloc(&d_origin, kNfK * sizeof(int)));
-  NF_CK(cudaMalloc(&d_frozen, kNfK));
-  NF_CK(cudaMalloc(&d_iters, kNfK * sizeof(long long)));
-  NF_CK(cudaMalloc(&d_gap, kNfK * sizeof(double)));
+  NF_CK(cudaMallocAsync(&d_origin, kNfK * sizeof(int), c->stream));
+  NF_CK(cudaMallocAsync(&d_frozen, kNfK, c->stream));
+  NF_CK(cudaMallocAsync(&d_iters, kNfK * sizeof(long long), c->stream));
+  NF_CK(cudaMallocAsync(&d_gap, kNfK * sizeof(double), c->stream));
   a.n = n;
   a.loff = c->g.nf_loff;
   a.leaders = c->g.nf_leaders;
@@ -811,9 +827,9 @@ psi_status psi_power_nf(psi_ctx* c, const int32_t* origins, int64_t k, double ep
   double *p_dev = p_out, *q_dev = q_out;
   if (mem_kind == PSI_MEM_HOST) {
     p_dev = q_dev = nullptr;
-    if (p_out) API_CK(cudaMalloc(&p_dev, bytes));
-    if (q_out && cudaMalloc(&q_dev, bytes) != cudaSuccess) {
-      if (p_dev) cudaFree(p_dev);
+    if (p_out) API_CK(cudaMallocAsync(&p_dev, bytes, c->stream));
+    if (q_out && cudaMallocAsync(&q_dev, bytes, c->stream) != cudaSuccess) {
+      if (p_dev) cudaFreeAsync(p_dev, c->stream);
       return fail(PSI_E_OOM, "cudaMalloc of the q columns failed");
     }
   }
@@ -829,8 +845,8 @@ psi_status psi_power_nf(psi_ctx* c, const int32_t* origins, int64_t k, double ep
     cudaStreamSynchronize(c->stream);
   }
   if (mem_kind == PSI_MEM_HOST) {
-    if (p_dev) cudaFree(p_dev);
-    if (q_dev) cudaFree(q_dev);
+    if (p_dev) cudaFreeAsync(p_dev, c->stream);
+    if (q_dev) cudaFreeAsync(q_dev, c->stream);
   }
   if (st != PSI_OK) return st;
   if (iters_out)
@@ -849,7 +865,7 @@ psi_status psi_nsystems(psi_ctx* c, double eps, int64_t max_iters, double* psi_o
     return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
   const long long n = c->n;
   double* psi_dev = psi_out;
-  if (mem_kind == PSI_MEM_HOST) API_CK(cudaMalloc(&psi_dev, (size_t)n * sizeof(double)));
+  if (mem_kind == PSI_MEM_HOST) API_CK(cudaMallocAsync(&psi_dev, (size_t)n * sizeof(double), c->stream));
   std::vector<int32_t> all(n);
   for (long long i = 0; i < n; ++i) all[i] = (int32_t)i;
   bool conv = true;
@@ -861,7 +877,7 @@ psi_status psi_nsystems(psi_ctx* c, double eps, int64_t max_iters, double* psi_o
                        c->stream) != cudaSuccess ||
        cudaStreamSynchronize(c->stream) != cudaSuccess))
     st = fail(PSI_E_CUDA, "copy of psi failed");
-  if (mem_kind == PSI_MEM_HOST) cudaFree(psi_dev);
+  if (mem_kind == PSI_MEM_HOST) cudaFreeAsync(psi_dev, c->stream);
   if (st != PSI_OK) return st;
   if (matvecs_out) *matvecs_out = sweeps;
   if (!conv) return fail(PSI_NOT_CONVERGED, "some origin reached max_iters with gap > eps");

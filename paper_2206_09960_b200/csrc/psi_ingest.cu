@@ -748,15 +748,15 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   out.npanels = npanels;
   out.heavy_entries = n_ent;
 
-  IG_CK(cudaMalloc(&out.h_prow, prow.size() * sizeof(int)));
-  IG_CK(cudaMalloc(&out.h_rslot, (size_t)NH * sizeof(int2)));
-  IG_CK(cudaMalloc(&out.h_wslot, wslot.size() * sizeof(int)));
+  IG_CK(cudaMallocAsync(&out.h_prow, prow.size() * sizeof(int), s));
+  IG_CK(cudaMallocAsync(&out.h_rslot, (size_t)NH * sizeof(int2), s));
+  IG_CK(cudaMallocAsync(&out.h_wslot, wslot.size() * sizeof(int), s));
   IG_CK(cudaMemcpyAsync(out.h_prow, prow.data(), prow.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   IG_CK(cudaMemcpyAsync(out.h_rslot, rslot.data(), (size_t)NH * sizeof(int2), cudaMemcpyHostToDevice, s));
   IG_CK(cudaMemcpyAsync(out.h_wslot, wslot.data(), wslot.size() * sizeof(int), cudaMemcpyHostToDevice, s));
 
   const long long nlists = (long long)npanels * nseg * kHeavyWarps;
-  IG_CK(cudaMalloc(&out.h_loff, (size_t)(nlists + 1) * sizeof(long long)));
+  IG_CK(cudaMallocAsync(&out.h_loff, (size_t)(nlists + 1) * sizeof(long long), s));
   Tmp keys, keys2, rpan, psb, sw, lstart, plen, scan_tmp, sort_tmp;
   IG_CK(keys.alloc((size_t)std::max<long long>(n_ent, 1) * 8));
   IG_CK(keys2.alloc((size_t)std::max<long long>(n_ent, 1) * 8));
@@ -793,7 +793,7 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   long long total = 0;
   IG_CK(cudaMemcpyAsync(&total, out.h_loff + nlists, sizeof(long long), cudaMemcpyDeviceToHost, s));
   IG_CK(cudaStreamSynchronize(s));
-  IG_CK(cudaMalloc(&out.h_ent, (size_t)std::max<long long>(total, 4) * sizeof(unsigned)));
+  IG_CK(cudaMallocAsync(&out.h_ent, (size_t)std::max<long long>(total, 4) * sizeof(unsigned), s));
   k_fill_u32<<<grid_for(total, 256), 256, 0, s>>>(out.h_ent, total, kNullEntry);
   k_heavy_fill<<<grid_for(n_ent, 256), 256, 0, s>>>(kb.Current(), n_ent, lstart.as<long long>(),
                                                    out.h_loff, out.h_ent);
@@ -906,9 +906,9 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
         wt_old.as<double>(), d_old.as<double>(), first_leader.as<int>(), kmax, cnt);
     long long nlong = long_segments(loff.as<int>(), nullptr, N, kShort, s, longu);
     if (m <= kPowerNfMaxEdges) {       // keep the leader lists for Power-NF (psi_powernf.cu)
-      IG_CK(cudaMalloc(&out.nf_loff, (size_t)(n + 1) * sizeof(int)));
-      IG_CK(cudaMalloc(&out.nf_leaders, (size_t)std::max<long long>(m, 1) * sizeof(int)));
-      IG_CK(cudaMalloc(&out.nf_lm, (size_t)n * sizeof(double2)));
+      IG_CK(cudaMallocAsync(&out.nf_loff, (size_t)(n + 1) * sizeof(int), s));
+      IG_CK(cudaMallocAsync(&out.nf_leaders, (size_t)std::max<long long>(m, 1) * sizeof(int), s));
+      IG_CK(cudaMallocAsync(&out.nf_lm, (size_t)n * sizeof(double2), s));
       IG_CK(cudaMemcpyAsync(out.nf_loff, loff.p, (size_t)(n + 1) * sizeof(int), cudaMemcpyDeviceToDevice, s));
       if (m > 0)
         IG_CK(cudaMemcpyAsync(out.nf_leaders, vals.Current(), (size_t)m * sizeof(int),
@@ -930,7 +930,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   }
 
   if (out.nf_loff) {
-    IG_CK(cudaMalloc(&out.nf_wt, (size_t)n * sizeof(double)));
+    IG_CK(cudaMallocAsync(&out.nf_wt, (size_t)n * sizeof(double), s));
     IG_CK(cudaMemcpyAsync(out.nf_wt, wt_old.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
   tr.mark("transpose+normalisers");
@@ -938,7 +938,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   Tmp cls, new_of_old, key, sel, flag8, nsel, stage_tmp, sort_tmp2, sorted;
   IG_CK(cls.alloc((size_t)n));
   IG_CK(new_of_old.alloc((size_t)n * sizeof(int)));
-  IG_CK(cudaMalloc(&out.old_of_new, (size_t)n * sizeof(int)));
+  IG_CK(cudaMallocAsync(&out.old_of_new, (size_t)n * sizeof(int), s));
   k_classify<<<grid_for(n, 256), 256, 0, s>>>(rp, nlead.as<int>(), N, cls.as<unsigned char>(),
                                               new_of_old.as<int>(), ccount);
   unsigned long long h[16];
@@ -1047,7 +1047,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   // ---- 6. relabelled edge stream over active rows, folded constants
   const int NA = (int)out.n_act;
   Tmp cntr, K, rp_new;
-  IG_CK(cudaMalloc(&out.kinv, (size_t)(NA > 0 ? NA : 1) * sizeof(double)));
+  IG_CK(cudaMallocAsync(&out.kinv, (size_t)(NA > 0 ? NA : 1) * sizeof(double), s));
   IG_CK(cntr.alloc((size_t)(NA + 1) * sizeof(int)));
   IG_CK(K.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(double)));
   IG_CK(rp_new.alloc((size_t)(NA + 1) * sizeof(int)));
@@ -1098,7 +1098,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   out.ntiles = (int)(((long long)m_act + kTile - 1) / kTile);
   const long long m_pad = (long long)out.ntiles * kTile;
   {
-    IG_CK(cudaMalloc(&out.edges, (size_t)(m_pad > 0 ? m_pad : 4) * sizeof(unsigned)));
+    IG_CK(cudaMallocAsync(&out.edges, (size_t)(m_pad > 0 ? m_pad : 4) * sizeof(unsigned), s));
     int* ed = (int*)out.edges;
     if (NA > 0) {
       RowFillArgs R{rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
@@ -1124,14 +1124,14 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
 
   tr.mark("heavy plan");
   const size_t na_b = (size_t)(NA > 0 ? NA : 1) * sizeof(double);
-  IG_CK(cudaMalloc(&out.a0, (size_t)n * sizeof(double)));
-  IG_CK(cudaMalloc(&out.wt, (size_t)n * sizeof(double)));
-  IG_CK(cudaMalloc(&out.psi, (size_t)n * sizeof(double)));
-  IG_CK(cudaMalloc(&out.a1, na_b));
-  IG_CK(cudaMalloc(&out.g, na_b));
-  IG_CK(cudaMalloc(&out.d1, na_b));
-  IG_CK(cudaMalloc(&out.lam, na_b));
-  IG_CK(cudaMalloc(&out.nlead, (size_t)n * sizeof(int)));
+  IG_CK(cudaMallocAsync(&out.a0, (size_t)n * sizeof(double), s));
+  IG_CK(cudaMallocAsync(&out.wt, (size_t)n * sizeof(double), s));
+  IG_CK(cudaMallocAsync(&out.psi, (size_t)n * sizeof(double), s));
+  IG_CK(cudaMallocAsync(&out.a1, na_b, s));
+  IG_CK(cudaMallocAsync(&out.g, na_b, s));
+  IG_CK(cudaMallocAsync(&out.d1, na_b, s));
+  IG_CK(cudaMallocAsync(&out.lam, na_b, s));
+  IG_CK(cudaMallocAsync(&out.nlead, (size_t)n * sizeof(int), s));
   k_permute_vectors<<<grid_for(n, 256), 256, 0, s>>>(
       out.old_of_new, N, NA, a_old.as<double>(), g_old.as<double>(), wt_old.as<double>(),
       d_old.as<double>(), lam, K.as<double>(), (double)n, nlead.as<int>(), out.a0, out.a1, out.g,
@@ -1140,7 +1140,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
 
   tr.mark("vectors");
   // ---- 7. edge tiles: first row of every tile, rows spanning tiles
-  IG_CK(cudaMalloc(&out.tile_row, (size_t)(out.ntiles + 1) * sizeof(int)));
+  IG_CK(cudaMallocAsync(&out.tile_row, (size_t)(out.ntiles + 1) * sizeof(int), s));
   k_tile_rows<<<grid_for(out.ntiles + 1, 256), 256, 0, s>>>(rp_new.as<int>(), NA, out.ntiles,
                                                             out.tile_row);
   {
@@ -1163,7 +1163,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
       IG_CK(cudaStreamSynchronize(s));
     }
     out.nsplit = (int)hs;
-    IG_CK(cudaMalloc(&out.split, (size_t)(hs > 0 ? hs : 1) * sizeof(int4)));
+    IG_CK(cudaMallocAsync(&out.split, (size_t)(hs > 0 ? hs : 1) * sizeof(int4), s));
     if (hs > 0)
       k_split_fill<<<grid_for(hs, 256), 256, 0, s>>>(rows.as<int>(), hs, rp_new.as<int>(),
                                                      out.split);
