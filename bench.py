@@ -206,6 +206,7 @@ def cpu_oracle_sample(w, target_edges=20_000_000, sweeps=3):
     t = statistics.median(times)
     edges = hi - lo
     return {"value": edges / t / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+            "ms_per_sweep": t * 1e3,
             "sample": f"oracle Alg.2 sweep (SciPy CSR fp64, 1 thread) on rows [0,{r1}) = {edges} "
                       f"edges of the same graph, median of {sweeps} sweeps, {t*1e3:.1f} ms/sweep",
             "cpu": _cpu_model(), "host_cpus": os.cpu_count()}
@@ -237,8 +238,10 @@ def run_reference(args, ws, rank):
     cb = dict(per_step[0])
     cb["value"] = val
     cb["sample"] = cb["sample"].replace("median of 1 sweeps", f"{args.steps} timed steps")
+    ms = statistics.median([r["ms_per_sweep"] for r in per_step])
     return {"metric": METRIC, "value": val, "unit": "GTEPS", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak",
             "impl": "reference", "dtype": "f64", "data": "synthetic",
             "config": _config_dict(args, w), "cpu_baseline": cb,
             "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
