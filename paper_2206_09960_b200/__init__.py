@@ -75,9 +75,10 @@ def load_library(build_if_stale: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
-    if build_if_stale and _build._stale():
-        _build.build()
+    checked = os.environ.get("PSI_LIB", "") == "checked"   # device bounds-checked build
+    path = _build.LIB_CHECKED if checked else _build.LIB
+    if build_if_stale and _build._stale(path):
+        _build.build(checked=checked)
     if not os.path.exists(path):
         raise RuntimeError(f"libpsi.so not found at {path}; run __graft_entry__.build()")
     lib = ctypes.CDLL(path)

@@ -97,6 +97,7 @@ __device__ __forceinline__ void process_chunk(const unsigned (&w)[8], const doub
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     sl[k] = w[k] >> kSegShift;
+    PSI_ASSERT(sl[k] <= (unsigned)kHeavySlots);
     acc[k] = seg[w[k] & (kSeg - 1)];
   }
   bool single = true;
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(kHeavyBlock, 1) k_heavy(SweepArgs A) {
     mbar_wait(full + q % kHeavyStages, (q / kHeavyStages) & 1u);      // segment 0 of panel k
     const int p = ring[k & 7];
     if (p < 0) break;
+    PSI_ASSERT(p < H.npanels);
     const int* ws = H.wslot + (size_t)p * (kHeavyWarps + 1);
     const int sl0 = ws[warp], sl1 = ws[warp + 1];
     for (int i = sl0 + lane; i < sl1; i += 32) rowsum[i] = 0.0;
@@ -256,6 +258,7 @@ __global__ void __launch_bounds__(kHeavyBlock, 1) k_heavy(SweepArgs A) {
     const int r0 = H.prow[p], r1 = H.prow[p + 1];
     for (int r = r0 + (int)threadIdx.x; r < r1; r += kHeavyWarps * 32) {
       const int2 sn = H.rslot[r];
+      PSI_ASSERT(r < A.n_heavy && sn.x >= 0 && sn.x + sn.y <= kHeavySlots);
       double S = 0.0;
       for (int j = 0; j < sn.y; ++j) S += rowsum[sn.x + j];
       A.hhot[r] = S;

@@ -21,6 +21,23 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// PSI_CHECKS builds (lib/libpsi_checked.so, PSI_LIB=checked) add device-side bounds checks
+// that trap on a violation; compute-sanitizer is not available on the GPU pool.
+#ifdef PSI_CHECKS
+#include <cstdio>
+#define PSI_ASSERT(c)                                                                    \
+  do {                                                                                   \
+    if (!(c)) {                                                                          \
+      printf("PSI_CHECKS: %s failed (%s:%d)\n", #c, __FILE__, __LINE__);                \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define PSI_ASSERT(c) \
+  do {                \
+  } while (0)
+#endif
+
 namespace psi {
 
 constexpr int kBlock = 256;              // threads per CTA of the sweep kernel

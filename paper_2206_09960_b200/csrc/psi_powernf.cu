@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(kNfBlock) k_nf_step(NfArgs a, const double* __
     double acc = 0.0;
     for (int q = b; q < e; ++q) {
       const int l = a.leaders[q];
+      PSI_ASSERT(l >= 0 && l < a.n);
       const double2 lm = a.lm[l];
       if (!init) acc = fma(lm.y, Pold[(size_t)l * kNfK + lane], acc);
       if (l == origin) acc += lm.x;

@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_t
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {
       const unsigned lab = w[q] & kLabelMask;
+      PSI_ASSERT((double)lab <= A.n_users);             // sentinel label n holds x = 0
       fl |= (w[q] >> 31) << q;
       if (lab < hs) v[q] = hot[lab];
       else if (lab < l1_lim) v[q] = ld_l1last(xs + lab, pl);
@@ -255,6 +256,7 @@ __global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_t
     const int nrows = (F > 0 && !next_flag) ? F - 1 : F;
     for (int i = tid; i < nrows; i += kBlock) {
       const int r = f0 + i;
+      PSI_ASSERT(r < A.n_act && i < kTile);
       double Sr = sm.rowsum[i];
       if (r < A.n_heavy) Sr += A.hhot[r];               // followers < H (k_heavy)
       if (READOUT) {
@@ -288,6 +290,7 @@ __global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
   for (int s = blockIdx.x * kFixBlock + tid; s < A.nsplit; s += gridDim.x * kFixBlock) {
     const int4 sp = A.split[s];
     const int r = sp.x;
+    PSI_ASSERT(r < A.n_act && sp.y <= sp.z && sp.z < A.ntiles);
     double S = A.p_out[sp.y];
     for (int k = sp.y + 1; k <= sp.z; ++k) S += A.p_in[k];
     if (r < A.n_heavy) S += A.hhot[r];

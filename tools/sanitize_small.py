@@ -27,6 +27,8 @@ def main():
             g.get_pagerank()
             g.time_sweep(2)
             g.iterate(0.0, 3)
+            if w.m <= 1 << 27:
+                g.power_nf([0, 1, w.n - 1], 1e-9)
             info = g.info()
         with psi.PsiGraph(w.row_ptr, w.followers, w.lam, w.mu) as g:   # host inputs
             g.iterate(w.eps)
