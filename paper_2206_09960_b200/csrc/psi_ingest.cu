@@ -288,6 +288,17 @@ __global__ void k_kappa_col_long(const int* list, int nlist, const int* rp, cons
 
 // ------------------------------------------------------------------ 5. relabel
 
+// class histogram: one atomic per class and warp (per-thread atomics on 5 counters serialise)
+__device__ __forceinline__ void count_class(unsigned char c, unsigned long long* counts) {
+  const unsigned active = __activemask();
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (unsigned char k = 0; k < 5; ++k) {
+    const unsigned m = __ballot_sync(active, c == k);
+    if (m && lane == __ffs(m) - 1) atomicAdd(counts + k, (unsigned long long)__popc(m));
+  }
+}
+
 __global__ void k_classify(const int* rp, const int* nlead, int n, unsigned char* cls,
                            int* new_of_old, unsigned long long* counts) {
   GRID_STRIDE(u, n) {
@@ -296,7 +307,7 @@ __global__ void k_classify(const int* rp, const int* nlead, int n, unsigned char
     unsigned char c = !active ? C_INACTIVE : nl >= 2 ? C_HOT : nl == 1 ? C_SINGLE : C_ROOT;
     cls[u] = c;
     new_of_old[u] = -1;
-    atomicAdd(counts + c, 1ull);
+    count_class(c, counts);
   }
 }
 
@@ -346,10 +357,21 @@ __global__ void k_assign(const unsigned long long* sel, long long cnt, int base,
 }
 
 // warp per (old) user: number of followers that are active (have followers themselves)
-__global__ void k_active_count(const int* rp, const int* idx, const unsigned char* cls, int n,
-                               int* act) {
+__global__ void k_active_count_short(const int* rp, const int* idx, const unsigned char* cls,
+                                     int n, int* act) {
+  GRID_STRIDE(u, n) {
+    const int b = rp[u], e = rp[u + 1];
+    if (e - b > kShort) continue;
+    int c = 0;
+    for (int q = b; q < e; ++q) c += cls[idx[q]] != C_INACTIVE;
+    act[u] = c;
+  }
+}
+__global__ void k_active_count_long(const int* list, int nlist, const int* rp, const int* idx,
+                                    const unsigned char* cls, int* act) {
   const int lane = threadIdx.x & 31;
-  WARP_STRIDE(u, n) {
+  WARP_STRIDE(i, nlist) {
+    const int u = list[i];
     const int b = rp[u], e = rp[u + 1];
     int c = 0;
     for (int q = b + lane; q < e; q += 32) c += cls[idx[q]] != C_INACTIVE;
@@ -364,7 +386,7 @@ __global__ void k_mark_heavy(const int* act, int n, int min_act, unsigned char* 
   GRID_STRIDE(u, n) {
     unsigned char c = cls[u];
     if (c != C_INACTIVE && act[u] >= min_act) cls[u] = c = C_HEAVY;
-    atomicAdd(counts + c, 1ull);
+    count_class(c, counts);
   }
 }
 
@@ -387,10 +409,11 @@ __global__ void k_row_count_short(RowCountArgs R) {
     double k = 0.0, ki = 0.0;
     for (int q = b; q < e; ++q) {
       const int v = R.idx[q];
-      if (R.cls[v] == C_INACTIVE) {
+      const int nv = R.new_of_old[v];                 // follower-less <=> label >= n_act
+      if (nv >= R.n_act) {
         k += R.a_old[v];
         ki += 1.0 / (double)max(R.nlead[v], 1);
-      } else if (heavy && R.new_of_old[v] < R.H) ++h;
+      } else if (heavy && nv < R.H) ++h;
       else ++c;
     }
     R.cnt[r] = c > 0 ? c : 1;      // 0 -> one pseudo edge
@@ -411,10 +434,11 @@ __global__ void k_row_count_long(RowCountArgs R, const int* list, int nlist) {
     double k = 0.0, ki = 0.0;
     for (int q = b + lane; q < e; q += 32) {
       const int v = R.idx[q];
-      if (R.cls[v] == C_INACTIVE) {
+      const int nv = R.new_of_old[v];                 // follower-less <=> label >= n_act
+      if (nv >= R.n_act) {
         k += R.a_old[v];
         ki += 1.0 / (double)max(R.nlead[v], 1);
-      } else if (heavy && R.new_of_old[v] < R.H) ++h;
+      } else if (heavy && nv < R.H) ++h;
       else ++c;
     }
     c = __reduce_add_sync(kFull, c);
@@ -453,9 +477,8 @@ __global__ void k_row_fill_short(RowFillArgs R) {
     int out = start;
     long long hout = heavy ? R.hoff[r] : 0;
     for (int q = b; q < e; ++q) {
-      const int v = R.idx[q];
-      if (R.cls[v] == C_INACTIVE) continue;
-      const int nv = R.new_of_old[v];
+      const int nv = R.new_of_old[R.idx[q]];
+      if (nv >= R.n_act) continue;                     // follower-less: folded into K
       if (heavy && nv < R.H) R.hot[hout++] = nv;
       else R.idx_new[out++] = nv;
     }
@@ -475,10 +498,9 @@ __global__ void k_row_fill_long(RowFillArgs R, const int* list, int nlist) {
     long long hout = heavy ? R.hoff[r] : 0;
     for (int q0 = b; q0 < e; q0 += 32) {
       const int q = q0 + lane;
-      int v = -1;
-      bool act = false;
-      if (q < e) { v = R.idx[q]; act = R.cls[v] != C_INACTIVE; }
-      const int nv = act ? R.new_of_old[v] : 0;
+      int nv = R.n_act;
+      if (q < e) nv = R.new_of_old[R.idx[q]];
+      const bool act = nv < R.n_act;                  // follower-less <=> label >= n_act
       const bool is_hot = act && heavy && nv < R.H;
       const bool is_str = act && !is_hot;
       const unsigned m1 = __ballot_sync(kFull, is_str), m2 = __ballot_sync(kFull, is_hot);
@@ -968,8 +990,17 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   if (nseg > 0) {
     Tmp act;
     IG_CK(act.alloc((size_t)n * sizeof(int)));
-    k_active_count<<<grid_for(n * 32, 256), 256, 0, s>>>(rp, idx_in, cls.as<unsigned char>(), N,
-                                                         act.as<int>());
+    k_active_count_short<<<grid_for(n, 256), 256, 0, s>>>(rp, idx_in, cls.as<unsigned char>(), N,
+                                                          act.as<int>());
+    {
+      Tmp longa;
+      const long long nl = long_segments(rp, nullptr, N, kShort, s, longa);
+      if (nl < 0) IG_CK(cudaErrorMemoryAllocation);
+      if (nl > 0)
+        k_active_count_long<<<grid_for(nl * 32, 256), 256, 0, s>>>(longa.as<int>(), (int)nl, rp,
+                                                                   idx_in, cls.as<unsigned char>(),
+                                                                   act.as<int>());
+    }
     IG_CK(cudaMemsetAsync(ccount, 0, 8 * sizeof(unsigned long long), s));
     k_mark_heavy<<<grid_for(n, 256), 256, 0, s>>>(act.as<int>(), N,
                                                   env_int("PSI_HEAVY_MIN", kDefaultHeavyMin),
