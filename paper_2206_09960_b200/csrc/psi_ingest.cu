@@ -797,9 +797,11 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   cub::DoubleBuffer<unsigned long long> kb(keys.as<unsigned long long>(), keys2.as<unsigned long long>());
   if (n_ent > 0) {
     size_t tb = 0;
-    IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, (int)n_ent, 0, end_bit, s));
+    // by (list, slot) only: the offset bits below kSegShift need no order (stable sort keeps
+    // the hot-list order inside a slot's run -- fixed, so the sums stay deterministic)
+    IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, (int)n_ent, kSegShift, end_bit, s));
     IG_CK(sort_tmp.alloc(tb));
-    IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp.p, tb, kb, (int)n_ent, 0, end_bit, s));
+    IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp.p, tb, kb, (int)n_ent, kSegShift, end_bit, s));
   }
   IG_CK(lstart.alloc((size_t)(nlists + 1) * sizeof(long long)));
   IG_CK(plen.alloc((size_t)(nlists + 1) * sizeof(long long)));
@@ -1025,7 +1027,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
                                    nsel.as<long long>(), N, s));
   IG_CK(stage_tmp.alloc(sel_bytes));
   IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, sel.as<unsigned long long>(),
-                                       sorted.as<unsigned long long>(), N, 0, 64, s));
+                                       sorted.as<unsigned long long>(), N, 32, 64, s));
   IG_CK(sort_tmp2.alloc(sort_bytes));
   int base = 0;
   int levels = 0;
@@ -1046,8 +1048,10 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     const unsigned long long* src = sel.as<unsigned long long>();
     if (sort_keys) {
       size_t b2 = sort_bytes;
+      // the selected keys arrive in ascending user order (DeviceSelect keeps it) and the
+      // radix sort is stable: sorting the high 32 bits keeps the user id as the tie-break
       IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp2.p, b2, sel.as<unsigned long long>(),
-                                           sorted.as<unsigned long long>(), (int)c, 0, 64, s));
+                                           sorted.as<unsigned long long>(), (int)c, 32, 64, s));
       src = sorted.as<unsigned long long>();
     }
     k_assign<<<grid_for(c, 256), 256, 0, s>>>(src, c, base, new_of_old.as<int>(), out.old_of_new);
