@@ -167,7 +167,18 @@ def make_workload(config, seed, pinned):
             t = torch.empty(shape, dtype={np.int64: torch.int64, np.int32: torch.int32}[dt],
                             pin_memory=True)
             return t.numpy()
-    return psigen.make_config(config, seed=seed, alloc=alloc)
+    w = psigen.make_config(config, seed=seed, alloc=alloc)
+    if pinned:                              # the activity vectors too: every H2D is from pinned memory
+        w.lam = _pinned_copy(w.lam)
+        w.mu = _pinned_copy(w.mu)
+    return w
+
+
+def _pinned_copy(a):
+    import torch
+    t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+    t.numpy()[:] = a
+    return t.numpy()
 
 
 def algorithmic_bytes_per_sweep(n, m, n_g, n_f):
