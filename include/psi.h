@@ -80,6 +80,9 @@ typedef struct psi_info {
   int64_t heavy_entries;  /* (heavy row, follower < heavy_labels) pairs summed from shared memory */
   int64_t heavy_panels;   /* work panels of the staged-segment kernel */
   int64_t heavy_labels;   /* H: labels of x staged through shared memory per sweep */
+  int64_t last_solver;    /* loop driver of the last psi_iterate / psi_pagerank: 0 = CUDA-graph
+                             WHILE node, 1 = persistent cooperative kernel (small graphs with no
+                             heavy rows), 2 = direct launches (PSI_GRAPH=0) */
 } psi_info;
 
 /*

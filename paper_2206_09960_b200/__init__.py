@@ -60,7 +60,8 @@ class psi_info(ctypes.Structure):
                 ("device_bytes", ctypes.c_int64), ("relabeled", ctypes.c_int64),
                 ("block", ctypes.c_int64), ("hot_smem", ctypes.c_int64),
                 ("n_heavy", ctypes.c_int64), ("heavy_entries", ctypes.c_int64),
-                ("heavy_panels", ctypes.c_int64), ("heavy_labels", ctypes.c_int64)]
+                ("heavy_panels", ctypes.c_int64), ("heavy_labels", ctypes.c_int64),
+                ("last_solver", ctypes.c_int64)]
 
 
 _lib = None

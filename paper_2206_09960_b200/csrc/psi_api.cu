@@ -56,6 +56,7 @@ struct psi_ctx {
   double* x[2] = {nullptr, nullptr};
   double* p_in = nullptr;        // per tile: partial of the row open at the tile start
   double* p_out = nullptr;       // per tile: partial of its last row if that row continues
+  int last_solver = 0;           // psi_info.last_solver
   double* eps_part1 = nullptr;
   double* eps_part2 = nullptr;
   double* history = nullptr;
@@ -264,6 +265,27 @@ psi_status iterate_direct(psi_ctx* c, bool pagerank = false) {
   return PSI_OK;
 }
 
+// The persistent cooperative solver (k_solve) replaces the graph's WHILE loop on graphs with
+// no k_heavy rows and at most PSI_COOP_TILES tiles (default kCoopTiles; 0 disables), when the
+// sweep grid is co-resident.  It pays off where a sweep is launch-bound.
+bool use_coop(const psi_ctx* c) {
+  long long lim = kCoopTiles;
+  if (const char* e = getenv("PSI_COOP_TILES")) lim = atoll(e);
+  return c->g.n_heavy == 0 && c->tc.solve && c->g.ntiles <= lim &&
+         c->grid1 <= c->tc.solve_max_grid;
+}
+
+psi_status iterate_coop(psi_ctx* c, bool pagerank) {
+  SweepArgs A = make_args(c, 0);
+  if (pagerank) pagerank_args(c, A);
+  A.use_cond = 0;
+  int readout = pagerank ? 0 : 1;
+  void* kp[2] = {&A, &readout};
+  API_CK(cudaLaunchCooperativeKernel(c->tc.solve, dim3(c->grid1), dim3(c->tc.block), kp, c->tc.smem,
+                                     c->stream));
+  return PSI_OK;
+}
+
 bool use_graph() {
   const char* e = getenv("PSI_GRAPH");
   return !(e && e[0] == '0');
@@ -436,8 +458,9 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   B_CK(cudaMemsetAsync(c->x[1] + n, 0, sizeof(double), c->stream));
   B_CK(cudaMallocAsync(&c->p_in, (c->g.ntiles + 1) * sizeof(double), c->stream));
   B_CK(cudaMallocAsync(&c->p_out, (c->g.ntiles + 1) * sizeof(double), c->stream));
-  B_CK(cudaMallocAsync(&c->eps_part1, c->grid1 * sizeof(double), c->stream));
-  B_CK(cudaMallocAsync(&c->eps_part2, c->grid2 * sizeof(double), c->stream));
+  // x 2: k_solve double-buffers the partials by the parity of t
+  B_CK(cudaMallocAsync(&c->eps_part1, 2 * c->grid1 * sizeof(double), c->stream));
+  B_CK(cudaMallocAsync(&c->eps_part2, 2 * std::max(c->grid1, c->grid2) * sizeof(double), c->stream));
   B_CK(cudaMallocAsync(&c->st, sizeof(LoopState), c->stream));
   B_CK(cudaMallocAsync(&c->prm, sizeof(LoopParams), c->stream));
   B_CK(cudaMemsetAsync(c->st, 0, sizeof(LoopState), c->stream));
@@ -487,7 +510,11 @@ psi_status psi_iterate(psi_ctx* c, double eps, int64_t max_iters, int norm, int6
   API_CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(LoopParams), cudaMemcpyHostToDevice, c->stream));
   API_CK(cudaEventRecord(c->ev0, c->stream));
   c->series_ok = false;
-  if (use_graph()) {
+  c->last_solver = use_coop(c) ? 1 : use_graph() ? 0 : 2;
+  if (c->last_solver == 1) {
+    psi_status cs = iterate_coop(c, false);
+    if (cs != PSI_OK) return cs;
+  } else if (c->last_solver == 0) {
     API_CK(cudaGraphLaunch(c->exec, c->stream));
   } else {
     psi_status ds = iterate_direct(c);
@@ -578,6 +605,7 @@ psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
   out->heavy_entries = c->g.heavy_entries;
   out->heavy_panels = c->g.npanels;
   out->heavy_labels = (int64_t)c->g.nseg * kSeg;
+  out->last_solver = c->last_solver;
   return PSI_OK;
 }
 
@@ -667,7 +695,11 @@ psi_status psi_pagerank(psi_ctx* c, double alpha, double eps, int64_t max_iters,
   API_CK(cudaMemcpyAsync(c->prm, c->h_prm, sizeof(LoopParams), cudaMemcpyHostToDevice, c->stream));
   c->series_ok = false;
   API_CK(cudaEventRecord(c->ev0, c->stream));
-  if (use_graph()) {
+  c->last_solver = use_coop(c) ? 1 : use_graph() ? 0 : 2;
+  if (c->last_solver == 1) {
+    psi_status cs = iterate_coop(c, true);
+    if (cs != PSI_OK) return cs;
+  } else if (c->last_solver == 0) {
     if (!c->pr_exec) {
       psi_status gs = build_graph_exec(c, true);
       if (gs != PSI_OK) return gs;

@@ -61,7 +61,8 @@ constexpr int kMaxHeavySegs = 512;       // shared-memory bound of the per-warp 
 // C5: 1 Mi; measured); PSI_HEAVY_LABELS overrides
 constexpr int kMinHeavyLabels = 1 << 19, kMaxHeavyLabels = 1 << 20;
 constexpr int kDefaultHeavyPPS = 1;      // heavy panels per SM (entry budget per panel)
-constexpr int kDefaultGroups = 4;        // tile groups (of kBlock threads) per sweep CTA
+constexpr int kDefaultGroups = 4;
+constexpr long long kCoopTiles = 4096;    // k_solve up to this many tiles (PSI_COOP_TILES)        // tile groups (of kBlock threads) per sweep CTA
 constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA
 constexpr int kDefaultL1Hot = 16384;     // labels below this gather through L1 (evict_last)
 
@@ -142,6 +143,8 @@ struct TilesCfg {                    // launch shape of k_tiles (sweep and reado
   int groups, grid, block;
   size_t smem;                       // dynamic: groups x TileSmem + hot cache
   int hot_smem, l1_lim;
+  void* solve;                       // k_solve<groups>: the persistent small-graph solver
+  int solve_max_grid;                // co-resident CTAs of k_solve (cooperative launch bound)
 };
 TilesCfg tiles_config(int ntiles, long long n);
 int fix_grid(int nsplit);            // CTAs of the fix-up kernel

@@ -27,10 +27,13 @@
 // reduction has a fixed order, so two runs give bitwise identical psi and eps_t.
 #include "psi_internal.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 
 namespace psi {
+namespace cg = cooperative_groups;
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -135,12 +138,19 @@ struct TileSmem {
 // cache holds x_{t-1}[0, hot_smem): the most-gathered labels, read from
 // shared memory instead of L2.  Gathers of labels in [hot_smem, l1_lim) allocate in L1
 // (evict_last); all others bypass L1, so streaming cold gathers cannot evict them.
-template <bool READOUT, int G>
-__global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_tiles(SweepArgs A) {
-  extern __shared__ __align__(16) unsigned char dsm[];   // [G x TileSmem][hot cache]
+// x loads of the sweep: the read-only path (L1, .nc) in a sweep kernel; in the persistent
+// small-graph solver (COH) x was written earlier in the same kernel, so L2-coherent loads.
+template <bool COH>
+__device__ __forceinline__ double ldx(const double* p, unsigned long long pol, int kind) {
+  if (COH) return __ldcg(p);
+  return kind == 0 ? ld_l1last(p, pol) : kind == 1 ? ld_l1first(p, pol) : ld_hint_na(p, pol);
+}
+
+template <bool READOUT, int G, bool COH>
+__device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* dsm, long long t,
+                                           double* part1) {
   TileSmem* smg = reinterpret_cast<TileSmem*>(dsm);
   double* hot = reinterpret_cast<double*>(dsm + G * sizeof(TileSmem));
-  const long long t = A.st->iter;
   const double* __restrict__ xs = (t & 1) ? A.x1 : A.x0;    // x_{t-1}
   double* __restrict__ xd = (t & 1) ? A.x0 : A.x1;          // x_t
   const int grp = G == 1 ? 0 : threadIdx.x / kBlock;
@@ -181,9 +191,9 @@ __global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_t
       PSI_ASSERT((double)lab <= A.n_users);             // sentinel label n holds x = 0
       fl |= (w[q] >> 31) << q;
       if (lab < hs) v[q] = hot[lab];
-      else if (lab < l1_lim) v[q] = ld_l1last(xs + lab, pl);
-      else if (lab >= single_lo) v[q] = ld_l1first(xs + lab, pf);
-      else v[q] = ld_hint_na(xs + lab, lab < hot_lim ? pl : pf);
+      else if (lab < l1_lim) v[q] = ldx<COH>(xs + lab, pl, 0);
+      else if (lab >= single_lo) v[q] = ldx<COH>(xs + lab, pf, 1);
+      else v[q] = ldx<COH>(xs + lab, lab < hot_lim ? pl : pf, 2);
     }
     if (tid == 0)
       sm.next_flag = (k + 1 >= ntiles) ? 1 : (int)(ld_stream(A.edges + (size_t)(k + 1) * kTile, pf) >> 31);
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_t
       } else {
         const unsigned long long px = (unsigned)r < hot_lim ? pl : pf;
         const double xn = fma(ld_stream(A.g + r, pf), Sr, ld_stream(acon + r, pf));
-        eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - ld_hint_na(xs + r, px));
+        eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - ldx<COH>(xs + r, px, 2));
         st_hint(xd + r, xn, st_last ? px : pf);
       }
     }
@@ -272,39 +282,52 @@ __global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_t
 
   if (!READOUT) {
     const double tot = block_sum<kBlock * G>(eps_acc, smg[0].red);
-    if (threadIdx.x == 0) A.eps_part1[blockIdx.x] = tot;
+    if (threadIdx.x == 0) part1[blockIdx.x] = tot;
   }
 }
 
-template <bool READOUT>
-__global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
+template <bool READOUT, int G>
+__global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_tiles(SweepArgs A) {
+  extern __shared__ __align__(16) unsigned char dsm[];   // [G x TileSmem][hot cache]
+  tiles_body<READOUT, G, false>(A, dsm, A.st->iter, A.eps_part1);
+}
+
+// Split rows, eps_t and the stop rule (k_fix), as a device function of any block size >= 32
+// (NT = block size).  p_in / p_out / x are read L2-coherently: in the persistent solver they
+// were written earlier in the same kernel by other CTAs.
+// COOP: only the per-CTA partial is written (the persistent solver reduces after a grid barrier).
+template <bool READOUT, int NT, bool COOP = false>
+__device__ __forceinline__ void fix_body(const SweepArgs& A, long long t, double* part2) {
   __shared__ double red[33];
   __shared__ int last;
-  const long long t = A.st->iter;
   const double* __restrict__ xs = (t & 1) ? A.x1 : A.x0;
   double* __restrict__ xd = (t & 1) ? A.x0 : A.x1;
   const int tid = threadIdx.x;
   double eps_acc = 0.0;
 
   if (blockIdx.x == 0 && tid == 0) A.st->heavy_next = 0;   // k_heavy of this sweep is done
-  for (int s = blockIdx.x * kFixBlock + tid; s < A.nsplit; s += gridDim.x * kFixBlock) {
+  for (int s = blockIdx.x * NT + tid; s < A.nsplit; s += gridDim.x * NT) {
     const int4 sp = A.split[s];
     const int r = sp.x;
     PSI_ASSERT(r < A.n_act && sp.y <= sp.z && sp.z < A.ntiles);
-    double S = A.p_out[sp.y];
-    for (int k = sp.y + 1; k <= sp.z; ++k) S += A.p_in[k];
+    double S = __ldcg(A.p_out + sp.y);
+    for (int k = sp.y + 1; k <= sp.z; ++k) S += __ldcg(A.p_in + k);
     if (r < A.n_heavy) S += A.hhot[r];
     if (READOUT) {
       A.psi[r] = (A.d[r] + A.lam[r] * S) / A.n_users;
     } else {
       const double xn = fma(A.g[r], S, ((t == 0 && A.a_first) ? A.a_first : A.a)[r]);
-      eps_acc += A.wt[r] * fabs(xn - xs[r]);
+      eps_acc += A.wt[r] * fabs(xn - __ldcg(xs + r));
       xd[r] = xn;
     }
   }
   if (READOUT) return;
 
-  const double tot = block_sum<kFixBlock>(eps_acc, red);
+  const double tot = block_sum<NT>(eps_acc, red);
+  if (COOP) {
+    if (tid == 0) part2[blockIdx.x] = tot;
+    return;
+  }
   if (tid == 0) {
     A.eps_part2[blockIdx.x] = tot;
     __threadfence();
@@ -317,11 +340,11 @@ __global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
 
   // Final, fixed-order reduction of eps_t and the loop control of Alg. 2.
   double v = 0.0;
-  for (int q = tid; q < A.grid1; q += kFixBlock) v += __ldcg(A.eps_part1 + q);
-  const double e1 = block_sum<kFixBlock>(v, red);
+  for (int q = tid; q < A.grid1; q += NT) v += __ldcg(A.eps_part1 + q);
+  const double e1 = block_sum<NT>(v, red);
   v = 0.0;
-  for (int q = tid; q < (int)gridDim.x; q += kFixBlock) v += __ldcg(A.eps_part2 + q);
-  const double e2 = block_sum<kFixBlock>(v, red);
+  for (int q = tid; q < (int)gridDim.x; q += NT) v += __ldcg(A.eps_part2 + q);
+  const double e2 = block_sum<NT>(v, red);
   if (tid == 0) {
     const LoopParams P = *A.prm;
     const double eps_t = e1 + e2 + (t == 0 ? P.eps1_extra : 0.0);
@@ -338,6 +361,11 @@ __global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
   }
 }
 
+template <bool READOUT>
+__global__ void __launch_bounds__(kFixBlock) k_fix(SweepArgs A) {
+  fix_body<READOUT, kFixBlock>(A, A.st->iter, A.eps_part2);
+}
+
 // x_0 = a (s_0 = c, Alg. 2 line 1), t = 0, gap = 1 (line 4), WHILE condition = (1 > eps).
 // Only active users are reset: follower-less users hold x = a0 in both buffers forever.
 __global__ void k_init(SweepArgs A, int n) {
@@ -352,6 +380,68 @@ __global__ void k_init(SweepArgs A, int n) {
     A.st->heavy_next = 0;
     const LoopParams P = *A.prm;
     if (A.use_cond) cudaGraphSetConditional(A.cond, (P.gap0 > P.eps && P.max_iters > 0) ? 1u : 0u);
+  }
+}
+
+
+// Persistent small-graph solver (graphs with no k_heavy rows, few tiles): the whole of Alg. 2
+// -- x_0 = a, the WHILE loop of {sweep, eps_t + stop rule}, the readout -- as ONE cooperative
+// launch with grid-wide barriers between the phases, instead of a CUDA-graph WHILE node with
+// two kernel launches per sweep.  Same arithmetic, same fixed-order reductions and the same
+// stop rule as k_init / k_tiles / k_fix (sweep counts and results agree with the graph path).
+template <int G>
+__global__ void __launch_bounds__(kBlock * G, 1) k_solve(SweepArgs A, int readout) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  cg::grid_group grid = cg::this_grid();
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n_act; i += stride) A.x0[i] = A.a0[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.st->iter = 0;
+    A.st->gap = A.prm->gap0;
+    A.st->eps_t = 0.0;
+    A.st->done = 0;
+    A.st->status = 0;
+    A.st->heavy_next = 0;
+  }
+  grid.sync();
+  const LoopParams P = *A.prm;
+  __shared__ double red[33];
+  long long t = 0;
+  double gap = P.gap0;
+  bool bad = false;
+  // Every CTA reduces the eps_t partials itself, in the same fixed order as k_fix, so all CTAs
+  // take the same stop decision without a ticket or a third barrier; CTA 0 publishes the
+  // LoopState.  The partials are double-buffered by the parity of t: a CTA can be one sweep
+  // ahead of another one still reducing.
+  while (!bad && gap > P.eps && t < P.max_iters) {
+    double* p1 = A.eps_part1 + (t & 1) * A.grid1;
+    double* p2 = A.eps_part2 + (t & 1) * gridDim.x;
+    tiles_body<false, G, true>(A, dsm, t, p1);
+    grid.sync();
+    fix_body<false, kBlock * G, true>(A, t, p2);
+    grid.sync();
+    double v = 0.0;
+    for (int q = threadIdx.x; q < A.grid1; q += blockDim.x) v += __ldcg(p1 + q);
+    const double e1 = block_sum<kBlock * G>(v, red);
+    v = 0.0;
+    for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) v += __ldcg(p2 + q);
+    const double e2 = block_sum<kBlock * G>(v, red);
+    const double eps_t = e1 + e2 + (t == 0 ? P.eps1_extra : 0.0);
+    gap = P.kappa * eps_t;
+    bad = !isfinite(eps_t);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (t < P.hist_cap) P.history[t] = eps_t;
+      A.st->eps_t = eps_t;
+      A.st->gap = gap;
+      A.st->iter = t + 1;
+      if (bad) A.st->status |= 1;
+    }
+    ++t;
+  }
+  if (readout) {
+    tiles_body<true, G, true>(A, dsm, t, nullptr);
+    grid.sync();
+    fix_body<true, kBlock * G>(A, t, nullptr);
   }
 }
 
@@ -377,6 +467,11 @@ TilesCfg cfg_for(int ntiles, long long n, int hot_req, int l1_req) {
   c.l1_lim = (int)std::max<long long>(hs, std::min<long long>(l1_req, n + 1));
   c.smem = fixed + (size_t)hs * 8;
   c.sweep = (void*)k_tiles<false, G>;
+  c.solve = (void*)k_solve<G>;
+  cudaFuncSetAttribute(k_solve<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  int occ_s = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_solve<G>, c.block, c.smem);
+  c.solve_max_grid = occ_s * sms;
   c.readout = (void*)k_tiles<true, G>;
   cudaFuncSetAttribute(k_tiles<false, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   cudaFuncSetAttribute(k_tiles<true, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
