@@ -83,6 +83,7 @@ typedef struct psi_info {
   int64_t last_solver;    /* loop driver of the last psi_iterate / psi_pagerank: 0 = CUDA-graph
                              WHILE node, 1 = persistent cooperative kernel (small graphs with no
                              heavy rows), 2 = direct launches (PSI_GRAPH=0) */
+  int64_t n_profiles;     /* activity profiles of the context (1, or k of psi_build_graph_batch) */
 } psi_info;
 
 /*
@@ -162,6 +163,40 @@ psi_status psi_get_residual_history(const psi_ctx* ctx, double* out, int64_t cap
  */
 psi_status psi_pagerank(psi_ctx* ctx, double alpha, double eps, int64_t max_iters,
                         int64_t* iters_out, double* last_gap_out);
+
+/*
+ * psi_build_graph_batch -- one graph, k activity profiles ("multi-profile
+ * batching": k activity profiles sharing one index stream).  Alg. 2 depends on
+ * the activity only through the per-user constants c, d, W; the follower lists
+ * are the graph's.  Arguments as psi_build_graph, except lambda and mu: k * n doubles each,
+ * PROFILE-MAJOR (profile p's rates at lambda[p*n .. p*n+n)), every profile obeying the
+ * activity contract.  psi_iterate on the returned context then runs Alg. 2 for every profile,
+ * four profiles per pass over the edge stream (their x interleaved: one 32-byte gather per
+ * edge for four profiles), each profile stopping on its own rule (gap_p = kappa_p eps_t^(p) <=
+ * eps, kappa_p its own ||B||_row, or norm PSI_NORM_ONE; PSI_NORM_COL is rejected);
+ * *iters_out = max_p T_p, *last_gap_out = max_p gap_p, PSI_NOT_CONVERGED if any profile did
+ * not converge.  psi_get_psi then copies k * n doubles (profile-major, original labels).
+ * The single-profile calls (psi_pagerank, psi_power_nf, psi_nsystems, psi_time_sweep) use the
+ * graph and profile 0.  No staged-segment (k_heavy) path.  Errors: those of psi_build_graph;
+ * PSI_E_INVALID_ARG if k < 1 or k > 4096.
+ */
+psi_status psi_build_graph_batch(int64_t n, int64_t m, const int64_t* row_ptr,
+                                 const int32_t* followers, int64_t k, const double* lambda,
+                                 const double* mu, int mem_kind, void* stream, psi_ctx** out);
+
+/* psi_get_profile_stats -- T_p and gap_p of every profile (host arrays of k entries each,
+ * either may be NULL) after psi_iterate on a batch context.  PSI_E_STATE otherwise. */
+psi_status psi_get_profile_stats(const psi_ctx* ctx, int64_t* iters, double* gaps);
+
+/* psi_get_profile_history -- raw epsilon_t^(p), t = 1..T_p, of profile p of a batch context
+ * into host buffer `out` of capacity `cap`; *len_out = T_p.  PSI_E_STATE / PSI_E_INVALID_ARG. */
+psi_status psi_get_profile_history(const psi_ctx* ctx, int64_t profile, double* out, int64_t cap,
+                                   int64_t* len_out);
+
+/* psi_time_sweep_batch -- device time of one four-profile sweep (k_tiles_b + k_fix_b, CUDA
+ * events around `sweeps` direct launches on the context stream, eps = 0) of group 0, in ms.
+ * Leaves the batch iterate state mid-solve (psi_get_psi needs a new psi_iterate). */
+psi_status psi_time_sweep_batch(psi_ctx* ctx, int64_t sweeps, double* sweep_ms);
 
 /* psi_get_pagerank -- copy pi[n] of the last successful psi_pagerank (original labels) to a
  * host or device buffer of n doubles.  PSI_E_STATE if psi_pagerank has not succeeded. */

@@ -40,7 +40,9 @@ _STATUS_NAMES = {0: "PSI_OK", 1: "PSI_NOT_CONVERGED", -1: "PSI_E_INVALID_ARG", -
 
 EXPORTED = ["psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
             "psi_get_residual_history", "psi_time_sweep", "psi_get_info", "psi_pagerank",
-            "psi_get_pagerank", "psi_power_nf", "psi_nsystems", "psi_destroy", "psi_last_error"]
+            "psi_get_pagerank", "psi_power_nf", "psi_nsystems", "psi_build_graph_batch",
+            "psi_get_profile_stats", "psi_get_profile_history", "psi_time_sweep_batch",
+            "psi_destroy", "psi_last_error"]
 
 
 class PsiError(RuntimeError):
@@ -61,7 +63,7 @@ class psi_info(ctypes.Structure):
                 ("block", ctypes.c_int64), ("hot_smem", ctypes.c_int64),
                 ("n_heavy", ctypes.c_int64), ("heavy_entries", ctypes.c_int64),
                 ("heavy_panels", ctypes.c_int64), ("heavy_labels", ctypes.c_int64),
-                ("last_solver", ctypes.c_int64)]
+                ("last_solver", ctypes.c_int64), ("n_profiles", ctypes.c_int64)]
 
 
 _lib = None
@@ -96,12 +98,17 @@ def load_library(build_if_stale: bool = True):
     lib.psi_get_info.argtypes = [vp, ctypes.POINTER(psi_info)]
     lib.psi_time_sweep.argtypes = [vp, i64, ctypes.POINTER(dbl), ctypes.POINTER(dbl),
                                    ctypes.POINTER(dbl)]
+    lib.psi_build_graph_batch.argtypes = [i64, i64, vp, vp, i64, vp, vp, ci, vp, ctypes.POINTER(vp)]
+    lib.psi_get_profile_stats.argtypes = [vp, vp, vp]
+    lib.psi_get_profile_history.argtypes = [vp, i64, vp, i64, ctypes.POINTER(i64)]
+    lib.psi_time_sweep_batch.argtypes = [vp, i64, ctypes.POINTER(dbl)]
     lib.psi_destroy.argtypes = [vp]
     lib.psi_destroy.restype = None
     lib.psi_last_error.restype = ctypes.c_char_p
     for f in ("psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
               "psi_get_residual_history", "psi_get_info", "psi_time_sweep", "psi_pagerank",
-              "psi_get_pagerank", "psi_power_nf", "psi_nsystems"):
+              "psi_get_pagerank", "psi_power_nf", "psi_nsystems", "psi_build_graph_batch",
+              "psi_get_profile_stats", "psi_get_profile_history", "psi_time_sweep_batch"):
         getattr(lib, f).restype = ci
     _lib = lib
     return lib
@@ -136,21 +143,35 @@ class PsiGraph:
     row_ptr int64[N+1], followers int32[M] (CSR of followers per leader), lam/mu float64[N];
     all four on the device (torch CUDA tensors) or all on the host (pinned torch tensors or
     numpy arrays).  Work runs on torch's current CUDA stream at construction.
+
+    lam/mu of shape (k, N), k >= 2, build a multi-profile batch context
+    (psi_build_graph_batch): iterate() then runs Alg. 2 for every profile and get_psi()
+    returns (k, N); profile_stats() gives each profile's T and gap.
     """
 
     def __init__(self, row_ptr, followers, lam, mu, stream=None):
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
+        shape = tuple(lam.shape) if hasattr(lam, "shape") else (len(lam),)
+        self.k = int(shape[0]) if len(shape) == 2 else 1
+        self.batch = len(shape) == 2
         parts = [_ptr_kind(x) for x in (row_ptr, followers, lam, mu)]
         kinds = {k for _, k, _ in parts}
         if len(kinds) != 1:
             raise ValueError("row_ptr, followers, lam, mu must all be host or all device")
-        self.n = int(len(lam))
+        self.n = int(shape[-1])
         self.m = int(len(followers))
         self.stream = stream if stream is not None else _current_stream()
-        st = self._lib.psi_build_graph(self.n, self.m, parts[0][0], parts[1][0], parts[2][0],
-                                       parts[3][0], kinds.pop(), self.stream,
-                                       ctypes.byref(self._ctx))
+        if len(shape) == 2:
+            if tuple(mu.shape) != shape:
+                raise ValueError("lam and mu must have the same (k, N) shape")
+            st = self._lib.psi_build_graph_batch(self.n, self.m, parts[0][0], parts[1][0], self.k,
+                                                 parts[2][0], parts[3][0], kinds.pop(),
+                                                 self.stream, ctypes.byref(self._ctx))
+        else:
+            st = self._lib.psi_build_graph(self.n, self.m, parts[0][0], parts[1][0], parts[2][0],
+                                           parts[3][0], kinds.pop(), self.stream,
+                                           ctypes.byref(self._ctx))
         if st != PSI_OK:
             raise PsiError(st, _err(self._lib))
 
@@ -177,8 +198,43 @@ class PsiGraph:
         return out
 
     def get_psi(self, out=None, device: bool = True):
-        """psi[n] in the caller's original labels (torch.float64)."""
+        """psi[n] in the caller's original labels (torch.float64); (k, n) on a batch context."""
+        if self.batch and out is None:
+            import torch
+            out = torch.empty((self.k, self.n), dtype=torch.float64,
+                              device="cuda" if device else "cpu")
         return self._get(self._lib.psi_get_psi, out, device)
+
+    def profile_stats(self):
+        """Batch context: (T[k], gap[k]) numpy arrays of the last iterate()."""
+        T = np.zeros(self.k, dtype=np.int64)
+        gap = np.zeros(self.k, dtype=np.float64)
+        st = self._lib.psi_get_profile_stats(self._ctx, T.ctypes.data, gap.ctypes.data)
+        if st != PSI_OK:
+            raise PsiError(st, _err(self._lib))
+        return T, gap
+
+    def profile_history(self, p: int) -> np.ndarray:
+        """Batch context: raw eps_t of profile p, t = 1..T_p."""
+        n = ctypes.c_int64()
+        st = self._lib.psi_get_profile_history(self._ctx, int(p), None, 0, ctypes.byref(n))
+        if st != PSI_OK:
+            raise PsiError(st, _err(self._lib))
+        out = np.empty(max(n.value, 0), dtype=np.float64)
+        if n.value:
+            st = self._lib.psi_get_profile_history(self._ctx, int(p), out.ctypes.data, n.value,
+                                                   ctypes.byref(n))
+            if st != PSI_OK:
+                raise PsiError(st, _err(self._lib))
+        return out
+
+    def time_sweep_batch(self, sweeps: int = 20) -> float:
+        """Batch context: device ms of one four-profile sweep (k_tiles_b + k_fix_b)."""
+        ms = ctypes.c_double()
+        st = self._lib.psi_time_sweep_batch(self._ctx, int(sweeps), ctypes.byref(ms))
+        if st != PSI_OK:
+            raise PsiError(st, _err(self._lib))
+        return ms.value
 
     def get_series(self, out=None, device: bool = True):
         """s_T[n] (Eq. (13)-(14)) in original labels."""

@@ -10,7 +10,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libpsi.so")
 LIB_CHECKED = os.path.join(HERE, "lib", "libpsi_checked.so")   # -DPSI_CHECKS: device bounds checks
-SOURCES = ["psi_api.cu", "psi_ingest.cu", "psi_sweep.cu", "psi_heavy.cu", "psi_pagerank.cu", "psi_powernf.cu"]
+SOURCES = ["psi_api.cu", "psi_ingest.cu", "psi_sweep.cu", "psi_heavy.cu", "psi_pagerank.cu", "psi_powernf.cu",
+           "psi_batch.cu"]
 DEPS = SOURCES + ["psi_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

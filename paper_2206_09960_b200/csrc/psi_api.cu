@@ -86,6 +86,29 @@ struct psi_ctx {
   double* hhot = nullptr;        // [n_heavy] heavy rows' sums over followers < H (k_heavy)
   int heavy_grid = 0;
   size_t heavy_smem = 0;
+  // multi-profile batch (psi_build_graph_batch, psi_batch.cu); sweep state of one group
+  struct Batch {
+    BatchCfg cfg{};
+    d4* x[2] = {nullptr, nullptr};
+    d4* p_in = nullptr;
+    d4* p_out = nullptr;
+    d4* part1 = nullptr;
+    d4* part2 = nullptr;
+    LoopStateB* st = nullptr;
+    LoopStateB* h_st = nullptr;    // pinned
+    BatchParams* prm = nullptr;
+    BatchParams* h_prm = nullptr;  // pinned
+    double* history = nullptr;     // [hist_cap][kBP]
+    long long hist_cap = 0;
+    long long hot_lim = 0;
+    std::vector<cudaGraph_t> graph;
+    std::vector<cudaGraphExec_t> exec;
+    std::vector<long long> T;
+    std::vector<double> gap;
+    std::vector<int> bad;
+    std::vector<std::vector<double>> hist;
+    bool have = false;
+  } b;
 };
 
 namespace {
@@ -107,6 +130,15 @@ void free_ctx(psi_ctx* c) {
                   c->hhot, c->g.h_ent, c->g.h_loff, c->g.h_prow, c->g.h_rslot, c->g.h_wslot};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
+  for (auto e : c->b.exec) if (e) cudaGraphExecDestroy(e);
+  for (auto g : c->b.graph) if (g) cudaGraphDestroy(g);
+  for (void* p : {(void*)c->b.x[0], (void*)c->b.x[1], (void*)c->b.p_in, (void*)c->b.p_out,
+                  (void*)c->b.part1, (void*)c->b.part2, (void*)c->b.st, (void*)c->b.prm,
+                  (void*)c->b.history, (void*)c->g.b_a0, (void*)c->g.b_a1, (void*)c->g.b_g,
+                  (void*)c->g.b_wt, (void*)c->g.b_d1, (void*)c->g.b_lam, (void*)c->g.b_psi})
+    if (p) cudaFreeAsync(p, c->stream);
+  if (c->b.h_st) cudaFreeHost(c->b.h_st);
+  if (c->b.h_prm) cudaFreeHost(c->b.h_prm);
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_prm) cudaFreeHost(c->h_prm);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -343,15 +375,237 @@ psi_status copy_out(const psi_ctx* c, const double* src, const double* scale, do
   return PSI_OK;
 }
 
+// ------------------------------------------------------------- multi-profile batch
+BatchArgs batch_args(psi_ctx* c, int gi, cudaGraphConditionalHandle cond) {
+  const long long n = c->n, na = std::max<long long>(c->g.n_act, 1);
+  BatchArgs A{};
+  A.edges = c->g.edges;
+  A.tile_row = c->g.tile_row;
+  A.ntiles = c->g.ntiles;
+  A.split = c->g.split;
+  A.nsplit = c->g.nsplit;
+  A.p_in = c->b.p_in;
+  A.p_out = c->b.p_out;
+  A.a0 = reinterpret_cast<const d4*>(c->g.b_a0) + (size_t)gi * n;
+  A.a = reinterpret_cast<const d4*>(c->g.b_a1) + (size_t)gi * na;
+  A.g = reinterpret_cast<const d4*>(c->g.b_g) + (size_t)gi * na;
+  A.wt = reinterpret_cast<const d4*>(c->g.b_wt) + (size_t)gi * na;
+  A.d = reinterpret_cast<const d4*>(c->g.b_d1) + (size_t)gi * na;
+  A.lam = reinterpret_cast<const d4*>(c->g.b_lam) + (size_t)gi * na;
+  A.psi = reinterpret_cast<d4*>(c->g.b_psi) + (size_t)gi * n;
+  A.x0 = c->b.x[0];
+  A.x1 = c->b.x[1];
+  A.eps_part1 = c->b.part1;
+  A.eps_part2 = c->b.part2;
+  A.n_users = (double)n;
+  A.n_act = (int)c->g.n_act;
+  A.hot_smem = c->b.cfg.hot_smem;
+  A.hot_lim = (int)c->b.hot_lim;
+  A.grid1 = c->b.cfg.grid1;
+  A.st = c->b.st;
+  A.prm = c->b.prm;
+  A.cond = cond;
+  A.use_cond = cond ? 1 : 0;
+  return A;
+}
+
+cudaError_t add_bnode(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode_t* dep, size_t ndep,
+                      void* fn, int grid, int block, BatchArgs* args, size_t smem = 0) {
+  cudaKernelNodeParams p{};
+  p.func = fn;
+  p.gridDim = dim3(grid);
+  p.blockDim = dim3(block);
+  p.sharedMemBytes = (unsigned)smem;
+  void* kp[1] = {args};
+  p.kernelParams = kp;
+  return cudaGraphAddKernelNode(node, g, dep, ndep, &p);
+}
+
+// k_init_b -> WHILE { k_tiles_b -> k_fix_b } -> k_tiles_b<readout> -> k_fix_b<readout>, per group
+psi_status batch_graph(psi_ctx* c, int gi) {
+  cudaGraph_t& graph = c->b.graph[gi];
+  API_CK(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle cond;
+  API_CK(cudaGraphConditionalHandleCreate(&cond, graph, 0, cudaGraphCondAssignDefault));
+  BatchArgs A = batch_args(c, gi, cond);
+  const BatchCfg& B = c->b.cfg;
+  int init_grid = (int)std::min<long long>((c->g.n_act + 255) / 256, 148LL * 8);
+  if (init_grid < 1) init_grid = 1;
+  cudaGraphNode_t n0, nw, b1, b2, r1, r2;
+  API_CK(add_bnode(graph, &n0, nullptr, 0, batch_init_ptr(), init_grid, 256, &A));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  API_CK(cudaGraphAddNode(&nw, graph, &n0, 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  API_CK(add_bnode(body, &b1, nullptr, 0, batch_tiles_ptr(false), B.grid1, B.block1, &A, B.smem));
+  API_CK(add_bnode(body, &b2, &b1, 1, batch_fix_ptr(false), B.grid2, batch_fix_block(), &A));
+  API_CK(add_bnode(graph, &r1, &nw, 1, batch_tiles_ptr(true), B.grid1, B.block1, &A, B.smem));
+  API_CK(add_bnode(graph, &r2, &r1, 1, batch_fix_ptr(true), B.grid2, batch_fix_block(), &A));
+  API_CK(cudaGraphInstantiate(&c->b.exec[gi], graph, 0));
+  return PSI_OK;
+}
+
+// sweep buffers of one group (reused by every group) and one graph per group
+psi_status batch_setup(psi_ctx* c) {
+  const long long n = c->n;
+  auto& b = c->b;
+  b.cfg = batch_config(c->g.ntiles, n, c->g.nsplit);
+  int dev = 0, l2 = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  b.hot_lim = std::min<long long>((long long)(l2 / 3.0 / sizeof(d4)), c->g.n_hot);
+  API_CK(cudaMallocAsync((void**)&b.x[0], (n + 1) * sizeof(d4), c->stream));
+  API_CK(cudaMallocAsync((void**)&b.x[1], (n + 1) * sizeof(d4), c->stream));
+  API_CK(cudaMemsetAsync(b.x[0] + n, 0, sizeof(d4), c->stream));      // sentinel x[n] = 0
+  API_CK(cudaMemsetAsync(b.x[1] + n, 0, sizeof(d4), c->stream));
+  API_CK(cudaMallocAsync((void**)&b.p_in, (c->g.ntiles + 1) * sizeof(d4), c->stream));
+  API_CK(cudaMallocAsync((void**)&b.p_out, (c->g.ntiles + 1) * sizeof(d4), c->stream));
+  API_CK(cudaMallocAsync((void**)&b.part1, b.cfg.grid1 * sizeof(d4), c->stream));
+  API_CK(cudaMallocAsync((void**)&b.part2, b.cfg.grid2 * sizeof(d4), c->stream));
+  API_CK(cudaMallocAsync((void**)&b.st, sizeof(LoopStateB), c->stream));
+  API_CK(cudaMallocAsync((void**)&b.prm, sizeof(BatchParams), c->stream));
+  API_CK(cudaMemsetAsync(b.st, 0, sizeof(LoopStateB), c->stream));
+  API_CK(cudaHostAlloc((void**)&b.h_st, sizeof(LoopStateB), cudaHostAllocDefault));
+  API_CK(cudaHostAlloc((void**)&b.h_prm, sizeof(BatchParams), cudaHostAllocDefault));
+  const int G = c->g.ngroups;
+  b.graph.assign(G, nullptr);
+  b.exec.assign(G, nullptr);
+  for (int gi = 0; gi < G; ++gi) {
+    psi_status st = batch_graph(c, gi);
+    if (st != PSI_OK) return st;
+  }
+  c->device_bytes += (size_t)(2 * (n + 1) + 2 * (c->g.ntiles + 1)) * sizeof(d4) +
+                     (size_t)G * (2 * n + 5 * std::max<long long>(c->g.n_act, 1)) * sizeof(d4);
+  API_CK(cudaStreamSynchronize(c->stream));
+  return PSI_OK;
+}
+
+psi_status batch_iterate(psi_ctx* c, double eps, long long max_iters, int norm, int64_t* iters_out,
+                         double* last_gap_out) {
+  if (norm != PSI_NORM_ROW && norm != PSI_NORM_ONE)
+    return fail(PSI_E_INVALID_ARG, "batch contexts support PSI_NORM_ROW and PSI_NORM_ONE");
+  auto& b = c->b;
+  const long long n = c->n, na = c->g.n_act;
+  const int P = c->g.nprof;
+  long long need = std::min<long long>(std::max<long long>(max_iters, 1), 1LL << 22);
+  if (!b.history || b.hist_cap < need) {
+    if (b.history) API_CK(cudaFreeAsync(b.history, c->stream));
+    b.hist_cap = std::max<long long>(need, 1024);
+    API_CK(cudaMallocAsync((void**)&b.history, b.hist_cap * kBP * sizeof(double), c->stream));
+  }
+  b.T.assign(P, 0);
+  b.gap.assign(P, 1.0);
+  b.bad.assign(P, 0);
+  b.hist.assign(P, {});
+  b.have = false;
+  std::vector<double> h;
+  API_CK(cudaEventRecord(c->ev0, c->stream));
+  for (int gi = 0; gi < c->g.ngroups; ++gi) {
+    BatchParams& hp = *b.h_prm;
+    hp.eps = eps;
+    hp.max_iters = max_iters;
+    hp.history = b.history;
+    hp.hist_cap = b.hist_cap;
+    hp.valid = 0;
+    for (int l = 0; l < kBP; ++l) {
+      const int p = gi * kBP + l;
+      hp.kappa[l] = (p < P && norm == PSI_NORM_ROW) ? c->g.b_kappa_row[p] : 1.0;
+      if (p < P) hp.valid |= 1u << l;
+    }
+    API_CK(cudaMemcpyAsync(b.prm, b.h_prm, sizeof(BatchParams), cudaMemcpyHostToDevice, c->stream));
+    // follower-less users hold x = a0 in both buffers (never swept)
+    const d4* a0 = reinterpret_cast<const d4*>(c->g.b_a0) + (size_t)gi * n;
+    if (n > na) {
+      API_CK(cudaMemcpyAsync(b.x[0] + na, a0 + na, (n - na) * sizeof(d4), cudaMemcpyDeviceToDevice,
+                             c->stream));
+      API_CK(cudaMemcpyAsync(b.x[1] + na, a0 + na, (n - na) * sizeof(d4), cudaMemcpyDeviceToDevice,
+                             c->stream));
+    }
+    API_CK(cudaGraphLaunch(b.exec[gi], c->stream));
+    API_CK(cudaMemcpyAsync(b.h_st, b.st, sizeof(LoopStateB), cudaMemcpyDeviceToHost, c->stream));
+    API_CK(cudaStreamSynchronize(c->stream));
+    const long long iters = std::min<long long>(b.h_st->iter, b.hist_cap);
+    h.resize((size_t)iters * kBP);
+    if (iters > 0) {
+      API_CK(cudaMemcpyAsync(h.data(), b.history, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream));
+      API_CK(cudaStreamSynchronize(c->stream));
+    }
+    for (int l = 0; l < kBP; ++l) {
+      const int p = gi * kBP + l;
+      if (p >= P) continue;
+      b.T[p] = b.h_st->T[l];
+      b.gap[p] = b.h_st->gap[l];
+      b.bad[p] = (b.h_st->status >> l) & 1;
+      const long long tp = std::min<long long>(b.T[p], iters);
+      b.hist[p].resize(tp);
+      for (long long t = 0; t < tp; ++t) b.hist[p][t] = h[(size_t)t * kBP + l];
+    }
+  }
+  API_CK(cudaEventRecord(c->ev1, c->stream));
+  API_CK(cudaEventSynchronize(c->ev1));
+  float ms = 0;
+  API_CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  c->iterate_ms = ms;
+  c->last_solver = 0;
+  long long Tm = 0;
+  double gm = 0.0;
+  bool any_bad = false, unconv = false;
+  for (int p = 0; p < P; ++p) {
+    Tm = std::max(Tm, b.T[p]);
+    gm = std::max(gm, b.gap[p]);
+    any_bad |= b.bad[p] != 0;
+    unconv |= b.gap[p] > eps;
+  }
+  c->last_T = Tm;
+  c->last_gap = gm;
+  c->series_ok = false;
+  if (iters_out) *iters_out = Tm;
+  if (last_gap_out) *last_gap_out = gm;
+  if (any_bad) return fail(PSI_E_NUMERIC, "epsilon_t became non-finite for some profile");
+  c->have_psi = true;
+  b.have = true;
+  if (unconv) {
+    fail(PSI_NOT_CONVERGED, "not converged: some profile's gap %.3e > eps %.3e", gm, eps);
+    return PSI_NOT_CONVERGED;
+  }
+  return PSI_OK;
+}
+
+psi_status batch_copy_out(const psi_ctx* c, double* out, int mem_kind) {
+  const size_t bytes = (size_t)c->g.nprof * c->n * sizeof(double);
+  double* dst = out;
+  double* tmp = nullptr;
+  if (mem_kind == PSI_MEM_HOST) {
+    API_CK(cudaMallocAsync((void**)&tmp, bytes, c->stream));
+    dst = tmp;
+  }
+  API_CK(batch_unpermute(c->g.b_psi, c->g.old_of_new, c->n, c->g.nprof, dst, c->stream));
+  if (tmp) {
+    API_CK(cudaMemcpyAsync(out, tmp, bytes, cudaMemcpyDeviceToHost, c->stream));
+    API_CK(cudaFreeAsync(tmp, c->stream));
+  }
+  API_CK(cudaStreamSynchronize(c->stream));
+  return PSI_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 const char* psi_last_error(void) { return g_err.c_str(); }
 
-psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* followers,
-                           const double* lambda, const double* mu, int mem_kind, void* stream,
-                           psi_ctx** out) {
+}  // extern "C"
+
+namespace {
+psi_status batch_setup(psi_ctx* c);
+
+psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* followers,
+                 const double* lambda, const double* mu, int nprof, int mem_kind, void* stream,
+                 psi_ctx** out) {
   g_err.clear();
   if (!out) return fail(PSI_E_INVALID_ARG, "out is NULL");
   *out = nullptr;
@@ -405,13 +659,15 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   if (mem_kind == PSI_MEM_HOST) {
     B_CK(cudaMallocAsync(&staged[0], (n + 1) * sizeof(long long), c->stream));
     B_CK(cudaMallocAsync(&staged[1], (m > 0 ? m : 1) * sizeof(int), c->stream));
-    B_CK(cudaMallocAsync(&staged[2], n * sizeof(double), c->stream));
-    B_CK(cudaMallocAsync(&staged[3], n * sizeof(double), c->stream));
+    B_CK(cudaMallocAsync(&staged[2], nprof * n * sizeof(double), c->stream));
+    B_CK(cudaMallocAsync(&staged[3], nprof * n * sizeof(double), c->stream));
     B_CK(cudaMemcpyAsync(staged[0], row_ptr, (n + 1) * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
     if (m > 0)
       B_CK(cudaMemcpyAsync(staged[1], followers, m * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    B_CK(cudaMemcpyAsync(staged[2], lambda, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    B_CK(cudaMemcpyAsync(staged[3], mu, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    B_CK(cudaMemcpyAsync(staged[2], lambda, nprof * n * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream));
+    B_CK(cudaMemcpyAsync(staged[3], mu, nprof * n * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream));
     rp_d = (const long long*)staged[0];
     idx_d = (const int*)staged[1];
     lam_d = (const double*)staged[2];
@@ -419,7 +675,7 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
   }
 
   char msg[512] = {0};
-  int rc = ingest(n, m, rp_d, idx_d, lam_d, mu_d, c->stream, c->g, msg, sizeof(msg));
+  int rc = ingest(n, m, rp_d, idx_d, lam_d, mu_d, nprof, c->stream, c->g, msg, sizeof(msg));
   if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
 
   // Iteration buffers.
@@ -479,9 +735,37 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const i
 
   psi_status gs = build_graph_exec(c);
   if (gs != PSI_OK) return bail(gs);
+  if (nprof > 1) {
+    gs = batch_setup(c);
+    if (gs != PSI_OK) return bail(gs);
+  }
   *out = c;
   return PSI_OK;
 #undef B_CK
+}
+}  // namespace
+
+extern "C" {
+
+psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* followers,
+                           const double* lambda, const double* mu, int mem_kind, void* stream,
+                           psi_ctx** out) {
+  return build(n, m, row_ptr, followers, lambda, mu, 1, mem_kind, stream, out);
+}
+
+psi_status psi_build_graph_batch(int64_t n, int64_t m, const int64_t* row_ptr,
+                                 const int32_t* followers, int64_t nprof, const double* lambda,
+                                 const double* mu, int mem_kind, void* stream, psi_ctx** out) {
+  g_err.clear();
+  if (nprof < 1 || nprof > 4096) {
+    if (out) *out = nullptr;
+    return fail(PSI_E_INVALID_ARG, "nprof = %lld outside [1, 4096]", (long long)nprof);
+  }
+  if ((double)nprof * (double)n > 2147483647.0 * 64.0) {
+    if (out) *out = nullptr;
+    return fail(PSI_E_INVALID_ARG, "nprof * n too large");
+  }
+  return build(n, m, row_ptr, followers, lambda, mu, (int)nprof, mem_kind, stream, out);
 }
 
 psi_status psi_iterate(psi_ctx* c, double eps, int64_t max_iters, int norm, int64_t* iters_out,
@@ -498,6 +782,7 @@ psi_status psi_iterate(psi_ctx* c, double eps, int64_t max_iters, int norm, int6
     default: return fail(PSI_E_INVALID_ARG, "bad norm %d", norm);
   }
   c->have_psi = false;
+  if (c->g.nprof > 1) return batch_iterate(c, eps, max_iters, norm, iters_out, last_gap_out);
   psi_status hs = ensure_history(c, max_iters);
   if (hs != PSI_OK) return hs;
   c->h_prm->eps = eps;
@@ -548,6 +833,7 @@ psi_status psi_get_psi(const psi_ctx* c, double* out, int mem_kind) {
   if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
     return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
   if (!c->have_psi) return fail(PSI_E_STATE, "no successful psi_iterate on this context");
+  if (c->g.nprof > 1) return batch_copy_out(c, out, mem_kind);
   return copy_out(c, c->g.psi, nullptr, out, mem_kind);
 }
 
@@ -567,6 +853,8 @@ psi_status psi_get_residual_history(const psi_ctx* c, double* out, int64_t cap, 
   if (!c || (cap > 0 && !out)) return fail(PSI_E_INVALID_ARG, "NULL argument");
   if (!c->have_psi && !c->have_pr)
     return fail(PSI_E_STATE, "no successful psi_iterate / psi_pagerank on this context");
+  if (c->g.nprof > 1 && c->b.have)
+    return fail(PSI_E_STATE, "batch context: use psi_get_profile_history");
   if (len_out) *len_out = c->last_T;
   long long k = c->last_T;
   if (k > cap) k = cap;
@@ -606,6 +894,7 @@ psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
   out->heavy_panels = c->g.npanels;
   out->heavy_labels = (int64_t)c->g.nseg * kSeg;
   out->last_solver = c->last_solver;
+  out->n_profiles = c->g.nprof;
   return PSI_OK;
 }
 
@@ -731,6 +1020,72 @@ psi_status psi_pagerank(psi_ctx* c, double alpha, double eps, int64_t max_iters,
     fail(PSI_NOT_CONVERGED, "not converged: gap %.3e > eps %.3e after %lld sweeps", gap, eps, T);
     return PSI_NOT_CONVERGED;
   }
+  return PSI_OK;
+}
+
+psi_status psi_get_profile_stats(const psi_ctx* c, int64_t* iters, double* gaps) {
+  g_err.clear();
+  if (!c) return fail(PSI_E_INVALID_ARG, "ctx is NULL");
+  if (c->g.nprof < 2) return fail(PSI_E_STATE, "not a batch context (psi_build_graph_batch)");
+  if (!c->b.have) return fail(PSI_E_STATE, "no successful psi_iterate on this batch context");
+  for (int p = 0; p < c->g.nprof; ++p) {
+    if (iters) iters[p] = c->b.T[p];
+    if (gaps) gaps[p] = c->b.gap[p];
+  }
+  return PSI_OK;
+}
+
+psi_status psi_get_profile_history(const psi_ctx* c, int64_t profile, double* out, int64_t cap,
+                                   int64_t* len_out) {
+  g_err.clear();
+  if (!c || (cap > 0 && !out)) return fail(PSI_E_INVALID_ARG, "NULL argument");
+  if (c->g.nprof < 2) return fail(PSI_E_STATE, "not a batch context (psi_build_graph_batch)");
+  if (!c->b.have) return fail(PSI_E_STATE, "no successful psi_iterate on this batch context");
+  if (profile < 0 || profile >= c->g.nprof) return fail(PSI_E_INVALID_ARG, "bad profile %lld", (long long)profile);
+  const auto& h = c->b.hist[profile];
+  if (len_out) *len_out = c->b.T[profile];
+  const long long k = std::min<long long>(cap, (long long)h.size());
+  for (long long t = 0; t < k; ++t) out[t] = h[t];
+  return PSI_OK;
+}
+
+psi_status psi_time_sweep_batch(psi_ctx* c, int64_t sweeps, double* sweep_ms) {
+  g_err.clear();
+  if (!c || sweeps < 1) return fail(PSI_E_INVALID_ARG, "ctx NULL or sweeps < 1");
+  if (c->g.nprof < 2) return fail(PSI_E_STATE, "not a batch context (psi_build_graph_batch)");
+  auto& b = c->b;
+  BatchParams& hp = *b.h_prm;
+  if (!b.history || b.hist_cap < sweeps) {
+    if (b.history) API_CK(cudaFreeAsync(b.history, c->stream));
+    b.hist_cap = std::max<long long>(sweeps, 1024);
+    API_CK(cudaMallocAsync((void**)&b.history, b.hist_cap * kBP * sizeof(double), c->stream));
+  }
+  hp.eps = 0.0;
+  hp.max_iters = sweeps;
+  hp.history = b.history;
+  hp.hist_cap = b.hist_cap;
+  hp.valid = (1u << kBP) - 1;
+  for (int l = 0; l < kBP; ++l) hp.kappa[l] = 1.0;
+  API_CK(cudaMemcpyAsync(b.prm, b.h_prm, sizeof(BatchParams), cudaMemcpyHostToDevice, c->stream));
+  BatchArgs A = batch_args(c, 0, 0);
+  void* kp[1] = {&A};
+  int init_grid = (int)std::min<long long>((c->g.n_act + 255) / 256, 148LL * 8);
+  API_CK(cudaLaunchKernel(batch_init_ptr(), dim3(init_grid < 1 ? 1 : init_grid), dim3(256), kp, 0,
+                          c->stream));
+  API_CK(cudaEventRecord(c->ev0, c->stream));
+  for (long long t = 0; t < sweeps; ++t) {
+    API_CK(cudaLaunchKernel(batch_tiles_ptr(false), dim3(b.cfg.grid1), dim3(b.cfg.block1), kp,
+                            b.cfg.smem, c->stream));
+    API_CK(cudaLaunchKernel(batch_fix_ptr(false), dim3(b.cfg.grid2), dim3(batch_fix_block()), kp, 0,
+                            c->stream));
+  }
+  API_CK(cudaEventRecord(c->ev1, c->stream));
+  API_CK(cudaEventSynchronize(c->ev1));
+  float ms = 0;
+  API_CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  c->have_psi = false;
+  b.have = false;
+  if (sweep_ms) *sweep_ms = ms / sweeps;
   return PSI_OK;
 }
 

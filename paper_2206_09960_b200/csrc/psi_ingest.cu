@@ -828,9 +828,102 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
 
 }  // namespace
 
+// ---- batch (nprof > 1): folded constants and interleaved vectors of every profile
+// K_j^(p) = sum of a^(p) over the follower-less followers of row j, in input order -- the
+// summation of k_row_count_short / _long, so profile 0 gets the single-profile K bit for bit.
+__global__ void k_fold_short(const int* rp, const int* idx, const int* old_of_new,
+                             const int* new_of_old, const double* a_old, int n_act, double* K) {
+  GRID_STRIDE(r, n_act) {
+    const int o = old_of_new[r];
+    const int b = rp[o], e = rp[o + 1];
+    if (e - b > kShort) continue;
+    double k = 0.0;
+    for (int q = b; q < e; ++q) {
+      const int v = idx[q];
+      if (new_of_old[v] >= n_act) k += a_old[v];
+    }
+    K[r] = k;
+  }
+}
+__global__ void k_fold_long(const int* list, int nlist, const int* rp, const int* idx,
+                            const int* old_of_new, const int* new_of_old, const double* a_old,
+                            int n_act, double* K) {
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(i, nlist) {
+    const int r = list[i];
+    const int o = old_of_new[r];
+    const int b = rp[o], e = rp[o + 1];
+    double k = 0.0;
+    for (int q = b + lane; q < e; q += 32) {
+      const int v = idx[q];
+      if (new_of_old[v] >= n_act) k += a_old[v];
+    }
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) k += __shfl_xor_sync(kFull, k, sh);
+    if (lane == 0) K[r] = k;
+  }
+}
+// profile p into lane p % kBP of group p / kBP (the k_permute_vectors arithmetic)
+__global__ void k_permute_b(const int* old_of_new, long long n, int n_act, int p,
+                            const double* a_old, const double* g_old, const double* wt_old,
+                            const double* d_old, const double* lam, const double* K,
+                            IngestOut o) {
+  const int gi = p / kBP, l = p % kBP;
+  GRID_STRIDE(r, n) {
+    const int u = old_of_new[r];
+    o.b_a0[((size_t)gi * n + r) * kBP + l] = a_old[u];
+    if (r < n_act) {
+      const size_t q = ((size_t)gi * n_act + r) * kBP + l;
+      const double k = K[r];
+      o.b_a1[q] = fma(g_old[u], k, a_old[u]);
+      o.b_g[q] = g_old[u];
+      o.b_wt[q] = wt_old[u];
+      o.b_d1[q] = fma(lam[u], k, d_old[u]);
+      o.b_lam[q] = lam[u];
+    } else {
+      o.b_psi[((size_t)gi * n + r) * kBP + l] = d_old[u] / (double)n;
+    }
+  }
+}
+
+int batch_vectors(IngestOut& out, long long n, int NA, int nprof, const int* rp, const int* idx,
+                  const int* new_of_old, const int* longr, long long nlongr, const double* bold,
+                  const double* lam, cudaStream_t s, char* msg, size_t msg_len) {
+  const int G = (nprof + kBP - 1) / kBP;
+  out.nprof = nprof;
+  out.ngroups = G;
+  const size_t nb = (size_t)G * n * kBP * sizeof(double);
+  const size_t ab = (size_t)G * std::max(NA, 1) * kBP * sizeof(double);
+  IG_CK(cudaMallocAsync(&out.b_a0, nb, s));
+  IG_CK(cudaMallocAsync(&out.b_psi, nb, s));
+  for (double** q : {&out.b_a1, &out.b_g, &out.b_wt, &out.b_d1, &out.b_lam})
+    IG_CK(cudaMallocAsync(q, ab, s));
+  for (double* q : {out.b_a0, out.b_psi}) IG_CK(cudaMemsetAsync(q, 0, nb, s));
+  for (double* q : {out.b_a1, out.b_g, out.b_wt, out.b_d1, out.b_lam}) IG_CK(cudaMemsetAsync(q, 0, ab, s));
+  Tmp K;
+  IG_CK(K.alloc((size_t)std::max(NA, 1) * sizeof(double)));
+  for (int p = 0; p < nprof; ++p) {
+    const double* base = bold + (size_t)p * 4 * n;
+    if (NA > 0) {
+      k_fold_short<<<grid_for(NA, 256), 256, 0, s>>>(rp, idx, out.old_of_new, new_of_old, base, NA,
+                                                     K.as<double>());
+      if (nlongr > 0)
+        k_fold_long<<<grid_for(nlongr * 32, 256), 256, 0, s>>>(longr, (int)nlongr, rp, idx,
+                                                               out.old_of_new, new_of_old, base, NA,
+                                                               K.as<double>());
+    }
+    k_permute_b<<<grid_for(n, 256), 256, 0, s>>>(out.old_of_new, n, NA, p, base, base + n,
+                                                 base + 2 * n, base + 3 * n, lam + (size_t)p * n,
+                                                 K.as<double>(), out);
+  }
+  IG_CK(cudaStreamSynchronize(s));
+  return PSI_OK;
+}
+
 int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
-           const double* lam, const double* mu, cudaStream_t s, IngestOut& out, char* msg,
-           size_t msg_len) {
+           const double* lam, const double* mu, int nprof, cudaStream_t s, IngestOut& out,
+           char* msg, size_t msg_len) {
+  if (nprof < 1) nprof = 1;
   const int N = (int)n, Mm = (int)m;
   Tmp flags;
   IG_CK(flags.alloc(sizeof(int)));
@@ -849,7 +942,9 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   }
   // ---- 1. validation
   k_check_rowptr<<<grid_for(n, 256), 256, 0, s>>>(rp64, n, m, flags.as<int>());
-  k_check_activity<<<grid_for(n, 256), 256, 0, s>>>(lam, mu, n, flags.as<int>());
+  for (int p = 0; p < nprof; ++p)
+    k_check_activity<<<grid_for(n, 256), 256, 0, s>>>(lam + (size_t)p * n, mu + (size_t)p * n, n,
+                                                      flags.as<int>());
   IG_CK(cudaMemcpyAsync(&hflags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   IG_CK(cudaStreamSynchronize(s));
   if (hflags & (F_RP0 | F_RPN | F_RPMONO)) {
@@ -878,6 +973,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   tr.mark("validate");
   // ---- 2.-4. transpose, normalisers, constants (old labels)
   Tmp a_old, g_old, wt_old, d_old, first_leader, nlead, red;
+  Tmp bold, bkmax;                       // batch: old-label constants of every profile
   IG_CK(a_old.alloc((size_t)n * sizeof(double)));
   IG_CK(g_old.alloc((size_t)n * sizeof(double)));
   IG_CK(wt_old.alloc((size_t)n * sizeof(double)));
@@ -951,6 +1047,36 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     if (nlong > 0)
       k_kappa_col_long<<<grid_for(nlong * 32, 256), 256, 0, s>>>(longu.as<int>(), (int)nlong, rp,
                                                                  idx_in, wt_old.as<double>(), lam, kmax);
+    if (nprof > 1) {
+      // the constants (a, g, Wt, d) and ||B||_row of every profile, old labels, same kernels
+      IG_CK(bold.alloc((size_t)nprof * 4 * n * sizeof(double)));
+      IG_CK(bkmax.alloc((size_t)nprof * 4 * sizeof(unsigned long long)));
+      IG_CK(cudaMemsetAsync(bkmax.p, 0, (size_t)nprof * 4 * sizeof(unsigned long long), s));
+      Tmp fl_dummy, cnt_dummy, longb;
+      IG_CK(fl_dummy.alloc((size_t)n * sizeof(int)));
+      IG_CK(cnt_dummy.alloc(4 * sizeof(unsigned long long)));
+      const long long nlb = long_segments(loff.as<int>(), nullptr, N, kShort, s, longb);
+      if (nlb < 0) IG_CK(cudaErrorMemoryAllocation);
+      for (int p = 0; p < nprof; ++p) {
+        double* base = bold.as<double>() + (size_t)p * 4 * n;
+        unsigned long long* km = bkmax.as<unsigned long long>() + 4 * p;
+        k_pack_activity<<<grid_for(n, 256), 256, 0, s>>>(lam + (size_t)p * n, mu + (size_t)p * n, n,
+                                                         lm.as<double2>());
+        k_norm_short<<<grid_for(n, 256), 256, 0, s>>>(
+            loff.as<int>(), vals.Current(), lm.as<double2>(), N, base, base + n, base + 2 * n,
+            base + 3 * n, fl_dummy.as<int>(), km, cnt_dummy.as<unsigned long long>());
+        if (nlb > 0)
+          k_norm_long<<<grid_for(nlb * 32, 256), 256, 0, s>>>(
+              longb.as<int>(), (int)nlb, loff.as<int>(), vals.Current(), lm.as<double2>(), base,
+              base + n, base + 2 * n, base + 3 * n, fl_dummy.as<int>(), km);
+      }
+      std::vector<unsigned long long> hk((size_t)nprof * 4);
+      IG_CK(cudaMemcpyAsync(hk.data(), bkmax.p, hk.size() * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
+      IG_CK(cudaStreamSynchronize(s));
+      out.b_kappa_row.resize(nprof);
+      for (int p = 0; p < nprof; ++p) memcpy(&out.b_kappa_row[p], &hk[4 * p], 8);
+    }
   }
 
   if (out.nf_loff) {
@@ -988,6 +1114,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   // forces it on/off
   const int heavy_env = env_int("PSI_HEAVY", -1);
   if (heavy_env == 0 || (heavy_env < 0 && n < kDefaultHeavyMinN)) nseg = 0;
+  if (nprof > 1) nseg = 0;                     // the batch sweep has no staged-segment path
   nseg = (int)std::min<long long>(std::min(nseg, kMaxHeavySegs), (n + 1) / kSeg);
   if (nseg > 0) {
     Tmp act;
@@ -1172,6 +1299,12 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
       d_old.as<double>(), lam, K.as<double>(), (double)n, nlead.as<int>(), out.a0, out.a1, out.g,
       out.wt, out.d1, out.lam, out.psi, out.nlead);
   out.relabeled = 1;
+  if (nprof > 1) {
+    int rc3 = batch_vectors(out, n, NA, nprof, rp, idx_in, new_of_old.as<int>(), longr.as<int>(),
+                            nlongr, bold.as<double>(), lam, s, msg, msg_len);
+    if (rc3 != PSI_OK) return rc3;
+    bold.reset();
+  }
 
   tr.mark("vectors");
   // ---- 7. edge tiles: first row of every tile, rows spanning tiles

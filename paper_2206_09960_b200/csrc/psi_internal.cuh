@@ -21,6 +21,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <vector>
+
 // PSI_CHECKS builds (lib/libpsi_checked.so, PSI_LIB=checked) add device-side bounds checks
 // that trap on a violation; compute-sanitizer is not available on the GPU pool.
 #ifdef PSI_CHECKS
@@ -61,8 +63,8 @@ constexpr int kMaxHeavySegs = 512;       // shared-memory bound of the per-warp 
 // C5: 1 Mi; measured); PSI_HEAVY_LABELS overrides
 constexpr int kMinHeavyLabels = 1 << 19, kMaxHeavyLabels = 1 << 20;
 constexpr int kDefaultHeavyPPS = 1;      // heavy panels per SM (entry budget per panel)
-constexpr int kDefaultGroups = 4;
-constexpr long long kCoopTiles = 4096;    // k_solve up to this many tiles (PSI_COOP_TILES)        // tile groups (of kBlock threads) per sweep CTA
+constexpr int kDefaultGroups = 4;        // tile groups (of kBlock threads) per sweep CTA
+constexpr long long kCoopTiles = 4096;   // k_solve up to this many tiles (PSI_COOP_TILES)
 constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA
 constexpr int kDefaultL1Hot = 16384;     // labels below this gather through L1 (evict_last)
 
@@ -191,6 +193,17 @@ struct IngestOut {
   double kappa_row = 0, kappa_col = 0, rho_A = 0;
   long long n_f = 0, n_g = 0, n_leaderless = 0;
   int relabeled = 0;
+  // multi-profile batch (psi_build_graph_batch): nprof activity profiles on one graph, in
+  // groups of kBP interleaved per user ([group][user][kBP]; unused lanes of the last group 0)
+  int nprof = 1, ngroups = 0;
+  double* b_a0 = nullptr;     // [ngroups][n][kBP]     x_0
+  double* b_a1 = nullptr;     // [ngroups][n_act][kBP] sweep constant a + g K
+  double* b_g = nullptr;      // [ngroups][n_act][kBP]
+  double* b_wt = nullptr;     // [ngroups][n_act][kBP] Wt (residual weights)
+  double* b_d1 = nullptr;     // [ngroups][n_act][kBP] readout constant d + lambda K
+  double* b_lam = nullptr;    // [ngroups][n_act][kBP]
+  double* b_psi = nullptr;    // [ngroups][n][kBP]     readout; [n_act, n) prefilled with d/N
+  std::vector<double> b_kappa_row;  // [nprof] ||B||_row of every profile
 };
 
 // ---- Power-NF (psi_powernf.cu): Alg. 1 for a batch of kNfK origins, caller labels
@@ -233,9 +246,75 @@ cudaError_t pagerank_prep(const IngestOut& G, long long n, double alpha, const P
 cudaError_t pagerank_readout(const IngestOut& G, long long n, double alpha, const double* xT,
                              long long T, const PrBuffers& B, cudaStream_t s);
 
-// Returns 0 or a negative psi_status; msg gets a description on error.
+// Returns 0 or a negative psi_status; msg gets a description on error.  nprof > 1: lam_dev /
+// mu_dev hold nprof profiles (profile-major, nprof * n); the single-profile outputs are those
+// of profile 0, the b_* arrays those of all profiles, and the heavy-row path is off.
 int ingest(long long n, long long m, const long long* rp64_dev, const int* idx_dev,
-           const double* lam_dev, const double* mu_dev, cudaStream_t s, IngestOut& out,
-           char* msg, size_t msg_len);
+           const double* lam_dev, const double* mu_dev, int nprof, cudaStream_t s,
+           IngestOut& out, char* msg, size_t msg_len);
+
+// ---- multi-profile batch sweep (psi_batch.cu): kBP profiles per pass over the edge stream
+constexpr int kBP = 4;                   // profiles per group (one 32-byte x gather per edge)
+struct __align__(32) d4 { double v[kBP]; };
+
+struct LoopStateB {
+  long long iter;            // sweeps of this group
+  unsigned active;           // bit p: profile p still iterating
+  unsigned done;             // CTA arrival counter of k_fix_b
+  int status;                // bit p: non-finite eps_t of profile p
+  int pad;
+  double gap[kBP];
+  double eps_t[kBP];
+  long long T[kBP];          // T of every profile (its own stop, Alg. 2 per profile)
+};
+struct BatchParams {
+  double eps;
+  long long max_iters;
+  double kappa[kBP];
+  double* history;           // [hist_cap][kBP]
+  long long hist_cap;
+  unsigned valid;            // profiles of this group that exist
+};
+struct BatchArgs {
+  const unsigned* edges;
+  const int* tile_row;
+  int ntiles;
+  const int4* split;
+  int nsplit;
+  d4* p_in;                  // [ntiles + 1]
+  d4* p_out;
+  const d4* a0;              // [n]
+  const d4* a;               // [n_act]
+  const d4* g;
+  const d4* wt;
+  const d4* d;
+  const d4* lam;
+  d4* psi;                   // [n]
+  d4* x0;                    // [n + 1] ping-pong, x[n] = 0
+  d4* x1;
+  d4* eps_part1;             // [grid1]
+  d4* eps_part2;             // [grid2]
+  double n_users;
+  int n_act;
+  int hot_smem;
+  int hot_lim;
+  int grid1;
+  LoopStateB* st;
+  const BatchParams* prm;
+  cudaGraphConditionalHandle cond;
+  int use_cond;
+};
+struct BatchCfg {
+  int grid1, block1, grid2;
+  size_t smem;
+  int hot_smem;
+};
+BatchCfg batch_config(int ntiles, long long n, int nsplit);
+void* batch_tiles_ptr(bool readout);
+void* batch_fix_ptr(bool readout);
+void* batch_init_ptr();
+int batch_fix_block();
+cudaError_t batch_unpermute(const double* psi_groups, const int* old_of_new, long long n, int nprof,
+                            double* out, cudaStream_t s);
 
 }  // namespace psi

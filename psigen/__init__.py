@@ -187,6 +187,31 @@ def _lognormal_activity(n, seed):
     return lam, mu
 
 
+def activity_profiles(n: int, k: int, kind: str = "lognormal", seed: int = SEED,
+                      pure_posters: bool = False):
+    """k independent activity profiles (lam, mu), each of shape (k, n), for the multi-profile
+    batch.  Profile j draws from streams 100 + 2j / 101 + 2j of the
+    configs' generator: "lognormal" = configs 3-5 (LogNormal(-1, 1.5), LogNormal(-0.5, 1.0)),
+    "uniform" = config 1 (U(0.05, 1)); pure_posters zeroes floor(0.05 n) mu per profile
+    (config 5)."""
+    lam = np.empty((k, n), dtype=np.float64)
+    mu = np.empty((k, n), dtype=np.float64)
+    for j in range(k):
+        if kind == "lognormal":
+            lam[j] = lognormal(n, -1.0, 1.5, seed, 100 + 2 * j)
+            mu[j] = lognormal(n, -0.5, 1.0, seed, 101 + 2 * j)
+        elif kind == "uniform":
+            lam[j] = uniform(n, 0.05, 1.0, seed, 100 + 2 * j)
+            mu[j] = uniform(n, 0.05, 1.0, seed, 101 + 2 * j)
+        else:
+            raise ValueError(kind)
+        if pure_posters:
+            row = np.ascontiguousarray(mu[j])
+            zero_subset(row, n // 20, seed + 1 + j)
+            mu[j] = row
+    return lam, mu
+
+
 def make_config(k: int, seed: int = SEED, alloc=None, scale: int | None = None) -> Workload:
     """Config k of BASELINE.json (k = 1..5; 0 = the N=64 ER companion of config 1).
 

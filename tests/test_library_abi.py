@@ -49,6 +49,10 @@ def test_error_paths_without_device():
     assert st == psi.PSI_E_INVALID_ARG
     info = psi.psi_info()
     assert lib.psi_get_info(None, ctypes.byref(info)) == psi.PSI_E_INVALID_ARG
+    st = lib.psi_build_graph_batch(10, 0, None, None, 0, None, None, 0, None, ctypes.byref(ctx))
+    assert st == psi.PSI_E_INVALID_ARG and b"nprof" in lib.psi_last_error()
+    assert lib.psi_get_profile_stats(None, None, None) == psi.PSI_E_INVALID_ARG
+    assert lib.psi_time_sweep_batch(None, 1, None) == psi.PSI_E_INVALID_ARG
     lib.psi_destroy(None)   # no-op
 
 
