@@ -337,7 +337,42 @@ def run_ours(args, ws, rank, local):
     sweep_ms = heavy_ms + tiles_ms + fix_ms
     g.iterate(eps)   # leave the context at the eps solution
 
-    # ---- e2e through the C-ABI with host (pinned) buffers
+    # ---- roofline of the sweep
+    peak, peak_kind = _peaks()
+    bsweep = algorithmic_bytes_per_sweep(n, m, info["n_g"], info["n_f"])
+    achieved = bsweep / (sweep_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": _traffic_from_profiles("sweep", args.config),
+            "kernel": "one sweep = k_heavy + k_tiles<sweep> + k_fix<sweep>; each launch timed "
+                      "with CUDA events on the library stream (psi_time_sweep, 20 sweeps)",
+            "k_heavy_ms": round(heavy_ms, 4), "k_tiles_ms": round(tiles_ms, 4),
+            "k_fix_ms": round(fix_ms, 4),
+            "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+            "algorithmic_bytes_per_sweep": bsweep,
+            "sweep_ms": round(sweep_ms, 4), "sweep_gteps": round(m / (sweep_ms * 1e-3) / 1e9, 2),
+            "frac_of_8TBs_nominal": round(achieved / 8000.0, 4)}
+
+    out = {"metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (psigen, seed = rank)", "config": _config_dict(args, w),
+           "time_to_eps_ms": round(ms_step, 4), "iterations_T": T,
+           "ingest_ms": round(info["ingest_ms"], 2), "gpu_launches": launches,
+           "roofline": roof, "clocks": clk.summary(),
+           "pagerank": {"what": "psi_pagerank: PageRank power method, Eq. (22), alpha = 0.85, "
+                                "same graph, eps and kernels (SURVEY 8(f) row 1)",
+                        "time_to_eps_ms": round(pr_ms, 3), "iterations_T": pr_T,
+                        "gteps": round(float(m) * pr_T / (pr_ms * 1e-3) / 1e9, 2)},
+           "graph_info": {k: info[k] for k in ("n_f", "n_g", "n_leaderless", "kappa_row", "kappa_col",
+                                               "rho_A", "num_tiles", "num_long_rows", "grid", "block", "hot_smem",
+                                               "n_heavy", "heavy_entries", "heavy_panels", "heavy_labels",
+                                               "relabeled")}}
+    g.close()
+    del d_in
+    torch.cuda.empty_cache()
+
+    # ---- e2e through the C-ABI with host (pinned) buffers -- after the device-resident
+    # context is gone, as a user of the public API would run it
     host = [torch.from_numpy(a) for a in (w.row_ptr, w.followers, w.lam, w.mu)]
     psi_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
     h2d = (n + 1) * 8 + m * 4 + 2 * n * 8
@@ -364,42 +399,9 @@ def run_ours(args, ws, rank, local):
     e2e_edges = sum_over_ranks(float(m) * (Te[-1] + 1), ws, dev)
     e2e_val = e2e_edges / (e2e_ms * 1e-3) / 1e9
 
-    # ---- roofline of the sweep
-    peak, peak_kind = _peaks()
-    bsweep = algorithmic_bytes_per_sweep(n, m, info["n_g"], info["n_f"])
-    achieved = bsweep / (sweep_ms * 1e-3) / 1e9
-    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": _traffic_from_profiles("sweep", args.config),
-            "kernel": "one sweep = k_heavy + k_tiles<sweep> + k_fix<sweep>; each launch timed "
-                      "with CUDA events on the library stream (psi_time_sweep, 20 sweeps)",
-            "k_heavy_ms": round(heavy_ms, 4), "k_tiles_ms": round(tiles_ms, 4),
-            "k_fix_ms": round(fix_ms, 4),
-            "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-            "algorithmic_bytes_per_sweep": bsweep,
-            "sweep_ms": round(sweep_ms, 4), "sweep_gteps": round(m / (sweep_ms * 1e-3) / 1e9, 2),
-            "frac_of_8TBs_nominal": round(achieved / 8000.0, 4)}
-
-    out = {"metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": ws,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (psigen, seed = rank)", "config": _config_dict(args, w),
-           "time_to_eps_ms": round(ms_step, 4), "iterations_T": T,
-           "ingest_ms": round(info["ingest_ms"], 2), "gpu_launches": launches,
-           "e2e": {"value": round(e2e_val, 3), "unit": "GTEPS", "ms_per_step": round(e2e_ms, 2),
-                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                   "what": "psi_build_graph(pinned host CSR) + psi_iterate(eps) + psi_get_psi(host)"},
-           "roofline": roof, "clocks": clk.summary(),
-           "pagerank": {"what": "psi_pagerank: PageRank power method, Eq. (22), alpha = 0.85, "
-                                "same graph, eps and kernels (SURVEY 8(f) row 1)",
-                        "time_to_eps_ms": round(pr_ms, 3), "iterations_T": pr_T,
-                        "gteps": round(float(m) * pr_T / (pr_ms * 1e-3) / 1e9, 2)},
-           "graph_info": {k: info[k] for k in ("n_f", "n_g", "n_leaderless", "kappa_row", "kappa_col",
-                                               "rho_A", "num_tiles", "num_long_rows", "grid", "block", "hot_smem",
-                                               "n_heavy", "heavy_entries", "heavy_panels", "heavy_labels",
-                                               "relabeled")}}
-    g.close()
-    del d_in
-    torch.cuda.empty_cache()
+    out["e2e"] = {"value": round(e2e_val, 3), "unit": "GTEPS", "ms_per_step": round(e2e_ms, 2),
+                  "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                  "what": "psi_build_graph(pinned host CSR) + psi_iterate(eps) + psi_get_psi(host)"}
     if rank == 0 and not args.no_batch:
         try:
             out["batch"] = batch_side(w, dev, args.config, sweep_ms)

@@ -932,14 +932,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
 
   Trace tr(s);
   g_tmp_stream = s;
-  {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      unsigned long long keep = 64ull << 30;         // ingest temporaries stay reserved
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-  }
+  // (the pool's release threshold is set by psi_build_graph: temporaries stay reserved)
   // ---- 1. validation
   k_check_rowptr<<<grid_for(n, 256), 256, 0, s>>>(rp64, n, m, flags.as<int>());
   for (int p = 0; p < nprof; ++p)
