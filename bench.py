@@ -378,7 +378,7 @@ def run_ours(args, ws, rank, local):
     h2d = (n + 1) * 8 + m * 4 + 2 * n * 8
     d2h = n * 8
     e2e_steps = max(1, min(args.steps, 3))
-    for _ in range(1):
+    for _ in range(2):             # untimed: the first builds grow the stream-ordered pool
         with psi.PsiGraph(*host) as gh:
             gh.iterate(eps)
             gh.get_psi(out=psi_host)
