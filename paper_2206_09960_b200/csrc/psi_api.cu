@@ -153,6 +153,7 @@ SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   A.ntiles = c->g.ntiles;
   A.split = c->g.split;
   A.nsplit = c->g.nsplit;
+  A.nsplit_long = c->g.nsplit_long;
   A.p_in = c->p_in;
   A.p_out = c->p_out;
   A.a0 = c->g.a0;
@@ -384,6 +385,7 @@ BatchArgs batch_args(psi_ctx* c, int gi, cudaGraphConditionalHandle cond) {
   A.ntiles = c->g.ntiles;
   A.split = c->g.split;
   A.nsplit = c->g.nsplit;
+  A.nsplit_long = c->g.nsplit_long;
   A.p_in = c->b.p_in;
   A.p_out = c->b.p_out;
   A.a0 = reinterpret_cast<const d4*>(c->g.b_a0) + (size_t)gi * n;

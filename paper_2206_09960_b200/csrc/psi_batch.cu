@@ -27,12 +27,12 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned kLabelMask = 0x7fffffffu;
-constexpr int kTB = 512;               // threads per tile (16 warps)
+constexpr int kTB = kTile / 4;         // threads per tile (4 edges each)
 constexpr int kEB = kTile / kTB;       // 4 edges per thread
 constexpr int kWB = kTB / 32;
 constexpr int kBHot = 1024;            // labels of x_{t-1} (x 4 profiles) in shared memory
 constexpr int kFixB = 256;
-constexpr int kGB = 2;                 // tile groups per CTA (named barriers 1..kGB)
+constexpr int kGB = 1024 / kTB;        // tile groups per CTA (named barriers 1..kGB)
 static_assert(kEB == 4, "one 128-bit index load per thread");
 
 __device__ __forceinline__ unsigned long long pol_first() {
@@ -297,12 +297,7 @@ __global__ void __launch_bounds__(kFixB) k_fix_b(BatchArgs A) {
   d4* __restrict__ xd = (t & 1) ? A.x0 : A.x1;
   const int tid = threadIdx.x;
   d4 eps_acc = zero4();
-  for (int s = blockIdx.x * kFixB + tid; s < A.nsplit; s += gridDim.x * kFixB) {
-    const int4 sp = A.split[s];
-    const int r = sp.x;
-    PSI_ASSERT(r < A.n_act && sp.y <= sp.z && sp.z < A.ntiles);
-    d4 S = A.p_out[sp.y];
-    for (int k = sp.y + 1; k <= sp.z; ++k) add4(S, A.p_in[k]);
+  auto finish = [&](int r, const d4& S) {
     if (READOUT) {
       d4 o;
 #pragma unroll
@@ -319,6 +314,30 @@ __global__ void __launch_bounds__(kFixB) k_fix_b(BatchArgs A) {
       }
       xd[r] = xn;
     }
+  };
+  // rows spanning more than kLongSpan tiles: a warp each (lane-strided, fixed shuffle tree)
+  const int lane = tid & 31;
+  for (int s = (blockIdx.x * kFixB + tid) >> 5; s < A.nsplit_long; s += gridDim.x * (kFixB / 32)) {
+    const int4 sp = A.split[s];
+    PSI_ASSERT(sp.x < A.n_act && sp.y <= sp.z && sp.z < A.ntiles);
+    d4 S = zero4();
+    for (int k = sp.y + 1 + lane; k <= sp.z; k += 32) add4(S, A.p_in[k]);
+#pragma unroll
+    for (int p = 0; p < kBP; ++p)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) S.v[p] += __shfl_xor_sync(kFull, S.v[p], o);
+    if (lane == 0) {
+      d4 T = A.p_out[sp.y];
+      add4(T, S);
+      finish(sp.x, T);
+    }
+  }
+  for (int s = A.nsplit_long + blockIdx.x * kFixB + tid; s < A.nsplit; s += gridDim.x * kFixB) {
+    const int4 sp = A.split[s];
+    PSI_ASSERT(sp.x < A.n_act && sp.y <= sp.z && sp.z < A.ntiles);
+    d4 S = A.p_out[sp.y];
+    for (int k = sp.y + 1; k <= sp.z; ++k) add4(S, A.p_in[k]);
+    finish(sp.x, S);
   }
   if (READOUT) return;
 

@@ -28,6 +28,7 @@
 #include "psi_internal.cuh"
 #include "../../include/psi.h"
 
+#include <cub/device/device_partition.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -886,6 +887,10 @@ __global__ void k_permute_b(const int* old_of_new, long long n, int n_act, int p
   }
 }
 
+__global__ void k_long_split_flags(const int4* split, long long ns, unsigned char* flag) {
+  GRID_STRIDE(i, ns) flag[i] = (split[i].z - split[i].y) > kLongSpan;
+}
+
 int batch_vectors(IngestOut& out, long long n, int NA, int nprof, const int* rp, const int* idx,
                   const int* new_of_old, const int* longr, long long nlongr, const double* bold,
                   const double* lam, cudaStream_t s, char* msg, size_t msg_len) {
@@ -1325,9 +1330,26 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     }
     out.nsplit = (int)hs;
     IG_CK(cudaMallocAsync(&out.split, (size_t)(hs > 0 ? hs : 1) * sizeof(int4), s));
-    if (hs > 0)
+    if (hs > 0) {
       k_split_fill<<<grid_for(hs, 256), 256, 0, s>>>(rows.as<int>(), hs, rp_new.as<int>(),
                                                      out.split);
+      // rows spanning more than kLongSpan tiles first (summed by a warp each in k_fix)
+      Tmp sp2, lf, part_tmp;
+      IG_CK(sp2.alloc((size_t)hs * sizeof(int4)));
+      IG_CK(lf.alloc((size_t)hs));
+      k_long_split_flags<<<grid_for(hs, 256), 256, 0, s>>>(out.split, hs, lf.as<unsigned char>());
+      size_t pb = 0;
+      IG_CK(cub::DevicePartition::Flagged(nullptr, pb, out.split, lf.as<unsigned char>(),
+                                          sp2.as<int4>(), ns.as<long long>(), (int)hs, s));
+      IG_CK(part_tmp.alloc(pb));
+      IG_CK(cub::DevicePartition::Flagged(part_tmp.p, pb, out.split, lf.as<unsigned char>(),
+                                          sp2.as<int4>(), ns.as<long long>(), (int)hs, s));
+      IG_CK(cudaMemcpyAsync(out.split, sp2.p, (size_t)hs * sizeof(int4), cudaMemcpyDeviceToDevice, s));
+      long long nl = 0;
+      IG_CK(cudaMemcpyAsync(&nl, ns.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+      IG_CK(cudaStreamSynchronize(s));
+      out.nsplit_long = (int)nl;
+    }
     IG_CK(cudaStreamSynchronize(s));
   }
   IG_CK(cudaGetLastError());

@@ -42,10 +42,11 @@
 
 namespace psi {
 
-constexpr int kBlock = 256;              // threads per CTA of the sweep kernel
+constexpr int kBlock = 128;              // threads per tile group of the sweep kernel
 constexpr int kEpt = 8;                  // edges per thread
-constexpr int kTile = kBlock * kEpt;     // 2048 edges per tile
+constexpr int kTile = kBlock * kEpt;     // 1024 edges per tile
 constexpr int kFixBlock = 256;           // threads per CTA of the split-row fix-up kernel
+constexpr int kLongSpan = 16;            // split rows over more tiles are summed by a warp
 constexpr unsigned kRowFlag = 0x80000000u;
 // staged-segment heavy-row kernel (psi_heavy.cu)
 constexpr int kSegShift = 13;
@@ -63,7 +64,7 @@ constexpr int kMaxHeavySegs = 512;       // shared-memory bound of the per-warp 
 // C5: 1 Mi; measured); PSI_HEAVY_LABELS overrides
 constexpr int kMinHeavyLabels = 1 << 19, kMaxHeavyLabels = 1 << 20;
 constexpr int kDefaultHeavyPPS = 1;      // heavy panels per SM (entry budget per panel)
-constexpr int kDefaultGroups = 4;        // tile groups (of kBlock threads) per sweep CTA
+constexpr int kDefaultGroups = 8;        // tile groups (of kBlock threads) per sweep CTA
 constexpr long long kCoopTiles = 4096;   // k_solve up to this many tiles (PSI_COOP_TILES)
 constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA
 constexpr int kDefaultL1Hot = 16384;     // labels below this gather through L1 (evict_last)
@@ -105,8 +106,9 @@ struct SweepArgs {
   const unsigned* edges;     // flagged edge stream [ntiles * kTile]
   const int* tile_row;       // tile_row[k] = number of row flags before edge k*kTile (k <= ntiles)
   int ntiles;
-  const int4* split;         // rows spanning tiles: {row, first tile, last tile, 0}
-  int nsplit;
+  const int4* split;         // rows spanning tiles: {row, first tile, last tile, 0}; the
+  int nsplit;                // first nsplit_long span more than kLongSpan tiles (warp each)
+  int nsplit_long;
   double* p_in;              // per tile: partial of the row open at the tile's start
   double* p_out;             // per tile: partial of the last row started in it, if it continues
   const double* a0;          // x_0 (init)                       [n_act]
@@ -177,8 +179,9 @@ struct IngestOut {
   double* nf_wt = nullptr;
   double2* nf_lm = nullptr;
   int ntiles = 0;
-  int4* split = nullptr;
+  int4* split = nullptr;      // [nsplit] rows spanning tiles, the nsplit_long long ones first
   int nsplit = 0;
+  int nsplit_long = 0;
   long long n_act = 0, m_act = 0, n_hot = 0, n_pseudo = 0;
   long long single_lo = 0;    // first label of the single-leader users (gathered once, in order)
   // heavy rows (labels [0, n_heavy)): followers < H served by k_heavy (HeavyPlan)
@@ -281,6 +284,7 @@ struct BatchArgs {
   int ntiles;
   const int4* split;
   int nsplit;
+  int nsplit_long;
   d4* p_in;                  // [ntiles + 1]
   d4* p_out;
   const d4* a0;              // [n]

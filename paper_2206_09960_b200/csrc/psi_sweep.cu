@@ -306,12 +306,7 @@ __device__ __forceinline__ void fix_body(const SweepArgs& A, long long t, double
   double eps_acc = 0.0;
 
   if (blockIdx.x == 0 && tid == 0) A.st->heavy_next = 0;   // k_heavy of this sweep is done
-  for (int s = blockIdx.x * NT + tid; s < A.nsplit; s += gridDim.x * NT) {
-    const int4 sp = A.split[s];
-    const int r = sp.x;
-    PSI_ASSERT(r < A.n_act && sp.y <= sp.z && sp.z < A.ntiles);
-    double S = __ldcg(A.p_out + sp.y);
-    for (int k = sp.y + 1; k <= sp.z; ++k) S += __ldcg(A.p_in + k);
+  auto finish = [&](int r, double S) {
     if (r < A.n_heavy) S += A.hhot[r];
     if (READOUT) {
       A.psi[r] = (A.d[r] + A.lam[r] * S) / A.n_users;
@@ -320,6 +315,24 @@ __device__ __forceinline__ void fix_body(const SweepArgs& A, long long t, double
       eps_acc += A.wt[r] * fabs(xn - __ldcg(xs + r));
       xd[r] = xn;
     }
+  };
+  // rows spanning more than kLongSpan tiles: a warp each (lane-strided, fixed shuffle tree)
+  const int lane = tid & 31;
+  for (int s = (blockIdx.x * NT + tid) >> 5; s < A.nsplit_long; s += gridDim.x * (NT / 32)) {
+    const int4 sp = A.split[s];
+    PSI_ASSERT(sp.x < A.n_act && sp.y <= sp.z && sp.z < A.ntiles);
+    double S = 0.0;
+    for (int k = sp.y + 1 + lane; k <= sp.z; k += 32) S += __ldcg(A.p_in + k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+    if (lane == 0) finish(sp.x, __ldcg(A.p_out + sp.y) + S);
+  }
+  for (int s = A.nsplit_long + blockIdx.x * NT + tid; s < A.nsplit; s += gridDim.x * NT) {
+    const int4 sp = A.split[s];
+    PSI_ASSERT(sp.x < A.n_act && sp.y <= sp.z && sp.z < A.ntiles);
+    double S = __ldcg(A.p_out + sp.y);
+    for (int k = sp.y + 1; k <= sp.z; ++k) S += __ldcg(A.p_in + k);
+    finish(sp.x, S);
   }
   if (READOUT) return;
 
@@ -498,7 +511,8 @@ TilesCfg tiles_config(int ntiles, long long n) {
   switch (G) {
     case 1: return cfg_for<1>(ntiles, n, hot, l1);
     case 2: return cfg_for<2>(ntiles, n, hot, l1);
-    default: return cfg_for<4>(ntiles, n, hot, l1);
+    case 4: return cfg_for<4>(ntiles, n, hot, l1);
+    default: return cfg_for<8>(ntiles, n, hot, l1);
   }
 }
 
