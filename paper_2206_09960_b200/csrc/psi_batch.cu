@@ -136,7 +136,7 @@ __device__ __forceinline__ void grp_bar(int id) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(kTB) : "memory");
 }
 
-// kGB tile groups of kTB threads per CTA, one 2048-edge tile per group pass (persistent grid).
+// kGB tile groups of kTB threads per CTA, one kTile-edge tile per group pass (persistent grid).
 // Per tile: the gathers are issued first; while they are in flight the row-flag counts are
 // scanned (so every thread knows the local index n_ex of the first row it starts); the
 // thread's values are then folded in ONE pass -- rows that start and end inside the thread

@@ -94,7 +94,7 @@ __device__ __forceinline__ double ld_l1last(const double* p, unsigned long long 
                : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
-// named barrier over one 256-thread tile group of the CTA (id 0 is __syncthreads)
+// named barrier over one kBlock-thread tile group of the CTA (id 0 is __syncthreads)
 __device__ __forceinline__ void group_bar(int id) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(kBlock) : "memory");
 }
