@@ -685,11 +685,12 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   c->grid1 = c->tc.grid;
   {
     // Hot prefix of x kept in L2 (evict_last) in BOTH ping-pong buffers: PSI_HOT_MB per
-    // buffer (default: a third of L2 each), never more than the users with >= 2 leaders.
+    // buffer (default: 0.65 of L2, measured best at C5: profiles/r1/tune_hot_mb_r1.txt), never
+    // more than the users with >= 2 leaders.
     int dev = 0, l2 = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-    double hot_mb = l2 / 3.0 / (1 << 20);
+    double hot_mb = l2 * 0.65 / (1 << 20);
     if (const char* e = getenv("PSI_HOT_MB")) hot_mb = atof(e);
     long long lim = (long long)(hot_mb * (1 << 20) / 8.0);
     c->hot_lim = std::min<long long>(std::max<long long>(lim, 0), c->g.n_hot);
