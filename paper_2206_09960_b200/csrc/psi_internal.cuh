@@ -65,7 +65,7 @@ constexpr int kMaxHeavySegs = 512;       // shared-memory bound of the per-warp 
 constexpr int kMinHeavyLabels = 1 << 19, kMaxHeavyLabels = 1 << 20;
 constexpr int kDefaultHeavyPPS = 1;      // heavy panels per SM (entry budget per panel)
 constexpr int kDefaultGroups = 8;        // tile groups (of kBlock threads) per sweep CTA
-constexpr long long kCoopTiles = 4096;   // k_solve up to this many tiles (PSI_COOP_TILES)
+constexpr long long kCoopTiles = 8192;   // k_solve up to this many tiles (8.4M edge slots; PSI_COOP_TILES)
 constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA
 constexpr int kDefaultL1Hot = 16384;     // labels below this gather through L1 (evict_last)
 
