@@ -628,6 +628,24 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
       unsigned long long keep = ~0ull;
       if (const char* e = getenv("PSI_POOL_KEEP_GB")) keep = (unsigned long long)atoll(e) << 30;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      // Reserve the ingest's working set in ONE block the first time a graph this large is
+      // built: later builds carve their temporaries out of it instead of mapping new memory
+      // when the pool is fragmented (measured: +0.2-0.6 s builds at C5 without it).
+      // PSI_POOL_RESERVE=0 disables.
+      static unsigned long long reserved_for = 0;
+      const unsigned long long est = 16ull * (unsigned long long)m +
+                                     (unsigned long long)nprof * 160ull * (unsigned long long)n +
+                                     (256ull << 20);
+      const char* rv = getenv("PSI_POOL_RESERVE");
+      if (!(rv && rv[0] == '0') && est > reserved_for && keep == ~0ull) {
+        cudaMemPoolTrimTo(pool, 0);
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, est, (cudaStream_t)stream) == cudaSuccess) {
+          cudaFreeAsync(p, (cudaStream_t)stream);
+          reserved_for = est;
+        }
+        cudaGetLastError();
+      }
     }
   }
   psi_ctx* c = new psi_ctx;
