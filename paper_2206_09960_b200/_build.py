@@ -15,7 +15,7 @@ SOURCES = ["psi_api.cu", "psi_ingest.cu", "psi_sweep.cu", "psi_heavy.cu", "psi_p
 DEPS = SOURCES + ["psi_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-t", "0"]
 
 
 def _stale(lib: str = LIB) -> bool:
