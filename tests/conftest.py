@@ -29,3 +29,12 @@ def gpu():
     import paper_2206_09960_b200 as psi
     psi.load_library()  # raises if libpsi.so is missing: no fallback
     return psi
+
+
+@pytest.fixture(params=["default", "graph"])
+def driver(request, monkeypatch):
+    """Small graphs run in the persistent cooperative solver by default (k_solve); "graph"
+    forces the CUDA-graph WHILE loop (k_init / k_tiles / k_fix) on the same inputs."""
+    if request.param == "graph":
+        monkeypatch.setenv("PSI_COOP_TILES", "0")
+    return request.param

@@ -51,7 +51,7 @@ def pr_parity(psi, w, alpha, eps=1e-12):
 
 
 @pytest.mark.parametrize("alpha", [0.85, 0.5])
-def test_pagerank_config1(gpu, alpha):
+def test_pagerank_config1(gpu, alpha, driver):
     pr_parity(gpu, psigen.make_config(1), alpha)
 
 
@@ -80,7 +80,7 @@ def test_pagerank_rmat_heavy_rows(gpu, heavy, monkeypatch):
     assert (got["info"]["n_heavy"] > 0) == (heavy == "1")
 
 
-def test_pagerank_edgeless_and_chain(gpu):
+def test_pagerank_edgeless_and_chain(gpu, driver):
     # edgeless: every user is follower-less -> pi = (1 - alpha)/N after one sweep, and the
     # second sweep changes nothing (exact fixed point: the loop stops at T = 2 < max_iters)
     n = 5

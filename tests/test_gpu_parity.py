@@ -75,8 +75,9 @@ def parity(psi, w, norm="row", eps=None, full=True):
 
 # ---------------------------------------------------------------- fixtures
 
+
 @pytest.mark.parametrize("name", ["chain", "mutual", "cycle3_homogeneous", "edgeless"])
-def test_spec_fixtures_on_gpu(gpu, name):
+def test_spec_fixtures_on_gpu(gpu, name, driver):
     import json, os
     case = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
                                        "spec_examples.json")))[name]
@@ -88,14 +89,14 @@ def test_spec_fixtures_on_gpu(gpu, name):
         assert abs(got["psi"].sum() - case["psi_sum"]) < 1e-12
 
 
-def test_chain_iteration_count_and_history(gpu):
+def test_chain_iteration_count_and_history(gpu, driver):
     rp, f = psigen.csr_from_edges(2, [(0, 1)])
     got = gpu_run(gpu, rp, f, np.array([0.5, 0.5]), np.array([0.5, 0.5]), 1e-12)
     assert got["T"] == 2 and got["hist"][0] == pytest.approx(0.25, abs=1e-15) and got["hist"][1] == 0
     np.testing.assert_allclose(got["s"], [0.5, 0.75], atol=1e-15)
 
 
-def test_heterogeneous_cycle_and_star_closed_forms(gpu):
+def test_heterogeneous_cycle_and_star_closed_forms(gpu, driver):
     rng = np.random.default_rng(11)
     n = 9
     rp, f = psigen.csr_from_edges(n, [(j, (j + 1) % n) for j in range(n)])
@@ -116,7 +117,7 @@ def test_heterogeneous_cycle_and_star_closed_forms(gpu):
 
 
 @pytest.mark.parametrize("seed", range(30))
-def test_random_small_graphs_fixed_count(gpu, seed):
+def test_random_small_graphs_fixed_count(gpu, seed, driver):
     """Random graphs N in [10, 300] (leaderless, mu = 0 and lambda = 0 users): exact
     Alg. 2 parity at a fixed T, all three norms."""
     rng = np.random.default_rng(500 + seed)
@@ -173,7 +174,7 @@ def test_config0_and_nsystems(gpu):
 
 
 @pytest.mark.parametrize("norm", ["row", "col", "one"])
-def test_config1_parity(gpu, norm):
+def test_config1_parity(gpu, norm, driver):
     w = psigen.make_config(1)
     parity(gpu, w, norm=norm)
 
