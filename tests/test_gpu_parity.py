@@ -299,3 +299,31 @@ def test_full_size_parity(gpu, cfg):
     T*, the same top-k, and the eps-mode stop within one sweep of T*."""
     w = psigen.make_config(cfg)
     parity(gpu, w, full=True)
+
+
+# ------------------------------------------------ exact and ragged tile boundaries, tiny graphs
+
+@pytest.mark.parametrize("F", [511, 512, 513, 1023, 1024, 1025, 1536])
+def test_tile_boundary_sizes(gpu, F, driver):
+    """Leader 0 followed by users 1..F, each of them followed by 0: 2F active edge slots, so the
+    edge stream ends exactly on, just before or just after a 1024-edge tile boundary, and row 0
+    spans one or two tiles (a split row)."""
+    n = F + 1
+    edges = [(i, 0) for i in range(1, n)] + [(0, i) for i in range(1, n)]
+    rp, f = psigen.csr_from_edges(n, edges)
+    rng = np.random.default_rng(F)
+    lam, mu = rng.uniform(0.05, 1.0, n), rng.uniform(0.05, 1.0, n)
+    ref = oracle.power_psi(rp, f, lam, mu, eps=1e-13)
+    got = gpu_run(gpu, rp, f, lam, mu, 0.0, ref.iterations)
+    assert got["T"] == ref.iterations
+    assert oracle.max_rel_error(ref.psi, got["psi"]) <= TOL
+
+
+def test_single_user_and_no_edges(gpu, driver):
+    """N = 1 (no edges possible): psi = d / N after T = 1 (epsilon_1 = 0)."""
+    rp, f = np.zeros(2, np.int64), np.zeros(0, np.int32)
+    lam, mu = np.array([0.3]), np.array([0.6])
+    ref = oracle.power_psi(rp, f, lam, mu, eps=1e-12)
+    got = gpu_run(gpu, rp, f, lam, mu, 1e-12)
+    assert got["T"] == ref.iterations
+    np.testing.assert_allclose(got["psi"], ref.psi, rtol=1e-15)
