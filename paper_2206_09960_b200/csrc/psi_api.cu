@@ -458,7 +458,9 @@ psi_status batch_setup(psi_ctx* c) {
   int dev = 0, l2 = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-  b.hot_lim = std::min<long long>((long long)(l2 / 3.0 / sizeof(d4)), c->g.n_hot);
+  double hot_frac = 0.65;                              // as the single-profile hot prefix
+  if (const char* e = getenv("PSI_BATCH_HOT_FRAC")) hot_frac = atof(e);
+  b.hot_lim = std::min<long long>((long long)(l2 * hot_frac / sizeof(d4)), c->g.n_hot);
   API_CK(cudaMallocAsync((void**)&b.x[0], (n + 1) * sizeof(d4), c->stream));
   API_CK(cudaMallocAsync((void**)&b.x[1], (n + 1) * sizeof(d4), c->stream));
   API_CK(cudaMemsetAsync(b.x[0] + n, 0, sizeof(d4), c->stream));      // sentinel x[n] = 0
