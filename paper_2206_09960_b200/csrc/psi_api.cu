@@ -135,7 +135,8 @@ void free_ctx(psi_ctx* c) {
   for (void* p : {(void*)c->b.x[0], (void*)c->b.x[1], (void*)c->b.p_in, (void*)c->b.p_out,
                   (void*)c->b.part1, (void*)c->b.part2, (void*)c->b.st, (void*)c->b.prm,
                   (void*)c->b.history, (void*)c->g.b_a0, (void*)c->g.b_a1, (void*)c->g.b_g,
-                  (void*)c->g.b_wt, (void*)c->g.b_d1, (void*)c->g.b_lam, (void*)c->g.b_psi})
+                  (void*)c->g.b_wt, (void*)c->g.b_d1, (void*)c->g.b_lam, (void*)c->g.b_psi,
+                  (void*)c->g.b_tile_row, (void*)c->g.b_split})
     if (p) cudaFreeAsync(p, c->stream);
   if (c->b.h_st) cudaFreeHost(c->b.h_st);
   if (c->b.h_prm) cudaFreeHost(c->b.h_prm);
@@ -381,11 +382,11 @@ BatchArgs batch_args(psi_ctx* c, int gi, cudaGraphConditionalHandle cond) {
   const long long n = c->n, na = std::max<long long>(c->g.n_act, 1);
   BatchArgs A{};
   A.edges = c->g.edges;
-  A.tile_row = c->g.tile_row;
-  A.ntiles = c->g.ntiles;
-  A.split = c->g.split;
-  A.nsplit = c->g.nsplit;
-  A.nsplit_long = c->g.nsplit_long;
+  A.tile_row = c->g.b_tile_row;                  // the batch sweep's own 512-edge tiling
+  A.ntiles = c->g.b_ntiles;
+  A.split = c->g.b_split;
+  A.nsplit = c->g.b_nsplit;
+  A.nsplit_long = c->g.b_nsplit_long;
   A.p_in = c->b.p_in;
   A.p_out = c->b.p_out;
   A.a0 = reinterpret_cast<const d4*>(c->g.b_a0) + (size_t)gi * n;
@@ -454,7 +455,7 @@ psi_status batch_graph(psi_ctx* c, int gi) {
 psi_status batch_setup(psi_ctx* c) {
   const long long n = c->n;
   auto& b = c->b;
-  b.cfg = batch_config(c->g.ntiles, n, c->g.nsplit);
+  b.cfg = batch_config(c->g.b_ntiles, n, c->g.b_nsplit);
   int dev = 0, l2 = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
@@ -465,8 +466,8 @@ psi_status batch_setup(psi_ctx* c) {
   API_CK(cudaMallocAsync((void**)&b.x[1], (n + 1) * sizeof(d4), c->stream));
   API_CK(cudaMemsetAsync(b.x[0] + n, 0, sizeof(d4), c->stream));      // sentinel x[n] = 0
   API_CK(cudaMemsetAsync(b.x[1] + n, 0, sizeof(d4), c->stream));
-  API_CK(cudaMallocAsync((void**)&b.p_in, (c->g.ntiles + 1) * sizeof(d4), c->stream));
-  API_CK(cudaMallocAsync((void**)&b.p_out, (c->g.ntiles + 1) * sizeof(d4), c->stream));
+  API_CK(cudaMallocAsync((void**)&b.p_in, (c->g.b_ntiles + 1) * sizeof(d4), c->stream));
+  API_CK(cudaMallocAsync((void**)&b.p_out, (c->g.b_ntiles + 1) * sizeof(d4), c->stream));
   API_CK(cudaMallocAsync((void**)&b.part1, b.cfg.grid1 * sizeof(d4), c->stream));
   API_CK(cudaMallocAsync((void**)&b.part2, b.cfg.grid2 * sizeof(d4), c->stream));
   API_CK(cudaMallocAsync((void**)&b.st, sizeof(LoopStateB), c->stream));
@@ -481,7 +482,7 @@ psi_status batch_setup(psi_ctx* c) {
     psi_status st = batch_graph(c, gi);
     if (st != PSI_OK) return st;
   }
-  c->device_bytes += (size_t)(2 * (n + 1) + 2 * (c->g.ntiles + 1)) * sizeof(d4) +
+  c->device_bytes += (size_t)(2 * (n + 1) + 2 * (c->g.b_ntiles + 1)) * sizeof(d4) +
                      (size_t)G * (2 * n + 5 * std::max<long long>(c->g.n_act, 1)) * sizeof(d4);
   API_CK(cudaStreamSynchronize(c->stream));
   return PSI_OK;

@@ -27,8 +27,8 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned kLabelMask = 0x7fffffffu;
-constexpr int kTB = kTile / 4;         // threads per tile (4 edges each)
-constexpr int kEB = kTile / kTB;       // 4 edges per thread
+constexpr int kTB = kTileB / 4;        // threads per tile (4 edges each)
+constexpr int kEB = kTileB / kTB;      // 4 edges per thread
 constexpr int kWB = kTB / 32;
 constexpr int kBHot = 1024;            // labels of x_{t-1} (x 4 profiles) in shared memory
 constexpr int kFixB = 256;
@@ -124,7 +124,7 @@ __device__ d4 block_sum4(d4 v, double (*red)[33]) {
 }
 
 struct TileSmemB {
-  d4 rowsum[kTile];          // S of the rows started in this tile, four profiles
+  d4 rowsum[kTileB];         // S of the rows started in this tile, four profiles
   d4 wv[kWB];                // warp aggregates of the value scan
   int wf[kWB];
   int wn[kWB];               // warp totals of the row-flag count scan
@@ -136,7 +136,7 @@ __device__ __forceinline__ void grp_bar(int id) {
   asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(kTB) : "memory");
 }
 
-// kGB tile groups of kTB threads per CTA, one kTile-edge tile per group pass (persistent grid).
+// kGB tile groups of kTB threads per CTA, one kTileB-edge tile per group pass (its own tiling of the edge stream) (persistent grid).
 // Per tile: the gathers are issued first; while they are in flight the row-flag counts are
 // scanned (so every thread knows the local index n_ex of the first row it starts); the
 // thread's values are then folded in ONE pass -- rows that start and end inside the thread
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kTB * kGB, 1) k_tiles_b(BatchArgs A) {
   const int stride = gridDim.x * kGB;
   int k = blockIdx.x * kGB + grp;
   uint4 u = make_uint4(0, 0, 0, 0);
-  if (k < ntiles) u = ld_idx4(A.edges + (size_t)k * kTile + tid * kEB, pf);
+  if (k < ntiles) u = ld_idx4(A.edges + (size_t)k * kTileB + tid * kEB, pf);
   for (; k < ntiles; k += stride) {
     const int f0 = __ldg(A.tile_row + k);
     const int F = __ldg(A.tile_row + k + 1) - f0;
@@ -184,9 +184,9 @@ __global__ void __launch_bounds__(kTB * kGB, 1) k_tiles_b(BatchArgs A) {
       v[q] = lab < hs ? hot[lab] : ld4(xs + lab, lab < hot_lim ? pl : pf);
     }
     if (tid == 0)
-      sm.next_flag = (k + 1 >= ntiles) ? 1 : (int)(ld_idx(A.edges + (size_t)(k + 1) * kTile, pf) >> 31);
+      sm.next_flag = (k + 1 >= ntiles) ? 1 : (int)(ld_idx(A.edges + (size_t)(k + 1) * kTileB, pf) >> 31);
     const int kn = k + stride;
-    if (kn < ntiles) u = ld_idx4(A.edges + (size_t)kn * kTile + tid * kEB, pf);
+    if (kn < ntiles) u = ld_idx4(A.edges + (size_t)kn * kTileB + tid * kEB, pf);
 
     // ---- row-flag count scan (overlaps the gathers): n_ex = flags before this thread
     const int nf = __popc(fl);
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kTB * kGB, 1) k_tiles_b(BatchArgs A) {
     const int nrows = (F > 0 && !next_flag) ? F - 1 : F;
     for (int i = tid; i < nrows; i += kTB) {
       const int r = f0 + i;
-      PSI_ASSERT(r < A.n_act && i < kTile);
+      PSI_ASSERT(r < A.n_act && i < kTileB);
       const d4 S = sm.rowsum[i];
       if (READOUT) {
         const d4 dd = ld4(A.d + r, pf), lm = ld4(A.lam + r, pf);

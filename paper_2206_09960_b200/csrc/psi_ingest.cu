@@ -598,9 +598,9 @@ __global__ void k_permute_vectors(const int* old_of_new, int n, int n_act, const
 // ------------------------------------------------------------------ 7. tiles
 
 // tile_row[k] = number of rows whose first edge lies before edge k*kTile
-__global__ void k_tile_rows(const int* rp, int n_act, int ntiles, int* tile_row) {
+__global__ void k_tile_rows(const int* rp, int n_act, int ntiles, int tile, int* tile_row) {
   GRID_STRIDE(k, ntiles + 1) {
-    const long long e = k * (long long)kTile;
+    const long long e = k * (long long)tile;
     int lo = 0, hi = n_act;                 // first row r with rp[r] >= e
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -611,14 +611,14 @@ __global__ void k_tile_rows(const int* rp, int n_act, int ntiles, int* tile_row)
 }
 
 // rows whose edges fall in more than one tile
-__global__ void k_split_flags(const int* rp, int n, unsigned char* flag) {
-  GRID_STRIDE(r, n) flag[r] = (rp[r] / kTile) != ((rp[r + 1] - 1) / kTile) ? 1 : 0;
+__global__ void k_split_flags(const int* rp, int n, int tile, unsigned char* flag) {
+  GRID_STRIDE(r, n) flag[r] = (rp[r] / tile) != ((rp[r + 1] - 1) / tile) ? 1 : 0;
 }
 
-__global__ void k_split_fill(const int* rows, long long ns, const int* rp, int4* split) {
+__global__ void k_split_fill(const int* rows, long long ns, const int* rp, int tile, int4* split) {
   GRID_STRIDE(s, ns) {
     const int r = rows[s];
-    split[s] = make_int4(r, rp[r] / kTile, (rp[r + 1] - 1) / kTile, 0);
+    split[s] = make_int4(r, rp[r] / tile, (rp[r + 1] - 1) / tile, 0);
   }
 }
 
@@ -920,6 +920,56 @@ int batch_vectors(IngestOut& out, long long n, int NA, int nprof, const int* rp,
     k_permute_b<<<grid_for(n, 256), 256, 0, s>>>(out.old_of_new, n, NA, p, base, base + n,
                                                  base + 2 * n, base + 3 * n, lam + (size_t)p * n,
                                                  K.as<double>(), out);
+  }
+  IG_CK(cudaStreamSynchronize(s));
+  return PSI_OK;
+}
+
+// tile_row / split rows (long ones first) of the edge stream cut into `tile`-edge tiles
+int make_tiling(const int* rp_new, int NA, long long m_pad, int tile, cudaStream_t s, int** tile_row,
+                int4** split, int* nsplit, int* nsplit_long, char* msg, size_t msg_len) {
+  const int ntiles = (int)(m_pad / tile);
+  IG_CK(cudaMallocAsync(tile_row, (size_t)(ntiles + 1) * sizeof(int), s));
+  k_tile_rows<<<grid_for(ntiles + 1, 256), 256, 0, s>>>(rp_new, NA, ntiles, tile, *tile_row);
+  Tmp fl, rows, ns, sel_tmp;
+  IG_CK(fl.alloc((size_t)(NA > 0 ? NA : 1)));
+  IG_CK(rows.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(int)));
+  IG_CK(ns.alloc(sizeof(long long)));
+  IG_CK(cudaMemsetAsync(ns.p, 0, sizeof(long long), s));
+  long long hs = 0;
+  if (NA > 0) {
+    k_split_flags<<<grid_for(NA, 256), 256, 0, s>>>(rp_new, NA, tile, fl.as<unsigned char>());
+    cub::CountingInputIterator<int> it(0);
+    size_t tb = 0;
+    IG_CK(cub::DeviceSelect::Flagged(nullptr, tb, it, fl.as<unsigned char>(), rows.as<int>(),
+                                     ns.as<long long>(), NA, s));
+    IG_CK(sel_tmp.alloc(tb));
+    IG_CK(cub::DeviceSelect::Flagged(sel_tmp.p, tb, it, fl.as<unsigned char>(), rows.as<int>(),
+                                     ns.as<long long>(), NA, s));
+    IG_CK(cudaMemcpyAsync(&hs, ns.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+  }
+  *nsplit = (int)hs;
+  *nsplit_long = 0;
+  IG_CK(cudaMallocAsync(split, (size_t)(hs > 0 ? hs : 1) * sizeof(int4), s));
+  if (hs > 0) {
+    k_split_fill<<<grid_for(hs, 256), 256, 0, s>>>(rows.as<int>(), hs, rp_new, tile, *split);
+    // rows spanning more than kLongSpan tiles first (summed by a warp each in k_fix)
+    Tmp sp2, lf, part_tmp;
+    IG_CK(sp2.alloc((size_t)hs * sizeof(int4)));
+    IG_CK(lf.alloc((size_t)hs));
+    k_long_split_flags<<<grid_for(hs, 256), 256, 0, s>>>(*split, hs, lf.as<unsigned char>());
+    size_t pb = 0;
+    IG_CK(cub::DevicePartition::Flagged(nullptr, pb, *split, lf.as<unsigned char>(),
+                                        sp2.as<int4>(), ns.as<long long>(), (int)hs, s));
+    IG_CK(part_tmp.alloc(pb));
+    IG_CK(cub::DevicePartition::Flagged(part_tmp.p, pb, *split, lf.as<unsigned char>(),
+                                        sp2.as<int4>(), ns.as<long long>(), (int)hs, s));
+    IG_CK(cudaMemcpyAsync(*split, sp2.p, (size_t)hs * sizeof(int4), cudaMemcpyDeviceToDevice, s));
+    long long nl = 0;
+    IG_CK(cudaMemcpyAsync(&nl, ns.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+    *nsplit_long = (int)nl;
   }
   IG_CK(cudaStreamSynchronize(s));
   return PSI_OK;
@@ -1305,52 +1355,19 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   }
 
   tr.mark("vectors");
-  // ---- 7. edge tiles: first row of every tile, rows spanning tiles
-  IG_CK(cudaMallocAsync(&out.tile_row, (size_t)(out.ntiles + 1) * sizeof(int), s));
-  k_tile_rows<<<grid_for(out.ntiles + 1, 256), 256, 0, s>>>(rp_new.as<int>(), NA, out.ntiles,
-                                                            out.tile_row);
+  // ---- 7. edge tiles: first row of every tile, rows spanning tiles (and, for a batch
+  // context, the same for the batch sweep's 512-edge tiles)
   {
-    Tmp fl, rows, ns, sel_tmp;
-    IG_CK(fl.alloc((size_t)(NA > 0 ? NA : 1)));
-    IG_CK(rows.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(int)));
-    IG_CK(ns.alloc(sizeof(long long)));
-    IG_CK(cudaMemsetAsync(ns.p, 0, sizeof(long long), s));
-    long long hs = 0;
-    if (NA > 0) {
-      k_split_flags<<<grid_for(NA, 256), 256, 0, s>>>(rp_new.as<int>(), NA, fl.as<unsigned char>());
-      cub::CountingInputIterator<int> it(0);
-      size_t tb = 0;
-      IG_CK(cub::DeviceSelect::Flagged(nullptr, tb, it, fl.as<unsigned char>(), rows.as<int>(),
-                                       ns.as<long long>(), NA, s));
-      IG_CK(sel_tmp.alloc(tb));
-      IG_CK(cub::DeviceSelect::Flagged(sel_tmp.p, tb, it, fl.as<unsigned char>(), rows.as<int>(),
-                                       ns.as<long long>(), NA, s));
-      IG_CK(cudaMemcpyAsync(&hs, ns.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
-      IG_CK(cudaStreamSynchronize(s));
+    int rc4 = make_tiling(rp_new.as<int>(), NA, (long long)out.ntiles * kTile, kTile, s, &out.tile_row,
+                          &out.split, &out.nsplit, &out.nsplit_long, msg, msg_len);
+    if (rc4 != PSI_OK) return rc4;
+    if (nprof > 1) {
+      // as many tiles as hold the m_act real edge words: the last one is never all padding
+      out.b_ntiles = (int)(((long long)out.m_act + kTileB - 1) / kTileB);
+      rc4 = make_tiling(rp_new.as<int>(), NA, (long long)out.b_ntiles * kTileB, kTileB, s, &out.b_tile_row,
+                        &out.b_split, &out.b_nsplit, &out.b_nsplit_long, msg, msg_len);
+      if (rc4 != PSI_OK) return rc4;
     }
-    out.nsplit = (int)hs;
-    IG_CK(cudaMallocAsync(&out.split, (size_t)(hs > 0 ? hs : 1) * sizeof(int4), s));
-    if (hs > 0) {
-      k_split_fill<<<grid_for(hs, 256), 256, 0, s>>>(rows.as<int>(), hs, rp_new.as<int>(),
-                                                     out.split);
-      // rows spanning more than kLongSpan tiles first (summed by a warp each in k_fix)
-      Tmp sp2, lf, part_tmp;
-      IG_CK(sp2.alloc((size_t)hs * sizeof(int4)));
-      IG_CK(lf.alloc((size_t)hs));
-      k_long_split_flags<<<grid_for(hs, 256), 256, 0, s>>>(out.split, hs, lf.as<unsigned char>());
-      size_t pb = 0;
-      IG_CK(cub::DevicePartition::Flagged(nullptr, pb, out.split, lf.as<unsigned char>(),
-                                          sp2.as<int4>(), ns.as<long long>(), (int)hs, s));
-      IG_CK(part_tmp.alloc(pb));
-      IG_CK(cub::DevicePartition::Flagged(part_tmp.p, pb, out.split, lf.as<unsigned char>(),
-                                          sp2.as<int4>(), ns.as<long long>(), (int)hs, s));
-      IG_CK(cudaMemcpyAsync(out.split, sp2.p, (size_t)hs * sizeof(int4), cudaMemcpyDeviceToDevice, s));
-      long long nl = 0;
-      IG_CK(cudaMemcpyAsync(&nl, ns.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
-      IG_CK(cudaStreamSynchronize(s));
-      out.nsplit_long = (int)nl;
-    }
-    IG_CK(cudaStreamSynchronize(s));
   }
   IG_CK(cudaGetLastError());
   tr.mark("tiles");

@@ -199,6 +199,10 @@ struct IngestOut {
   // multi-profile batch (psi_build_graph_batch): nprof activity profiles on one graph, in
   // groups of kBP interleaved per user ([group][user][kBP]; unused lanes of the last group 0)
   int nprof = 1, ngroups = 0;
+  int b_ntiles = 0;           // the batch sweep's tiling: kTileB-edge tiles of the same stream
+  int* b_tile_row = nullptr;  // [b_ntiles + 1]
+  int4* b_split = nullptr;    // [b_nsplit], the b_nsplit_long long ones first
+  int b_nsplit = 0, b_nsplit_long = 0;
   double* b_a0 = nullptr;     // [ngroups][n][kBP]     x_0
   double* b_a1 = nullptr;     // [ngroups][n_act][kBP] sweep constant a + g K
   double* b_g = nullptr;      // [ngroups][n_act][kBP]
@@ -258,6 +262,7 @@ int ingest(long long n, long long m, const long long* rp64_dev, const int* idx_d
 
 // ---- multi-profile batch sweep (psi_batch.cu): kBP profiles per pass over the edge stream
 constexpr int kBP = 4;                   // profiles per group (one 32-byte x gather per edge)
+constexpr int kTileB = 512;              // edges per tile of the batch sweep (its own tiling)
 struct __align__(32) d4 { double v[kBP]; };
 
 struct LoopStateB {
