@@ -118,8 +118,11 @@ psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr,
  *
  * Runs sweeps s <- s A + c with the fused L1 residual and the stop rule
  * gap_t = ||B||_norm * epsilon_t <= eps (gap_0 = 1, Alg. 2, so eps >= 1
- * gives T = 0) entirely on the device (a CUDA-graph conditional loop: no host
- * round trip per sweep), then the readout psi = (s^T B + d^T)/N.  Also stops
+ * gives T = 0) entirely on the device (a CUDA-graph conditional loop, or for graphs
+ * with no heavy rows and at most 8.4M edge slots one persistent cooperative kernel: no
+ * host round trip per sweep; psi_info.last_solver says which), then the readout
+ * psi = (s^T B + d^T)/N.  On a batch context (psi_build_graph_batch) it runs every
+ * profile, see there.  Also stops
  * at T = max_iters.  eps = 0 runs exactly max_iters sweeps unless the fp
  * iteration reaches an exact fixed point first (gap_t == 0): the fixed-count
  * parity mode.  Blocks until T is known; psi is ready on return.
