@@ -138,7 +138,8 @@ psi_status psi_iterate(psi_ctx* ctx, double eps, int64_t max_iters, int norm,
 
 /* psi_get_psi -- copy psi[n] (fp64, the CALLER'S ORIGINAL user labels) to `out`,
  * a host (PSI_MEM_HOST) or device (PSI_MEM_DEVICE) buffer of n doubles owned by
- * the caller.  PSI_E_STATE if no psi_iterate has succeeded on this context. */
+ * the caller (k * n, profile-major, on a batch context).  PSI_E_STATE if no
+ * psi_iterate has succeeded on this context. */
 psi_status psi_get_psi(const psi_ctx* ctx, double* out, int mem_kind);
 
 /* psi_get_series -- copy s_T[n] (the paper's series iterate after the last
