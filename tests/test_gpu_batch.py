@@ -173,3 +173,15 @@ def test_batch_full_size_config5(gpu):
     assert r["Tp"][0] == T0
     assert oracle.max_rel_error(psi0, r["psi"][0]) <= 1e-12
     assert np.all(r["gp"] <= w.eps) and np.all(r["Tp"] > 10)
+
+
+def test_batch_host_inputs_equal_device_inputs(gpu):
+    """psi_build_graph_batch from host (PSI_MEM_HOST) arrays = from device arrays, bitwise."""
+    w = psigen.make_config(1)
+    lam, mu = psigen.activity_profiles(w.row_ptr.size - 1, 3, "uniform", seed=4)
+    d = batch_run(gpu, w.row_ptr, w.followers, lam, mu, 1e-12)
+    with gpu.PsiGraph(w.row_ptr, w.followers, lam, mu) as g:
+        g.iterate(1e-12)
+        h = g.get_psi(device=False).numpy()
+        Tp, _ = g.profile_stats()
+    assert np.array_equal(Tp, d["Tp"]) and np.array_equal(h, d["psi"])
