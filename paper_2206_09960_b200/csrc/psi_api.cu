@@ -303,7 +303,7 @@ psi_status iterate_direct(psi_ctx* c, bool pagerank = false) {
 // no k_heavy rows and at most PSI_COOP_TILES tiles (default kCoopTiles; 0 disables), when the
 // sweep grid is co-resident.  It pays off where a sweep is launch-bound.
 bool use_coop(const psi_ctx* c) {
-  long long lim = kCoopTiles;
+  long long lim = kCoopEdges / c->g.tile;
   if (const char* e = getenv("PSI_COOP_TILES")) lim = atoll(e);
   return c->g.n_heavy == 0 && c->tc.solve && c->g.ntiles <= lim &&
          c->grid1 <= c->tc.solve_max_grid;
@@ -702,7 +702,7 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
 
   // Iteration buffers.
-  c->tc = tiles_config(c->g.ntiles, n);
+  c->tc = tiles_config(c->g.ntiles, n, c->g.tile);
   c->grid1 = c->tc.grid;
   {
     // Hot prefix of x kept in L2 (evict_last) in BOTH ping-pong buffers: PSI_HOT_MB per
@@ -754,7 +754,7 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   float ms = 0;
   B_CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   c->ingest_ms = ms;
-  c->device_bytes = (long long)c->g.ntiles * kTile * 4 + 6 * n * 8 + 4 * c->g.n_act * 8 +
+  c->device_bytes = (long long)c->g.ntiles * c->g.tile * 4 + 6 * n * 8 + 4 * c->g.n_act * 8 +
                     (c->g.ntiles + 1) * (4 + 16) + (long long)c->g.nsplit * 16 + n * 4;
 
   psi_status gs = build_graph_exec(c);

@@ -597,7 +597,7 @@ __global__ void k_permute_vectors(const int* old_of_new, int n, int n_act, const
 
 // ------------------------------------------------------------------ 7. tiles
 
-// tile_row[k] = number of rows whose first edge lies before edge k*kTile
+// tile_row[k] = number of rows whose first edge lies before edge k*tile
 __global__ void k_tile_rows(const int* rp, int n_act, int ntiles, int tile, int* tile_row) {
   GRID_STRIDE(k, ntiles + 1) {
     const long long e = k * (long long)tile;
@@ -1305,8 +1305,15 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   IG_CK(cudaMemcpyAsync(&m_act, rp_new.as<int>() + NA, sizeof(int), cudaMemcpyDeviceToHost, s));
   IG_CK(cudaStreamSynchronize(s));
   out.m_act = m_act;
-  out.ntiles = (int)(((long long)m_act + kTile - 1) / kTile);
-  const long long m_pad = (long long)out.ntiles * kTile;
+  // 1024-edge tiles where heavy rows exist (C4/C5: the sweep's L1 holds more of x with one
+  // hot cache for 8 groups); 512-edge tiles otherwise (smaller barrier groups; C2/C3 measured,
+  // DESIGN.md §12).  PSI_TILE=512|1024 forces one.
+  {
+    const int te = env_int("PSI_TILE", 0);
+    out.tile = (te == 512 || te == 1024) ? te : (out.n_heavy > 0 ? kTile : 512);
+  }
+  out.ntiles = (int)(((long long)m_act + out.tile - 1) / out.tile);
+  const long long m_pad = (long long)out.ntiles * out.tile;
   {
     IG_CK(cudaMallocAsync(&out.edges, (size_t)(m_pad > 0 ? m_pad : 4) * sizeof(unsigned), s));
     int* ed = (int*)out.edges;
@@ -1358,7 +1365,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   // ---- 7. edge tiles: first row of every tile, rows spanning tiles (and, for a batch
   // context, the same for the batch sweep's 512-edge tiles)
   {
-    int rc4 = make_tiling(rp_new.as<int>(), NA, (long long)out.ntiles * kTile, kTile, s, &out.tile_row,
+    int rc4 = make_tiling(rp_new.as<int>(), NA, (long long)out.ntiles * out.tile, out.tile, s, &out.tile_row,
                           &out.split, &out.nsplit, &out.nsplit_long, msg, msg_len);
     if (rc4 != PSI_OK) return rc4;
     if (nprof > 1) {

@@ -65,7 +65,7 @@ constexpr int kMaxHeavySegs = 512;       // shared-memory bound of the per-warp 
 constexpr int kMinHeavyLabels = 1 << 19, kMaxHeavyLabels = 1 << 20;
 constexpr int kDefaultHeavyPPS = 1;      // heavy panels per SM (entry budget per panel)
 constexpr int kDefaultGroups = 8;        // tile groups (of kBlock threads) per sweep CTA
-constexpr long long kCoopTiles = 8192;   // k_solve up to this many tiles (8.4M edge slots; PSI_COOP_TILES)
+constexpr long long kCoopEdges = 1LL << 23;  // k_solve up to this many edge slots (PSI_COOP_TILES: tiles)
 constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA
 constexpr int kDefaultL1Hot = 16384;     // labels below this gather through L1 (evict_last)
 
@@ -150,7 +150,7 @@ struct TilesCfg {                    // launch shape of k_tiles (sweep and reado
   void* solve;                       // k_solve<groups>: the persistent small-graph solver
   int solve_max_grid;                // co-resident CTAs of k_solve (cooperative launch bound)
 };
-TilesCfg tiles_config(int ntiles, long long n);
+TilesCfg tiles_config(int ntiles, long long n, int tile);   // tile: 512 or 1024 edges
 int fix_grid(int nsplit);            // CTAs of the fix-up kernel
 void* fix_kernel_ptr(bool readout);
 void* heavy_kernel_ptr();            // psi_heavy.cu
@@ -179,6 +179,7 @@ struct IngestOut {
   double* nf_wt = nullptr;
   double2* nf_lm = nullptr;
   int ntiles = 0;
+  int tile = kTile;           // edges per tile of the single-profile sweep (512 or kTile = 1024)
   int4* split = nullptr;      // [nsplit] rows spanning tiles, the nsplit_long long ones first
   int nsplit = 0;
   int nsplit_long = 0;

@@ -94,9 +94,10 @@ __device__ __forceinline__ double ld_l1last(const double* p, unsigned long long 
                : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
-// named barrier over one kBlock-thread tile group of the CTA (id 0 is __syncthreads)
+// named barrier over one TB-thread tile group of the CTA (id 0 is __syncthreads)
+template <int TB>
 __device__ __forceinline__ void group_bar(int id) {
-  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(kBlock) : "memory");
+  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(TB) : "memory");
 }
 __device__ __forceinline__ void st_hint(double* p, double v, unsigned long long pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
@@ -125,11 +126,12 @@ __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 
+template <int TB>
 struct TileSmem {
-  double rowsum[kTile];       // S of the rows started in this tile (local row index)
-  double wv[kBlock / 32];     // warp aggregates of the segmented scan
-  int wf[kBlock / 32];
-  int wn[kBlock / 32];
+  double rowsum[TB * kEpt];       // S of the rows started in this tile (local row index)
+  double wv[TB / 32];     // warp aggregates of the segmented scan
+  int wf[TB / 32];
+  int wn[TB / 32];
   double red[33];
   int next_flag;              // does the edge after this tile start a row?
 };
@@ -146,16 +148,16 @@ __device__ __forceinline__ double ldx(const double* p, unsigned long long pol, i
   return kind == 0 ? ld_l1last(p, pol) : kind == 1 ? ld_l1first(p, pol) : ld_hint_na(p, pol);
 }
 
-template <bool READOUT, int G, bool COH>
+template <bool READOUT, int G, bool COH, int TB>
 __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* dsm, long long t,
                                            double* part1) {
-  TileSmem* smg = reinterpret_cast<TileSmem*>(dsm);
-  double* hot = reinterpret_cast<double*>(dsm + G * sizeof(TileSmem));
+  TileSmem<TB>* smg = reinterpret_cast<TileSmem<TB>*>(dsm);
+  double* hot = reinterpret_cast<double*>(dsm + G * sizeof(TileSmem<TB>));
   const double* __restrict__ xs = (t & 1) ? A.x1 : A.x0;    // x_{t-1}
   double* __restrict__ xd = (t & 1) ? A.x0 : A.x1;          // x_t
-  const int grp = G == 1 ? 0 : threadIdx.x / kBlock;
-  const int tid = threadIdx.x - grp * kBlock, lane = tid & 31, warp = tid >> 5;
-  TileSmem& sm = smg[grp];
+  const int grp = G == 1 ? 0 : threadIdx.x / TB;
+  const int tid = threadIdx.x - grp * TB, lane = tid & 31, warp = tid >> 5;
+  TileSmem<TB>& sm = smg[grp];
   const unsigned long long pf = pol_evict_first(), pl = pol_evict_last();
   const unsigned hot_lim = (unsigned)A.hot_lim;
   const unsigned hs = (unsigned)A.hot_smem;
@@ -173,7 +175,7 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
   int k = blockIdx.x * G + grp;
   uint4 u0 = make_uint4(0, 0, 0, 0), u1 = u0;
   if (k < ntiles) {
-    const unsigned* p = A.edges + (size_t)k * kTile + tid * kEpt;
+    const unsigned* p = A.edges + (size_t)k * (TB * kEpt) + tid * kEpt;
     u0 = ld_stream4(p, pf);
     u1 = ld_stream4(p + 4, pf);
   }
@@ -196,11 +198,11 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
       else v[q] = ldx<COH>(xs + lab, lab < hot_lim ? pl : pf, 2);
     }
     if (tid == 0)
-      sm.next_flag = (k + 1 >= ntiles) ? 1 : (int)(ld_stream(A.edges + (size_t)(k + 1) * kTile, pf) >> 31);
+      sm.next_flag = (k + 1 >= ntiles) ? 1 : (int)(ld_stream(A.edges + (size_t)(k + 1) * (TB * kEpt), pf) >> 31);
     // ---- prefetch the next tile's edge words
     const int kn = k + stride;
     if (kn < ntiles) {
-      const unsigned* p = A.edges + (size_t)kn * kTile + tid * kEpt;
+      const unsigned* p = A.edges + (size_t)kn * (TB * kEpt) + tid * kEpt;
       u0 = ld_stream4(p, pf);
       u1 = ld_stream4(p + 4, pf);
     }
@@ -229,7 +231,7 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
       }
     }
     if (lane == 31) { sm.wv[warp] = v_in; sm.wf[warp] = f_in; sm.wn[warp] = n_in; }
-    if (G == 1) __syncthreads(); else group_bar(1 + grp);
+    if (G == 1) __syncthreads(); else group_bar<TB>(1 + grp);
     const int next_flag = sm.next_flag;
     int nP = 0;
     double vP = 0.0;
@@ -255,18 +257,18 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
       }
       run += v[q];
     }
-    if (tid == kBlock - 1) {                         // the tile's last open row
+    if (tid == TB - 1) {                         // the tile's last open row
       if (F == 0) { A.p_in[k] = run; A.p_out[k] = 0.0; }
       else if (next_flag) { sm.rowsum[F - 1] = run; A.p_out[k] = 0.0; }
       else A.p_out[k] = run;
     }
-    if (G == 1) __syncthreads(); else group_bar(1 + grp);
+    if (G == 1) __syncthreads(); else group_bar<TB>(1 + grp);
 
     // ---- epilogue over the rows completed in this tile (coalesced)
     const int nrows = (F > 0 && !next_flag) ? F - 1 : F;
-    for (int i = tid; i < nrows; i += kBlock) {
+    for (int i = tid; i < nrows; i += TB) {
       const int r = f0 + i;
-      PSI_ASSERT(r < A.n_act && i < kTile);
+      PSI_ASSERT(r < A.n_act && i < (TB * kEpt));
       double Sr = sm.rowsum[i];
       if (r < A.n_heavy) Sr += A.hhot[r];               // followers < H (k_heavy)
       if (READOUT) {
@@ -281,15 +283,15 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
   }
 
   if (!READOUT) {
-    const double tot = block_sum<kBlock * G>(eps_acc, smg[0].red);
+    const double tot = block_sum<TB * G>(eps_acc, smg[0].red);
     if (threadIdx.x == 0) part1[blockIdx.x] = tot;
   }
 }
 
-template <bool READOUT, int G>
-__global__ void __launch_bounds__(kBlock * G, G == 1 ? 4 : (G == 2 ? 2 : 1)) k_tiles(SweepArgs A) {
+template <bool READOUT, int G, int TB>
+__global__ void __launch_bounds__(TB * G, (1024 / (TB * G)) > 0 ? 1024 / (TB * G) : 1) k_tiles(SweepArgs A) {
   extern __shared__ __align__(16) unsigned char dsm[];   // [G x TileSmem][hot cache]
-  tiles_body<READOUT, G, false>(A, dsm, A.st->iter, A.eps_part1);
+  tiles_body<READOUT, G, false, TB>(A, dsm, A.st->iter, A.eps_part1);
 }
 
 // Split rows, eps_t and the stop rule (k_fix), as a device function of any block size >= 32
@@ -402,8 +404,8 @@ __global__ void k_init(SweepArgs A, int n) {
 // launch with grid-wide barriers between the phases, instead of a CUDA-graph WHILE node with
 // two kernel launches per sweep.  Same arithmetic, same fixed-order reductions and the same
 // stop rule as k_init / k_tiles / k_fix (sweep counts and results agree with the graph path).
-template <int G>
-__global__ void __launch_bounds__(kBlock * G, 1) k_solve(SweepArgs A, int readout) {
+template <int G, int TB>
+__global__ void __launch_bounds__(TB * G, 1) k_solve(SweepArgs A, int readout) {
   extern __shared__ __align__(16) unsigned char dsm[];
   cg::grid_group grid = cg::this_grid();
   const int stride = gridDim.x * blockDim.x;
@@ -429,16 +431,16 @@ __global__ void __launch_bounds__(kBlock * G, 1) k_solve(SweepArgs A, int readou
   while (!bad && gap > P.eps && t < P.max_iters) {
     double* p1 = A.eps_part1 + (t & 1) * A.grid1;
     double* p2 = A.eps_part2 + (t & 1) * gridDim.x;
-    tiles_body<false, G, true>(A, dsm, t, p1);
+    tiles_body<false, G, true, TB>(A, dsm, t, p1);
     grid.sync();
-    fix_body<false, kBlock * G, true>(A, t, p2);
+    fix_body<false, TB * G, true>(A, t, p2);
     grid.sync();
     double v = 0.0;
     for (int q = threadIdx.x; q < A.grid1; q += blockDim.x) v += __ldcg(p1 + q);
-    const double e1 = block_sum<kBlock * G>(v, red);
+    const double e1 = block_sum<TB * G>(v, red);
     v = 0.0;
     for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) v += __ldcg(p2 + q);
-    const double e2 = block_sum<kBlock * G>(v, red);
+    const double e2 = block_sum<TB * G>(v, red);
     const double eps_t = e1 + e2 + (t == 0 ? P.eps1_extra : 0.0);
     gap = P.kappa * eps_t;
     bad = !isfinite(eps_t);
@@ -452,16 +454,16 @@ __global__ void __launch_bounds__(kBlock * G, 1) k_solve(SweepArgs A, int readou
     ++t;
   }
   if (readout) {
-    tiles_body<true, G, true>(A, dsm, t, nullptr);
+    tiles_body<true, G, true, TB>(A, dsm, t, nullptr);
     grid.sync();
-    fix_body<true, kBlock * G>(A, t, nullptr);
+    fix_body<true, TB * G>(A, t, nullptr);
   }
 }
 
 }  // namespace
 
 namespace {
-template <int G>
+template <int G, int TB>
 TilesCfg cfg_for(int ntiles, long long n, int hot_req, int l1_req) {
   int dev = 0, sms = 0, optin = 0;
   cudaGetDevice(&dev);
@@ -469,8 +471,8 @@ TilesCfg cfg_for(int ntiles, long long n, int hot_req, int l1_req) {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   TilesCfg c{};
   c.groups = G;
-  c.block = kBlock * G;
-  const size_t fixed = G * sizeof(TileSmem);
+  c.block = TB * G;
+  const size_t fixed = G * sizeof(TileSmem<TB>);
   long long hs = hot_req;
   const long long cap = ((long long)optin - (long long)fixed - 1024) / 8;
   if (hs > cap) hs = cap;
@@ -479,17 +481,17 @@ TilesCfg cfg_for(int ntiles, long long n, int hot_req, int l1_req) {
   c.hot_smem = (int)hs;
   c.l1_lim = (int)std::max<long long>(hs, std::min<long long>(l1_req, n + 1));
   c.smem = fixed + (size_t)hs * 8;
-  c.sweep = (void*)k_tiles<false, G>;
-  c.solve = (void*)k_solve<G>;
-  cudaFuncSetAttribute(k_solve<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  c.sweep = (void*)k_tiles<false, G, TB>;
+  c.solve = (void*)k_solve<G, TB>;
+  cudaFuncSetAttribute(k_solve<G, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   int occ_s = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_solve<G>, c.block, c.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_solve<G, TB>, c.block, c.smem);
   c.solve_max_grid = occ_s * sms;
-  c.readout = (void*)k_tiles<true, G>;
-  cudaFuncSetAttribute(k_tiles<false, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-  cudaFuncSetAttribute(k_tiles<true, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  c.readout = (void*)k_tiles<true, G, TB>;
+  cudaFuncSetAttribute(k_tiles<false, G, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  cudaFuncSetAttribute(k_tiles<true, G, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiles<false, G>, c.block, c.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiles<false, G, TB>, c.block, c.smem);
   if (occ < 1) occ = 1;
   long long g = (long long)sms * occ;
   if (g * G > ntiles) g = (ntiles + G - 1) / G;
@@ -504,15 +506,17 @@ int env_int(const char* name, int dflt) {
 
 // Launch shape of the sweep/readout kernel.  Defaults from the C5 measurements in
 // DESIGN.md §12; PSI_GROUPS / PSI_SMEM_HOT / PSI_L1_HOT override them (tuning only).
-TilesCfg tiles_config(int ntiles, long long n) {
-  const int G = env_int("PSI_GROUPS", kDefaultGroups);
+TilesCfg tiles_config(int ntiles, long long n, int tile) {
   const int hot = env_int("PSI_SMEM_HOT", kDefaultSmemHot);
   const int l1 = env_int("PSI_L1_HOT", kDefaultL1Hot);
+  if (tile == 512) {
+    // 15 groups of 64 threads (barrier ids 1..15): one CTA and one hot cache per SM
+    return cfg_for<15, 64>(ntiles, n, hot, l1);
+  }
+  const int G = env_int("PSI_GROUPS", kDefaultGroups);
   switch (G) {
-    case 1: return cfg_for<1>(ntiles, n, hot, l1);
-    case 2: return cfg_for<2>(ntiles, n, hot, l1);
-    case 4: return cfg_for<4>(ntiles, n, hot, l1);
-    default: return cfg_for<8>(ntiles, n, hot, l1);
+    case 4: return cfg_for<4, 128>(ntiles, n, hot, l1);
+    default: return cfg_for<8, 128>(ntiles, n, hot, l1);
   }
 }
 
