@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 using namespace psi;
@@ -113,6 +114,42 @@ struct psi_ctx {
 
 namespace {
 
+// Small pinned host blocks (loop state read-backs, per-call parameters) come from one
+// process-wide pinned slab, never returned to the OS: cudaHostAlloc / cudaFreeHost per context
+// are system calls with a device synchronisation, and they stalled builds and destroys by
+// 0.1-1 s at random on the GPU box (tools/e2e_pool_diag.py).
+constexpr size_t kPinSlot = 256;
+constexpr int kPinSlots = 4096;
+std::mutex g_pin_mu;
+unsigned char* g_pin_base = nullptr;
+std::vector<int> g_pin_free;
+
+cudaError_t pin_alloc(void** p, size_t bytes) {
+  if (bytes > kPinSlot) return cudaHostAlloc(p, bytes, cudaHostAllocDefault);
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  if (!g_pin_base) {
+    cudaError_t e = cudaHostAlloc((void**)&g_pin_base, kPinSlot * kPinSlots, cudaHostAllocDefault);
+    if (e != cudaSuccess) return e;
+    for (int i = kPinSlots - 1; i >= 0; --i) g_pin_free.push_back(i);
+  }
+  if (g_pin_free.empty()) return cudaHostAlloc(p, bytes, cudaHostAllocDefault);
+  const int i = g_pin_free.back();
+  g_pin_free.pop_back();
+  *p = g_pin_base + (size_t)i * kPinSlot;
+  return cudaSuccess;
+}
+
+void pin_free(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  unsigned char* q = (unsigned char*)p;
+  if (g_pin_base && q >= g_pin_base && q < g_pin_base + kPinSlot * kPinSlots) {
+    g_pin_free.push_back((int)((q - g_pin_base) / kPinSlot));
+    return;
+  }
+  cudaFreeHost(p);
+}
+
 void free_ctx(psi_ctx* c) {
   if (!c) return;
   if (c->exec) cudaGraphExecDestroy(c->exec);
@@ -138,10 +175,10 @@ void free_ctx(psi_ctx* c) {
                   (void*)c->g.b_wt, (void*)c->g.b_d1, (void*)c->g.b_lam, (void*)c->g.b_psi,
                   (void*)c->g.b_tile_row, (void*)c->g.b_split})
     if (p) cudaFreeAsync(p, c->stream);
-  if (c->b.h_st) cudaFreeHost(c->b.h_st);
-  if (c->b.h_prm) cudaFreeHost(c->b.h_prm);
-  if (c->h_st) cudaFreeHost(c->h_st);
-  if (c->h_prm) cudaFreeHost(c->h_prm);
+  pin_free(c->b.h_st);
+  pin_free(c->b.h_prm);
+  pin_free(c->h_st);
+  pin_free(c->h_prm);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   delete c;
@@ -473,8 +510,8 @@ psi_status batch_setup(psi_ctx* c) {
   API_CK(cudaMallocAsync((void**)&b.st, sizeof(LoopStateB), c->stream));
   API_CK(cudaMallocAsync((void**)&b.prm, sizeof(BatchParams), c->stream));
   API_CK(cudaMemsetAsync(b.st, 0, sizeof(LoopStateB), c->stream));
-  API_CK(cudaHostAlloc((void**)&b.h_st, sizeof(LoopStateB), cudaHostAllocDefault));
-  API_CK(cudaHostAlloc((void**)&b.h_prm, sizeof(BatchParams), cudaHostAllocDefault));
+  API_CK(pin_alloc((void**)&b.h_st, sizeof(LoopStateB)));
+  API_CK(pin_alloc((void**)&b.h_prm, sizeof(BatchParams)));
   const int G = c->g.ngroups;
   b.graph.assign(G, nullptr);
   b.exec.assign(G, nullptr);
@@ -718,7 +755,11 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
     // Random 8-byte gathers: ask L2 to fetch single 32-byte sectors from DRAM.
     int fetch = 32;
     if (const char* e = getenv("PSI_L2_FETCH")) fetch = atoi(e);
-    if (fetch > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)fetch);
+    static int fetch_set = -1;                        // a device-wide limit: set once
+    if (fetch > 0 && fetch != fetch_set) {
+      cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)fetch);
+      fetch_set = fetch;
+    }
   }
   c->grid2 = fix_grid(c->g.nsplit);
   if (c->g.n_heavy > 0) {
@@ -747,8 +788,8 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   // Follower-less users keep x = a0 in both buffers for ever (they are never written).
   B_CK(cudaMemcpyAsync(c->x[0], c->g.a0, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   B_CK(cudaMemcpyAsync(c->x[1], c->g.a0, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  B_CK(cudaHostAlloc(&c->h_st, sizeof(LoopState), cudaHostAllocDefault));
-  B_CK(cudaHostAlloc(&c->h_prm, sizeof(LoopParams), cudaHostAllocDefault));
+  B_CK(pin_alloc((void**)&c->h_st, sizeof(LoopState)));
+  B_CK(pin_alloc((void**)&c->h_prm, sizeof(LoopParams)));
   B_CK(cudaEventRecord(c->ev1, c->stream));
   B_CK(cudaStreamSynchronize(c->stream));
   float ms = 0;
@@ -1146,7 +1187,7 @@ psi_status power_nf_run(psi_ctx* c, const int32_t* origins, long long k, double 
     for (void* p : {(void*)w.P[0], (void*)w.P[1], (void*)w.part, (void*)w.active, (void*)d_origin,
                     (void*)d_frozen, (void*)d_iters, (void*)d_gap})
       if (p) cudaFreeAsync(p, c->stream);
-    if (w.h_active) cudaFreeHost(w.h_active);
+    pin_free(w.h_active);
   };
 #define NF_CK(call)                                                                        \
   do {                                                                                     \
@@ -1162,7 +1203,7 @@ psi_status power_nf_run(psi_ctx* c, const int32_t* origins, long long k, double 
   NF_CK(cudaMallocAsync(&w.P[1], (size_t)n * kNfK * sizeof(double), c->stream));
   NF_CK(cudaMallocAsync(&w.part, power_nf_part_elems(n) * sizeof(double), c->stream));
   NF_CK(cudaMallocAsync(&w.active, sizeof(unsigned), c->stream));
-  NF_CK(cudaHostAlloc(&w.h_active, sizeof(unsigned), cudaHostAllocDefault));
+  NF_CK(pin_alloc((void**)&w.h_active, sizeof(unsigned)));
   NF_CK(cudaMallocAsync(&d_origin, kNfK * sizeof(int), c->stream));
   NF_CK(cudaMallocAsync(&d_frozen, kNfK, c->stream));
   NF_CK(cudaMallocAsync(&d_iters, kNfK * sizeof(long long), c->stream));
