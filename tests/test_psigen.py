@@ -85,3 +85,19 @@ def test_csr_from_edges():
     assert rp.tolist() == [0, 3, 3, 4, 4] and f.tolist() == [1, 2, 3, 0]
     with pytest.raises(ValueError):
         psigen.csr_from_edges(3, [(1, 1)])
+
+
+def test_activity_profiles_seeded_and_independent():
+    """Batch profiles (row 4): seeded, profile-major (k, n), valid rates, independent draws,
+    exactly floor(0.05 n) pure posters per profile when asked, the same arrays on every call."""
+    import psigen
+    n, k = 5000, 3
+    lam, mu = psigen.activity_profiles(n, k, "lognormal", pure_posters=True)
+    assert lam.shape == mu.shape == (k, n) and lam.flags.c_contiguous
+    assert np.all(lam > 0) and np.all(mu >= 0) and np.all(lam + mu > 0)
+    assert [(mu[j] == 0).sum() for j in range(k)] == [n // 20] * k
+    assert not np.array_equal(lam[0], lam[1]) and not np.array_equal(mu[1], mu[2])
+    lam2, mu2 = psigen.activity_profiles(n, k, "lognormal", pure_posters=True)
+    assert np.array_equal(lam, lam2) and np.array_equal(mu, mu2)
+    u, v = psigen.activity_profiles(n, 2, "uniform")
+    assert u.min() >= 0.05 and u.max() <= 1.0 and v.min() >= 0.05 and v.max() <= 1.0
