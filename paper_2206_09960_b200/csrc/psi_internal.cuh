@@ -14,8 +14,8 @@
 // row order, as uint32 words: bits 0..30 = follower label, bit 31 = "first edge of a row".
 // Every active row has >= 1 word (a row whose followers were all folded away gets one
 // pseudo edge to the sentinel label n, whose x is 0), so row r is simply the r-th flag:
-// no row_ptr is read by the sweep.  The stream is padded to a multiple of kTile with
-// unflagged sentinel words.
+// no row_ptr is read by the sweep.  The stream is padded to a multiple of the tile size
+// (IngestOut::tile) with unflagged sentinel words.
 #pragma once
 
 #include <cstdint>
@@ -42,9 +42,9 @@
 
 namespace psi {
 
-constexpr int kBlock = 128;              // threads per tile group of the sweep kernel
+constexpr int kBlock = 128;              // threads per tile group of the sweep kernel (1024-edge tiles)
 constexpr int kEpt = 8;                  // edges per thread
-constexpr int kTile = kBlock * kEpt;     // 1024 edges per tile
+constexpr int kTile = kBlock * kEpt;     // 1024 edges per tile (512 for graphs without heavy rows)
 constexpr int kFixBlock = 256;           // threads per CTA of the split-row fix-up kernel
 constexpr int kLongSpan = 16;            // split rows over more tiles are summed by a warp
 constexpr unsigned kRowFlag = 0x80000000u;
@@ -103,8 +103,8 @@ struct HeavyPlan {
 
 // Everything one sweep / readout launch needs (passed by value; frozen in the graph).
 struct SweepArgs {
-  const unsigned* edges;     // flagged edge stream [ntiles * kTile]
-  const int* tile_row;       // tile_row[k] = number of row flags before edge k*kTile (k <= ntiles)
+  const unsigned* edges;     // flagged edge stream [ntiles * tile]
+  const int* tile_row;       // tile_row[k] = number of row flags before edge k*tile (k <= ntiles)
   int ntiles;
   const int4* split;         // rows spanning tiles: {row, first tile, last tile, 0}; the
   int nsplit;                // first nsplit_long span more than kLongSpan tiles (warp each)
@@ -161,7 +161,7 @@ void* init_kernel_ptr();
 // Device arrays in the NEW (relabelled) user order; active users [0, n_act) have >= 1
 // follower, follower-less users [n_act, n) never change (x = a0, psi = d/N).
 struct IngestOut {
-  unsigned* edges = nullptr;  // [ntiles*kTile] flagged edge stream (see above)
+  unsigned* edges = nullptr;  // [ntiles*tile] flagged edge stream (see above)
   int* tile_row = nullptr;    // [ntiles+1]
   double* a0 = nullptr;       // [n]     x_0 = c / Wt
   double* a1 = nullptr;       // [n_act] sweep constant a + g K (K: folded follower-less terms)

@@ -1,10 +1,13 @@
 // psi_sweep.cu -- the Power-psi sweep, fused L1 residual + stop rule, and readout (sm_100a).
 //
-// One sweep = two launches inside the CUDA-graph WHILE loop (psi_api.cu):
+// One sweep = k_heavy (psi_heavy.cu, graphs with heavy rows) + two launches inside the
+// CUDA-graph WHILE loop (psi_api.cu); small graphs run the whole loop in k_solve below:
 //
 //  k_tiles   persistent, edge-balanced gather-SpMV over the flagged edge stream
-//            (psi_internal.cuh).  Tile k = edges [k*kTile, (k+1)*kTile): every CTA does the
-//            same number of gathers whatever the power-law row lengths.  Per
+//            (psi_internal.cuh).  Tile k = edges [k*tile, (k+1)*tile), tile = 1024 (8 groups
+//            of 128 threads per CTA) or 512 (15 groups of 64; graphs without heavy rows):
+//            every group does the same number of gathers whatever the power-law row lengths
+//            (SURVEY §7).  Per
 //            tile each thread loads 8 consecutive edge words (two 128-bit loads, prefetched
 //            one tile ahead), issues 8 independent 8-byte gathers of x_{t-1}, reduces its
 //            values by the row-start flags in registers, and a block-wide segmented scan
