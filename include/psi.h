@@ -84,6 +84,7 @@ typedef struct psi_info {
                              WHILE node, 1 = persistent cooperative kernel (small graphs with no
                              heavy rows), 2 = direct launches (PSI_GRAPH=0) */
   int64_t n_profiles;     /* activity profiles of the context (1, or k of psi_build_graph_batch) */
+  int64_t tile_edges;     /* edges per tile of the sweep: 1024 with heavy rows, else 512 */
 } psi_info;
 
 /*

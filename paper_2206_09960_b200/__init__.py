@@ -63,7 +63,8 @@ class psi_info(ctypes.Structure):
                 ("block", ctypes.c_int64), ("hot_smem", ctypes.c_int64),
                 ("n_heavy", ctypes.c_int64), ("heavy_entries", ctypes.c_int64),
                 ("heavy_panels", ctypes.c_int64), ("heavy_labels", ctypes.c_int64),
-                ("last_solver", ctypes.c_int64), ("n_profiles", ctypes.c_int64)]
+                ("last_solver", ctypes.c_int64), ("n_profiles", ctypes.c_int64),
+                ("tile_edges", ctypes.c_int64)]
 
 
 _lib = None

@@ -960,6 +960,7 @@ psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
   out->heavy_labels = (int64_t)c->g.nseg * kSeg;
   out->last_solver = c->last_solver;
   out->n_profiles = c->g.nprof;
+  out->tile_edges = c->g.tile;
   return PSI_OK;
 }
 

@@ -250,9 +250,10 @@ def test_heavy_rows_parity(gpu, env, monkeypatch):
     ref, got = parity(gpu, w)
     info = got["info"]
     if env.get("PSI_HEAVY") == "0":
-        assert info["n_heavy"] == 0
+        assert info["n_heavy"] == 0 and info["tile_edges"] == 512
     else:
         assert info["n_heavy"] > 0 and info["heavy_entries"] > 0 and info["heavy_panels"] > 0
+        assert info["tile_edges"] == 1024
 
 
 def test_heavy_hub_many_slots(gpu, monkeypatch):
