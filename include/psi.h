@@ -74,7 +74,7 @@ typedef struct psi_info {
   int64_t grid;           /* persistent CTAs per sweep launch */
   int64_t device_bytes;   /* device memory held by the context */
   int64_t relabeled;      /* 1 if users were relabeled for locality at ingest */
-  int64_t block;          /* threads per sweep CTA (tile groups x 128) */
+  int64_t block;          /* threads per sweep CTA (tile groups x threads per group) */
   int64_t hot_smem;       /* hottest labels of x gathered from each CTA's shared-memory copy */
   int64_t n_heavy;        /* heavy rows (labels [0, n_heavy)) served by the staged-segment kernel */
   int64_t heavy_entries;  /* (heavy row, follower < heavy_labels) pairs summed from shared memory */
