@@ -674,18 +674,35 @@ long long long_segments(const int* off, const int* perm, int n, int thr, cudaStr
 struct Trace {
   bool on = false;
   cudaStream_t s = nullptr;
+  cudaEvent_t ev_last = nullptr;
   std::chrono::steady_clock::time_point t0, last;
   explicit Trace(cudaStream_t st) : s(st) {
     const char* e = getenv("PSI_TRACE");
     on = e && *e == '1';
     t0 = last = std::chrono::steady_clock::now();
+    if (on) {
+      cudaEventCreate(&ev_last);
+      cudaEventRecord(ev_last, s);
+    }
   }
+  ~Trace() {
+    if (ev_last) cudaEventDestroy(ev_last);
+  }
+  // host time since the last mark, and the device time between the two marks' events on the
+  // stream (a phase whose host time exceeds its device time waited on the host side)
   void mark(const char* what) {
     if (!on) return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, s);
     cudaStreamSynchronize(s);
+    float dev_ms = 0.f;
+    cudaEventElapsedTime(&dev_ms, ev_last, ev);
+    cudaEventDestroy(ev_last);
+    ev_last = ev;
     const auto now = std::chrono::steady_clock::now();
-    fprintf(stderr, "[psi ingest] %-28s %9.2f ms  (total %9.2f ms)\n", what,
-            std::chrono::duration<double, std::milli>(now - last).count(),
+    fprintf(stderr, "[psi ingest] %-28s %9.2f ms  (device %9.2f ms, total %9.2f ms)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(), dev_ms,
             std::chrono::duration<double, std::milli>(now - t0).count());
     last = now;
   }
