@@ -20,7 +20,12 @@
  *  - All device work runs on the CUDA stream given to psi_build_graph
  *    (a cudaStream_t passed as void*; NULL = the legacy default stream).
  *  - A psi_ctx is not thread-safe; separate contexts are independent.
- *  - Device memory is owned by the context and freed by psi_destroy.
+ *  - Device memory is owned by the context and freed by psi_destroy.  All of it comes from
+ *    the device's default stream-ordered pool (cudaMallocAsync); the library sets the pool to
+ *    keep freed memory reserved and reserves an ingest's working set in one block on the
+ *    first large build, so repeated builds do not re-map memory.  Environment variable
+ *    PSI_POOL_KEEP_GB caps what stays reserved (PSI_POOL_RESERVE=0 skips the reservation)
+ *    for processes that share the GPU with other allocators.
  *  - Limits: 1 <= n <= 2^31 - 1 and m <= 2^31 - 1 (int32 indices and offsets
  *    on the device).
  */
