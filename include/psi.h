@@ -20,12 +20,13 @@
  *  - All device work runs on the CUDA stream given to psi_build_graph
  *    (a cudaStream_t passed as void*; NULL = the legacy default stream).
  *  - A psi_ctx is not thread-safe; separate contexts are independent.
- *  - Device memory is owned by the context and freed by psi_destroy.  All of it comes from
- *    the device's default stream-ordered pool (cudaMallocAsync); the library sets the pool to
- *    keep freed memory reserved and reserves an ingest's working set in one block on the
- *    first large build, so repeated builds do not re-map memory.  Environment variable
- *    PSI_POOL_KEEP_GB caps what stays reserved (PSI_POOL_RESERVE=0 skips the reservation)
- *    for processes that share the GPU with other allocators.
+ *  - Device memory is owned by the context and freed by psi_destroy.  All of it is
+ *    stream-ordered and comes from a memory pool the LIBRARY owns (one per device,
+ *    cudaMemPoolCreate) -- the device's default pool, the caller's allocator and device-wide
+ *    limits are never modified.  Like PyTorch's caching allocator, the pool keeps what the
+ *    library frees for its next builds (re-mapping made repeated C5 builds 3-5x slower);
+ *    psi_empty_cache() returns it to the system (the analogue of torch.cuda.empty_cache()),
+ *    and environment variable PSI_POOL_KEEP_GB=<x> caps what a pool keeps to x GiB.
  *  - Limits: 1 <= n <= 2^31 - 1 and m <= 2^31 - 1 (int32 indices and offsets
  *    on the device).
  */
@@ -148,14 +149,21 @@ psi_status psi_iterate(psi_ctx* ctx, double eps, int64_t max_iters, int norm,
  * psi_iterate has succeeded on this context. */
 psi_status psi_get_psi(const psi_ctx* ctx, double* out, int mem_kind);
 
+/* psi_empty_cache -- return the device memory the library's pool on the CURRENT device holds
+ * but no context uses (freed temporaries and destroyed contexts) to the system; synchronises
+ * the device.  Live contexts are unaffected.  PSI_E_CUDA on a CUDA error. */
+psi_status psi_empty_cache(void);
+
 /* psi_get_series -- copy s_T[n] (the paper's series iterate after the last
  * psi_iterate, Eq. (13)-(14), original labels) to a host or device buffer. */
 psi_status psi_get_series(const psi_ctx* ctx, double* out, int mem_kind);
 
 /* psi_get_residual_history -- raw epsilon_t = ||s_t - s_{t-1}||_1 for t = 1..T
  * (Eq. (15), NOT multiplied by ||B||) of the most recent psi_iterate -- or ||pi_t - pi_{t-1}||_1
- * if psi_pagerank ran last -- into host buffer `out` of capacity `cap`; *len_out = T (the
- * copy is truncated to min(T, cap, 2^24)).  PSI_E_STATE if neither has run. */
+ * if psi_pagerank ran last -- into host buffer `out` of capacity `cap`; *len_out = the
+ * number of entries stored, min(T, 2^24) (the device keeps the first 2^24; the last iterate's
+ * T is psi_get_info's last_iters); the copy is truncated to min(*len_out, cap).
+ * PSI_E_STATE if neither has run. */
 psi_status psi_get_residual_history(const psi_ctx* ctx, double* out, int64_t cap,
                                     int64_t* len_out);
 
@@ -199,7 +207,8 @@ psi_status psi_build_graph_batch(int64_t n, int64_t m, const int64_t* row_ptr,
 psi_status psi_get_profile_stats(const psi_ctx* ctx, int64_t* iters, double* gaps);
 
 /* psi_get_profile_history -- raw epsilon_t^(p), t = 1..T_p, of profile p of a batch context
- * into host buffer `out` of capacity `cap`; *len_out = T_p.  PSI_E_STATE / PSI_E_INVALID_ARG. */
+ * into host buffer `out` of capacity `cap`; *len_out = entries stored, min(T_p, 2^22).
+ * PSI_E_STATE / PSI_E_INVALID_ARG. */
 psi_status psi_get_profile_history(const psi_ctx* ctx, int64_t profile, double* out, int64_t cap,
                                    int64_t* len_out);
 

@@ -28,7 +28,7 @@ paper's invariants (sum rule, monotonicity, contraction, bound (19)).
 No function in this package is "parity unpinned".
 """
 
-from .operator import build_operator, leader_sets, norm_of_B
+from .operator import build_operator, graph_scalars, leader_sets, norm_of_B
 from .power_psi import power_psi, PowerPsiResult
 from .nsystems import psi_nsystems
 from .exact import psi_exact, dense_A_B
@@ -37,7 +37,7 @@ from .power_nf import power_nf, psi_power_nf, PowerNFResult
 from .metrics import relative_error, max_rel_error, top_k
 
 __all__ = [
-    "build_operator", "leader_sets", "norm_of_B", "power_psi", "PowerPsiResult",
+    "build_operator", "graph_scalars", "leader_sets", "norm_of_B", "power_psi", "PowerPsiResult",
     "psi_nsystems", "psi_exact", "dense_A_B", "pagerank_power", "power_nf", "psi_power_nf",
     "PowerNFResult",
     "relative_error", "max_rel_error", "top_k",

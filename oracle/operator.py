@@ -131,6 +131,29 @@ def norm_of_B(BT, which: str = "row") -> float:
     raise ValueError(f"unknown norm {which!r}")
 
 
+def graph_scalars(op: dict) -> dict:
+    """The per-graph scalars that the ingest reports (``psi_get_info``), from the explicit
+    operator:
+
+    * ``kappa_row`` = ||B|| read as the max row sum of B (Alg. 2 line 2; reading R1),
+      ``kappa_col`` = the max column sum of B (SPEC's reading) -- both via ``norm_of_B``;
+    * ``rho_A`` = the max row sum of A, max_j sum_{i in L(j)} mu_i / W_j: the
+      contraction factor of Eq. (14)'s residual recursion, < 1 under the convergence
+      condition (P:269, reading R14);
+    * ``n_f`` = users with >= 1 follower (a non-empty row of the input CSR),
+      ``n_g`` = users with >= 1 leader (j in F(l) for some l), ``n_leaderless`` = N - n_g
+      (W_j = 0, reading R5).
+    """
+    row_ptr, followers, n = op["row_ptr"], op["followers"], op["n"]
+    BT = op.get("BT")
+    if BT is None:
+        BT = B_transpose(op)
+    n_g = int(np.count_nonzero(np.bincount(followers, minlength=n)))
+    return {"kappa_row": norm_of_B(BT, "row"), "kappa_col": norm_of_B(BT, "col"),
+            "rho_A": norm_of_B(op["AT"], "row"),
+            "n_f": int(np.count_nonzero(np.diff(row_ptr))), "n_g": n_g, "n_leaderless": n - n_g}
+
+
 def leader_sets(row_ptr, followers, n) -> list[list[int]]:
     """L(j) for every user j (small graphs only): j in F(l)  <=>  l in L(j)."""
     L: list[list[int]] = [[] for _ in range(n)]

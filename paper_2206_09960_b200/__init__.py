@@ -42,7 +42,7 @@ EXPORTED = ["psi_build_graph", "psi_iterate", "psi_get_psi", "psi_get_series",
             "psi_get_residual_history", "psi_time_sweep", "psi_get_info", "psi_pagerank",
             "psi_get_pagerank", "psi_power_nf", "psi_nsystems", "psi_build_graph_batch",
             "psi_get_profile_stats", "psi_get_profile_history", "psi_time_sweep_batch",
-            "psi_destroy", "psi_last_error"]
+            "psi_empty_cache", "psi_destroy", "psi_last_error"]
 
 
 class PsiError(RuntimeError):
@@ -103,6 +103,8 @@ def load_library(build_if_stale: bool = True):
     lib.psi_get_profile_stats.argtypes = [vp, vp, vp]
     lib.psi_get_profile_history.argtypes = [vp, i64, vp, i64, ctypes.POINTER(i64)]
     lib.psi_time_sweep_batch.argtypes = [vp, i64, ctypes.POINTER(dbl)]
+    lib.psi_empty_cache.argtypes = []
+    lib.psi_empty_cache.restype = ci
     lib.psi_destroy.argtypes = [vp]
     lib.psi_destroy.restype = None
     lib.psi_last_error.restype = ctypes.c_char_p
@@ -119,18 +121,47 @@ def _err(lib) -> str:
     return (lib.psi_last_error() or b"").decode()
 
 
-def _ptr_kind(a):
-    """(pointer, mem_kind, keepalive) for a torch tensor or numpy array."""
+_DT = {"int64": (np.int64, "torch.int64"), "int32": (np.int32, "torch.int32"),
+       "float64": (np.float64, "torch.float64")}
+
+
+def _check(a, name: str, dtype: str, shape: tuple, writable: bool = False):
+    """Validate one array argument against the C-ABI contract (include/psi.h) and return
+    (pointer, mem_kind, keepalive).  Raises TypeError / ValueError instead of casting or
+    copying: the library reads and writes exactly the bytes this pointer addresses."""
     try:
         import torch
-        if isinstance(a, torch.Tensor):
-            if not a.is_contiguous():
-                a = a.contiguous()
-            return a.data_ptr(), (PSI_MEM_DEVICE if a.is_cuda else PSI_MEM_HOST), a
+        is_t = isinstance(a, torch.Tensor)
     except ImportError:
-        pass
-    arr = np.ascontiguousarray(a)
-    return arr.ctypes.data, PSI_MEM_HOST, arr
+        is_t = False
+    if is_t:
+        if str(a.dtype) != _DT[dtype][1]:
+            raise TypeError(f"{name}: dtype {a.dtype}, expected {_DT[dtype][1]}")
+        if tuple(a.shape) != tuple(shape):
+            raise ValueError(f"{name}: shape {tuple(a.shape)}, expected {tuple(shape)}")
+        if not a.is_contiguous():
+            raise ValueError(f"{name}: tensor must be contiguous")
+        if a.is_cuda and a.device.index != torch.cuda.current_device():
+            raise ValueError(f"{name}: on {a.device}, the current device is "
+                             f"cuda:{torch.cuda.current_device()}")
+        if not a.is_cuda and a.device.type != "cpu":
+            raise ValueError(f"{name}: unsupported device {a.device}")
+        return a.data_ptr(), (PSI_MEM_DEVICE if a.is_cuda else PSI_MEM_HOST), a
+    if not isinstance(a, np.ndarray):
+        if writable:
+            raise TypeError(f"{name}: output must be a numpy array or torch tensor")
+        a = np.asarray(a)
+        if a.dtype != _DT[dtype][0] and a.size == 0:
+            a = a.astype(_DT[dtype][0])           # an empty list has no dtype of its own
+    if a.dtype != _DT[dtype][0]:
+        raise TypeError(f"{name}: dtype {a.dtype}, expected {np.dtype(_DT[dtype][0])}")
+    if a.shape != tuple(shape):
+        raise ValueError(f"{name}: shape {a.shape}, expected {tuple(shape)}")
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"{name}: array must be C-contiguous")
+    if writable and not a.flags["WRITEABLE"]:
+        raise ValueError(f"{name}: array is read-only")
+    return a.ctypes.data, PSI_MEM_HOST, a
 
 
 def _current_stream():
@@ -154,18 +185,20 @@ class PsiGraph:
         self._lib = load_library()
         self._ctx = ctypes.c_void_p()
         shape = tuple(lam.shape) if hasattr(lam, "shape") else (len(lam),)
+        if len(shape) not in (1, 2):
+            raise ValueError(f"lam: shape {shape}, expected (N,) or (k, N)")
         self.k = int(shape[0]) if len(shape) == 2 else 1
         self.batch = len(shape) == 2
-        parts = [_ptr_kind(x) for x in (row_ptr, followers, lam, mu)]
+        self.n = int(shape[-1])
+        self.m = int(len(followers))
+        parts = [_check(row_ptr, "row_ptr", "int64", (self.n + 1,)),
+                 _check(followers, "followers", "int32", (self.m,)),
+                 _check(lam, "lam", "float64", shape), _check(mu, "mu", "float64", shape)]
         kinds = {k for _, k, _ in parts}
         if len(kinds) != 1:
             raise ValueError("row_ptr, followers, lam, mu must all be host or all device")
-        self.n = int(shape[-1])
-        self.m = int(len(followers))
         self.stream = stream if stream is not None else _current_stream()
         if len(shape) == 2:
-            if tuple(mu.shape) != shape:
-                raise ValueError("lam and mu must have the same (k, N) shape")
             st = self._lib.psi_build_graph_batch(self.n, self.m, parts[0][0], parts[1][0], self.k,
                                                  parts[2][0], parts[3][0], kinds.pop(),
                                                  self.stream, ctypes.byref(self._ctx))
@@ -187,12 +220,13 @@ class PsiGraph:
             raise PsiError(st, _err(self._lib))
         return st, T.value, gap.value
 
-    def _get(self, fn, out, device):
+    def _get(self, fn, out, device, shape=None):
         import torch
+        shape = (self.n,) if shape is None else shape
         if out is None:
-            out = torch.empty(self.n, dtype=torch.float64,
+            out = torch.empty(shape, dtype=torch.float64,
                               device="cuda" if device else "cpu")
-        ptr, kind, keep = _ptr_kind(out)
+        ptr, kind, keep = _check(out, "out", "float64", shape, writable=True)
         st = fn(self._ctx, ptr, kind)
         if st != PSI_OK:
             raise PsiError(st, _err(self._lib))
@@ -200,11 +234,8 @@ class PsiGraph:
 
     def get_psi(self, out=None, device: bool = True):
         """psi[n] in the caller's original labels (torch.float64); (k, n) on a batch context."""
-        if self.batch and out is None:
-            import torch
-            out = torch.empty((self.k, self.n), dtype=torch.float64,
-                              device="cuda" if device else "cpu")
-        return self._get(self._lib.psi_get_psi, out, device)
+        return self._get(self._lib.psi_get_psi, out, device,
+                         (self.k, self.n) if self.batch else None)
 
     def profile_stats(self):
         """Batch context: (T[k], gap[k]) numpy arrays of the last iterate()."""
@@ -327,6 +358,15 @@ class PsiGraph:
 
     def __exit__(self, *exc):
         self.close()
+
+
+def empty_cache() -> None:
+    """Return the device memory the library's pool (current device) caches but no context uses
+    (psi_empty_cache; the analogue of torch.cuda.empty_cache())."""
+    lib = load_library()
+    st = lib.psi_empty_cache()
+    if st != PSI_OK:
+        raise PsiError(st, _err(lib))
 
 
 def psi_scores(row_ptr, followers, lam, mu, eps=1e-9, max_iters=100_000, norm="row"):

@@ -13,6 +13,8 @@
 #include "psi_internal.cuh"
 #include "../../include/psi.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -28,6 +30,13 @@ using namespace psi;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range around every public call (ingest / iterate / readout phases in a profiler
+// timeline; free when no tool is attached -- NVTX v3 is header-only)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 psi_status fail(psi_status code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 psi_status fail(psi_status code, const char* fmt, ...) {
@@ -52,6 +61,7 @@ psi_status fail(psi_status code, const char* fmt, ...) {
 
 struct psi_ctx {
   long long n = 0, m = 0;
+  int dev = -1;                  // device of the context (its memory pool)
   cudaStream_t stream = nullptr;
   IngestOut g;
   double* x[2] = {nullptr, nullptr};
@@ -148,6 +158,38 @@ void pin_free(void* p) {
     return;
   }
   cudaFreeHost(p);
+}
+
+// ---- the library's device memory pools (psi_internal.cuh): one per device, created on first
+// use.  Like PyTorch's caching allocator, a pool keeps the memory the library frees for its
+// next allocations (re-mapping freed memory made C5 builds 3-5x slower: 1.3-2.8 s instead of
+// 0.43 s, measured); psi_empty_cache() returns it to the system, and PSI_POOL_KEEP_GB=<x>
+// caps what a pool keeps (its release threshold).  The device's default pool, the caller's
+// allocator and device-wide limits are never touched.
+constexpr int kMaxDevices = 64;
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[kMaxDevices] = {};
+unsigned long long g_reserved_for[kMaxDevices] = {};
+
+unsigned long long pool_keep_bytes() {
+  const char* e = getenv("PSI_POOL_KEEP_GB");
+  return e && *e ? (unsigned long long)(atof(e) * (double)(1ull << 30)) : ~0ull;
+}
+
+// Reserve a build's working set in ONE block of the pool the first time a graph this large
+// is built on the device: later builds carve their temporaries out of it instead of mapping
+// new memory around fragments (measured: +0.2-0.6 s C5 builds without it).
+void pool_reserve(int dev, unsigned long long est, cudaStream_t s) {
+  if (dev < 0 || dev >= kMaxDevices || pool_keep_bytes() != ~0ull) return;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool[dev] || est <= g_reserved_for[dev]) return;
+  cudaMemPoolTrimTo(g_pool[dev], 0);
+  void* p = nullptr;
+  if (cudaMallocFromPoolAsync(&p, est, g_pool[dev], s) == cudaSuccess) {
+    cudaFreeAsync(p, s);
+    g_reserved_for[dev] = est;
+  }
+  cudaGetLastError();
 }
 
 void free_ctx(psi_ctx* c) {
@@ -373,7 +415,7 @@ psi_status ensure_history(psi_ctx* c, long long need) {
     c->history = nullptr;
   }
   long long cap = need < 1024 ? 1024 : need;
-  API_CK(cudaMallocAsync(&c->history, cap * sizeof(double), c->stream));
+  API_CK(dev_alloc(&c->history, cap * sizeof(double), c->stream));
   c->hist_cap = cap;
   c->device_bytes += cap * sizeof(double);
   return PSI_OK;
@@ -400,7 +442,7 @@ psi_status copy_out(const psi_ctx* c, const double* src, const double* scale, do
   double* dst = out;
   double* tmp = nullptr;
   if (mem_kind == PSI_MEM_HOST) {
-    API_CK(cudaMallocAsync((void**)&tmp, c->n * sizeof(double), c->stream));
+    API_CK(dev_alloc((void**)&tmp, c->n * sizeof(double), c->stream));
     dst = tmp;
   }
   int grid = (int)std::min<long long>((c->n + 255) / 256, 148LL * 16);
@@ -499,16 +541,16 @@ psi_status batch_setup(psi_ctx* c) {
   double hot_frac = 0.65;                              // as the single-profile hot prefix
   if (const char* e = getenv("PSI_BATCH_HOT_FRAC")) hot_frac = atof(e);
   b.hot_lim = std::min<long long>((long long)(l2 * hot_frac / sizeof(d4)), c->g.n_hot);
-  API_CK(cudaMallocAsync((void**)&b.x[0], (n + 1) * sizeof(d4), c->stream));
-  API_CK(cudaMallocAsync((void**)&b.x[1], (n + 1) * sizeof(d4), c->stream));
+  API_CK(dev_alloc((void**)&b.x[0], (n + 1) * sizeof(d4), c->stream));
+  API_CK(dev_alloc((void**)&b.x[1], (n + 1) * sizeof(d4), c->stream));
   API_CK(cudaMemsetAsync(b.x[0] + n, 0, sizeof(d4), c->stream));      // sentinel x[n] = 0
   API_CK(cudaMemsetAsync(b.x[1] + n, 0, sizeof(d4), c->stream));
-  API_CK(cudaMallocAsync((void**)&b.p_in, (c->g.b_ntiles + 1) * sizeof(d4), c->stream));
-  API_CK(cudaMallocAsync((void**)&b.p_out, (c->g.b_ntiles + 1) * sizeof(d4), c->stream));
-  API_CK(cudaMallocAsync((void**)&b.part1, b.cfg.grid1 * sizeof(d4), c->stream));
-  API_CK(cudaMallocAsync((void**)&b.part2, b.cfg.grid2 * sizeof(d4), c->stream));
-  API_CK(cudaMallocAsync((void**)&b.st, sizeof(LoopStateB), c->stream));
-  API_CK(cudaMallocAsync((void**)&b.prm, sizeof(BatchParams), c->stream));
+  API_CK(dev_alloc((void**)&b.p_in, (c->g.b_ntiles + 1) * sizeof(d4), c->stream));
+  API_CK(dev_alloc((void**)&b.p_out, (c->g.b_ntiles + 1) * sizeof(d4), c->stream));
+  API_CK(dev_alloc((void**)&b.part1, b.cfg.grid1 * sizeof(d4), c->stream));
+  API_CK(dev_alloc((void**)&b.part2, b.cfg.grid2 * sizeof(d4), c->stream));
+  API_CK(dev_alloc((void**)&b.st, sizeof(LoopStateB), c->stream));
+  API_CK(dev_alloc((void**)&b.prm, sizeof(BatchParams), c->stream));
   API_CK(cudaMemsetAsync(b.st, 0, sizeof(LoopStateB), c->stream));
   API_CK(pin_alloc((void**)&b.h_st, sizeof(LoopStateB)));
   API_CK(pin_alloc((void**)&b.h_prm, sizeof(BatchParams)));
@@ -536,7 +578,7 @@ psi_status batch_iterate(psi_ctx* c, double eps, long long max_iters, int norm, 
   if (!b.history || b.hist_cap < need) {
     if (b.history) API_CK(cudaFreeAsync(b.history, c->stream));
     b.hist_cap = std::max<long long>(need, 1024);
-    API_CK(cudaMallocAsync((void**)&b.history, b.hist_cap * kBP * sizeof(double), c->stream));
+    API_CK(dev_alloc((void**)&b.history, b.hist_cap * kBP * sizeof(double), c->stream));
   }
   b.T.assign(P, 0);
   b.gap.assign(P, 1.0);
@@ -622,7 +664,7 @@ psi_status batch_copy_out(const psi_ctx* c, double* out, int mem_kind) {
   double* dst = out;
   double* tmp = nullptr;
   if (mem_kind == PSI_MEM_HOST) {
-    API_CK(cudaMallocAsync((void**)&tmp, bytes, c->stream));
+    API_CK(dev_alloc((void**)&tmp, bytes, c->stream));
     dst = tmp;
   }
   API_CK(batch_unpermute(c->g.b_psi, c->g.old_of_new, c->n, c->g.nprof, dst, c->stream));
@@ -636,9 +678,40 @@ psi_status batch_copy_out(const psi_ctx* c, double* out, int mem_kind) {
 
 }  // namespace
 
+cudaMemPool_t psi::lib_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
+    unsigned long long keep = pool_keep_bytes();       // default: keep everything (cached)
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    g_pool[dev] = p;
+  }
+  return g_pool[dev];
+}
+
 extern "C" {
 
 const char* psi_last_error(void) { return g_err.c_str(); }
+
+psi_status psi_empty_cache(void) {
+  g_err.clear();
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+    return fail(PSI_E_CUDA, "cudaGetDevice failed");
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool[dev]) return PSI_OK;
+  API_CK(cudaDeviceSynchronize());                    // stream-ordered frees have completed
+  API_CK(cudaMemPoolTrimTo(g_pool[dev], 0));
+  g_reserved_for[dev] = 0;
+  return PSI_OK;
+}
 
 }  // extern "C"
 
@@ -658,40 +731,16 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
     return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
 
-  {
-    // every device buffer is stream-ordered (cudaMallocAsync from the device's default pool);
-    // the pool keeps freed memory reserved (release threshold: unlimited) so build / destroy
-    // cycles reuse it instead of re-mapping it.  PSI_POOL_KEEP_GB caps what stays reserved.
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      unsigned long long keep = ~0ull;
-      if (const char* e = getenv("PSI_POOL_KEEP_GB")) keep = (unsigned long long)atoll(e) << 30;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      // Reserve the ingest's working set in ONE block the first time a graph this large is
-      // built: later builds carve their temporaries out of it instead of mapping new memory
-      // when the pool is fragmented (measured: +0.2-0.6 s builds at C5 without it).
-      // PSI_POOL_RESERVE=0 disables.
-      static unsigned long long reserved_for = 0;
-      const unsigned long long est = 16ull * (unsigned long long)m +
-                                     (unsigned long long)nprof * 160ull * (unsigned long long)n +
-                                     (256ull << 20);
-      const char* rv = getenv("PSI_POOL_RESERVE");
-      if (!(rv && rv[0] == '0') && est > reserved_for && keep == ~0ull) {
-        cudaMemPoolTrimTo(pool, 0);
-        void* p = nullptr;
-        if (cudaMallocAsync(&p, est, (cudaStream_t)stream) == cudaSuccess) {
-          cudaFreeAsync(p, (cudaStream_t)stream);
-          reserved_for = est;
-        }
-        cudaGetLastError();
-      }
-    }
-  }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(PSI_E_CUDA, "cudaGetDevice failed");
+  if (!lib_pool()) return fail(PSI_E_CUDA, "cannot create the library's memory pool");
   psi_ctx* c = new psi_ctx;
   c->n = n;
   c->m = m;
+  c->dev = dev;
   c->stream = (cudaStream_t)stream;
+  pool_reserve(dev, 16ull * (unsigned long long)m + (unsigned long long)nprof * 160ull *
+                        (unsigned long long)n + (256ull << 20), c->stream);
   auto bail = [&](psi_status st) { free_ctx(c); return st; };
 #define B_CK(call)                                                                          \
   do {                                                                                      \
@@ -717,10 +766,10 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
     ~Free4() { for (int i = 0; i < 4; ++i) if (p[i]) cudaFreeAsync(p[i], s); }
   } f4{staged, c->stream};
   if (mem_kind == PSI_MEM_HOST) {
-    B_CK(cudaMallocAsync(&staged[0], (n + 1) * sizeof(long long), c->stream));
-    B_CK(cudaMallocAsync(&staged[1], (m > 0 ? m : 1) * sizeof(int), c->stream));
-    B_CK(cudaMallocAsync(&staged[2], nprof * n * sizeof(double), c->stream));
-    B_CK(cudaMallocAsync(&staged[3], nprof * n * sizeof(double), c->stream));
+    B_CK(dev_alloc(&staged[0], (n + 1) * sizeof(long long), c->stream));
+    B_CK(dev_alloc(&staged[1], (m > 0 ? m : 1) * sizeof(int), c->stream));
+    B_CK(dev_alloc(&staged[2], nprof * n * sizeof(double), c->stream));
+    B_CK(dev_alloc(&staged[3], nprof * n * sizeof(double), c->stream));
     B_CK(cudaMemcpyAsync(staged[0], row_ptr, (n + 1) * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
     if (m > 0)
       B_CK(cudaMemcpyAsync(staged[1], followers, m * sizeof(int), cudaMemcpyHostToDevice, c->stream));
@@ -752,14 +801,10 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
     if (const char* e = getenv("PSI_HOT_MB")) hot_mb = atof(e);
     long long lim = (long long)(hot_mb * (1 << 20) / 8.0);
     c->hot_lim = std::min<long long>(std::max<long long>(lim, 0), c->g.n_hot);
-    // Random 8-byte gathers: ask L2 to fetch single 32-byte sectors from DRAM.
-    int fetch = 32;
-    if (const char* e = getenv("PSI_L2_FETCH")) fetch = atoi(e);
-    static int fetch_set = -1;                        // a device-wide limit: set once
-    if (fetch > 0 && fetch != fetch_set) {
-      cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)fetch);
-      fetch_set = fetch;
-    }
+    // cudaLimitMaxL2FetchGranularity is device-wide state: never changed by default (it made
+    // no measurable difference); PSI_L2_FETCH=<bytes> opts in (tuning only).
+    if (const char* e = getenv("PSI_L2_FETCH"))
+      if (atoi(e) > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
   }
   c->grid2 = fix_grid(c->g.nsplit);
   if (c->g.n_heavy > 0) {
@@ -770,20 +815,20 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
     c->heavy_smem = heavy_smem_bytes(c->g.nseg);
     B_CK(cudaFuncSetAttribute(heavy_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)c->heavy_smem));
-    B_CK(cudaMallocAsync(&c->hhot, (size_t)c->g.n_heavy * sizeof(double), c->stream));
+    B_CK(dev_alloc(&c->hhot, (size_t)c->g.n_heavy * sizeof(double), c->stream));
     B_CK(cudaMemsetAsync(c->hhot, 0, (size_t)c->g.n_heavy * sizeof(double), c->stream));
   }
-  B_CK(cudaMallocAsync(&c->x[0], (n + 1) * sizeof(double), c->stream));      // + sentinel x[n] = 0
-  B_CK(cudaMallocAsync(&c->x[1], (n + 1) * sizeof(double), c->stream));
+  B_CK(dev_alloc(&c->x[0], (n + 1) * sizeof(double), c->stream));      // + sentinel x[n] = 0
+  B_CK(dev_alloc(&c->x[1], (n + 1) * sizeof(double), c->stream));
   B_CK(cudaMemsetAsync(c->x[0] + n, 0, sizeof(double), c->stream));
   B_CK(cudaMemsetAsync(c->x[1] + n, 0, sizeof(double), c->stream));
-  B_CK(cudaMallocAsync(&c->p_in, (c->g.ntiles + 1) * sizeof(double), c->stream));
-  B_CK(cudaMallocAsync(&c->p_out, (c->g.ntiles + 1) * sizeof(double), c->stream));
+  B_CK(dev_alloc(&c->p_in, (c->g.ntiles + 1) * sizeof(double), c->stream));
+  B_CK(dev_alloc(&c->p_out, (c->g.ntiles + 1) * sizeof(double), c->stream));
   // x 2: k_solve double-buffers the partials by the parity of t
-  B_CK(cudaMallocAsync(&c->eps_part1, 2 * c->grid1 * sizeof(double), c->stream));
-  B_CK(cudaMallocAsync(&c->eps_part2, 2 * std::max(c->grid1, c->grid2) * sizeof(double), c->stream));
-  B_CK(cudaMallocAsync(&c->st, sizeof(LoopState), c->stream));
-  B_CK(cudaMallocAsync(&c->prm, sizeof(LoopParams), c->stream));
+  B_CK(dev_alloc(&c->eps_part1, 2 * c->grid1 * sizeof(double), c->stream));
+  B_CK(dev_alloc(&c->eps_part2, 2 * std::max(c->grid1, c->grid2) * sizeof(double), c->stream));
+  B_CK(dev_alloc(&c->st, sizeof(LoopState), c->stream));
+  B_CK(dev_alloc(&c->prm, sizeof(LoopParams), c->stream));
   B_CK(cudaMemsetAsync(c->st, 0, sizeof(LoopState), c->stream));
   // Follower-less users keep x = a0 in both buffers for ever (they are never written).
   B_CK(cudaMemcpyAsync(c->x[0], c->g.a0, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
@@ -815,12 +860,14 @@ extern "C" {
 psi_status psi_build_graph(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* followers,
                            const double* lambda, const double* mu, int mem_kind, void* stream,
                            psi_ctx** out) {
+  NvtxRange nvtx_("psi_build_graph");
   return build(n, m, row_ptr, followers, lambda, mu, 1, mem_kind, stream, out);
 }
 
 psi_status psi_build_graph_batch(int64_t n, int64_t m, const int64_t* row_ptr,
                                  const int32_t* followers, int64_t nprof, const double* lambda,
                                  const double* mu, int mem_kind, void* stream, psi_ctx** out) {
+  NvtxRange nvtx_("psi_build_graph_batch");
   g_err.clear();
   if (nprof < 1 || nprof > 4096) {
     if (out) *out = nullptr;
@@ -835,6 +882,7 @@ psi_status psi_build_graph_batch(int64_t n, int64_t m, const int64_t* row_ptr,
 
 psi_status psi_iterate(psi_ctx* c, double eps, int64_t max_iters, int norm, int64_t* iters_out,
                        double* last_gap_out) {
+  NvtxRange nvtx_("psi_iterate");
   g_err.clear();
   if (!c) return fail(PSI_E_INVALID_ARG, "ctx is NULL");
   if (!(eps >= 0.0)) return fail(PSI_E_INVALID_ARG, "eps must be >= 0 (got %g)", eps);
@@ -893,6 +941,7 @@ psi_status psi_iterate(psi_ctx* c, double eps, int64_t max_iters, int norm, int6
 }
 
 psi_status psi_get_psi(const psi_ctx* c, double* out, int mem_kind) {
+  NvtxRange nvtx_("psi_get_psi");
   g_err.clear();
   if (!c || !out) return fail(PSI_E_INVALID_ARG, "NULL argument");
   if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
@@ -903,6 +952,7 @@ psi_status psi_get_psi(const psi_ctx* c, double* out, int mem_kind) {
 }
 
 psi_status psi_get_series(const psi_ctx* c, double* out, int mem_kind) {
+  NvtxRange nvtx_("psi_get_series");
   g_err.clear();
   if (!c || !out) return fail(PSI_E_INVALID_ARG, "NULL argument");
   if (mem_kind != PSI_MEM_HOST && mem_kind != PSI_MEM_DEVICE)
@@ -920,10 +970,12 @@ psi_status psi_get_residual_history(const psi_ctx* c, double* out, int64_t cap, 
     return fail(PSI_E_STATE, "no successful psi_iterate / psi_pagerank on this context");
   if (c->g.nprof > 1 && c->b.have)
     return fail(PSI_E_STATE, "batch context: use psi_get_profile_history");
-  if (len_out) *len_out = c->last_T;
-  long long k = c->last_T;
+  // entries stored: T, or the history cap if T exceeded it (2^24); len_out never counts
+  // entries that were not written
+  const long long stored = std::min<long long>(c->last_T, c->hist_cap);
+  if (len_out) *len_out = stored;
+  long long k = stored;
   if (k > cap) k = cap;
-  if (k > c->hist_cap) k = c->hist_cap;
   if (k > 0) {
     API_CK(cudaMemcpyAsync(out, c->history, k * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     API_CK(cudaStreamSynchronize(c->stream));
@@ -966,6 +1018,7 @@ psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
 
 psi_status psi_time_sweep(psi_ctx* c, int64_t sweeps, double* heavy_ms, double* tiles_ms,
                           double* fix_ms) {
+  NvtxRange nvtx_("psi_time_sweep");
   g_err.clear();
   if (!c || sweeps < 1) return fail(PSI_E_INVALID_ARG, "ctx NULL or sweeps < 1");
   psi_status hs = ensure_history(c, sweeps);
@@ -1020,6 +1073,7 @@ psi_status psi_time_sweep(psi_ctx* c, int64_t sweeps, double* heavy_ms, double* 
 
 psi_status psi_pagerank(psi_ctx* c, double alpha, double eps, int64_t max_iters,
                         int64_t* iters_out, double* last_gap_out) {
+  NvtxRange nvtx_("psi_pagerank");
   g_err.clear();
   if (!c) return fail(PSI_E_INVALID_ARG, "ctx is NULL");
   if (!(alpha >= 0.0 && alpha < 1.0)) return fail(PSI_E_INVALID_ARG, "alpha must be in [0, 1)");
@@ -1027,12 +1081,12 @@ psi_status psi_pagerank(psi_ctx* c, double alpha, double eps, int64_t max_iters,
   if (max_iters < 0) return fail(PSI_E_INVALID_ARG, "max_iters must be >= 0");
   const long long n = c->n, na = std::max<long long>(c->g.n_act, 1);
   if (!c->pr.a) {
-    API_CK(cudaMallocAsync(&c->pr.a, na * sizeof(double), c->stream));
-    API_CK(cudaMallocAsync(&c->pr.a_first, na * sizeof(double), c->stream));
-    API_CK(cudaMallocAsync(&c->pr.g, na * sizeof(double), c->stream));
-    API_CK(cudaMallocAsync(&c->pr.dt, n * sizeof(double), c->stream));
-    API_CK(cudaMallocAsync(&c->pr.x0, n * sizeof(double), c->stream));
-    API_CK(cudaMallocAsync(&c->pr.pi, n * sizeof(double), c->stream));
+    API_CK(dev_alloc(&c->pr.a, na * sizeof(double), c->stream));
+    API_CK(dev_alloc(&c->pr.a_first, na * sizeof(double), c->stream));
+    API_CK(dev_alloc(&c->pr.g, na * sizeof(double), c->stream));
+    API_CK(dev_alloc(&c->pr.dt, n * sizeof(double), c->stream));
+    API_CK(dev_alloc(&c->pr.x0, n * sizeof(double), c->stream));
+    API_CK(dev_alloc(&c->pr.pi, n * sizeof(double), c->stream));
     c->device_bytes += (3 * na + 3 * n) * sizeof(double);
   }
   c->have_pr = false;
@@ -1109,7 +1163,7 @@ psi_status psi_get_profile_history(const psi_ctx* c, int64_t profile, double* ou
   if (!c->b.have) return fail(PSI_E_STATE, "no successful psi_iterate on this batch context");
   if (profile < 0 || profile >= c->g.nprof) return fail(PSI_E_INVALID_ARG, "bad profile %lld", (long long)profile);
   const auto& h = c->b.hist[profile];
-  if (len_out) *len_out = c->b.T[profile];
+  if (len_out) *len_out = (int64_t)h.size();     // min(T_p, history cap): only stored entries
   const long long k = std::min<long long>(cap, (long long)h.size());
   for (long long t = 0; t < k; ++t) out[t] = h[t];
   return PSI_OK;
@@ -1124,7 +1178,7 @@ psi_status psi_time_sweep_batch(psi_ctx* c, int64_t sweeps, double* sweep_ms) {
   if (!b.history || b.hist_cap < sweeps) {
     if (b.history) API_CK(cudaFreeAsync(b.history, c->stream));
     b.hist_cap = std::max<long long>(sweeps, 1024);
-    API_CK(cudaMallocAsync((void**)&b.history, b.hist_cap * kBP * sizeof(double), c->stream));
+    API_CK(dev_alloc((void**)&b.history, b.hist_cap * kBP * sizeof(double), c->stream));
   }
   hp.eps = 0.0;
   hp.max_iters = sweeps;
@@ -1200,15 +1254,15 @@ psi_status power_nf_run(psi_ctx* c, const int32_t* origins, long long k, double 
       return rc;                                                                           \
     }                                                                                      \
   } while (0)
-  NF_CK(cudaMallocAsync(&w.P[0], (size_t)n * kNfK * sizeof(double), c->stream));
-  NF_CK(cudaMallocAsync(&w.P[1], (size_t)n * kNfK * sizeof(double), c->stream));
-  NF_CK(cudaMallocAsync(&w.part, power_nf_part_elems(n) * sizeof(double), c->stream));
-  NF_CK(cudaMallocAsync(&w.active, sizeof(unsigned), c->stream));
+  NF_CK(dev_alloc(&w.P[0], (size_t)n * kNfK * sizeof(double), c->stream));
+  NF_CK(dev_alloc(&w.P[1], (size_t)n * kNfK * sizeof(double), c->stream));
+  NF_CK(dev_alloc(&w.part, power_nf_part_elems(n) * sizeof(double), c->stream));
+  NF_CK(dev_alloc(&w.active, sizeof(unsigned), c->stream));
   NF_CK(pin_alloc((void**)&w.h_active, sizeof(unsigned)));
-  NF_CK(cudaMallocAsync(&d_origin, kNfK * sizeof(int), c->stream));
-  NF_CK(cudaMallocAsync(&d_frozen, kNfK, c->stream));
-  NF_CK(cudaMallocAsync(&d_iters, kNfK * sizeof(long long), c->stream));
-  NF_CK(cudaMallocAsync(&d_gap, kNfK * sizeof(double), c->stream));
+  NF_CK(dev_alloc(&d_origin, kNfK * sizeof(int), c->stream));
+  NF_CK(dev_alloc(&d_frozen, kNfK, c->stream));
+  NF_CK(dev_alloc(&d_iters, kNfK * sizeof(long long), c->stream));
+  NF_CK(dev_alloc(&d_gap, kNfK * sizeof(double), c->stream));
   a.n = n;
   a.loff = c->g.nf_loff;
   a.leaders = c->g.nf_leaders;
@@ -1244,7 +1298,9 @@ psi_status power_nf_run(psi_ctx* c, const int32_t* origins, long long k, double 
     for (int j = 0; j < kb; ++j) {
       if (iters) iters[b0 + j] = h_iters[j];
       sweeps += h_iters[j];
-      if (h_iters[j] >= max_iters && h_iters[j] > 0 && h_gap[j] > eps) *all_converged = false;
+      // Alg. 1 left by the max_iters cap with gap > eps (gap_0 = 1: max_iters = 0 and
+      // eps < 1 is "not converged", as psi_iterate reports it)
+      if (h_iters[j] >= max_iters && h_gap[j] > eps) *all_converged = false;
     }
   }
 #undef NF_CK
@@ -1280,8 +1336,8 @@ psi_status psi_power_nf(psi_ctx* c, const int32_t* origins, int64_t k, double ep
   double *p_dev = p_out, *q_dev = q_out;
   if (mem_kind == PSI_MEM_HOST) {
     p_dev = q_dev = nullptr;
-    if (p_out) API_CK(cudaMallocAsync(&p_dev, bytes, c->stream));
-    if (q_out && cudaMallocAsync(&q_dev, bytes, c->stream) != cudaSuccess) {
+    if (p_out) API_CK(dev_alloc(&p_dev, bytes, c->stream));
+    if (q_out && dev_alloc(&q_dev, bytes, c->stream) != cudaSuccess) {
       if (p_dev) cudaFreeAsync(p_dev, c->stream);
       return fail(PSI_E_OOM, "cudaMalloc of the q columns failed");
     }
@@ -1318,7 +1374,7 @@ psi_status psi_nsystems(psi_ctx* c, double eps, int64_t max_iters, double* psi_o
     return fail(PSI_E_INVALID_ARG, "bad mem_kind %d", mem_kind);
   const long long n = c->n;
   double* psi_dev = psi_out;
-  if (mem_kind == PSI_MEM_HOST) API_CK(cudaMallocAsync(&psi_dev, (size_t)n * sizeof(double), c->stream));
+  if (mem_kind == PSI_MEM_HOST) API_CK(dev_alloc(&psi_dev, (size_t)n * sizeof(double), c->stream));
   std::vector<int32_t> all(n);
   for (long long i = 0; i < n; ++i) all[i] = (int32_t)i;
   bool conv = true;

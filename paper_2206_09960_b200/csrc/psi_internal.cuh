@@ -69,6 +69,17 @@ constexpr long long kCoopEdges = 1LL << 23;  // k_solve up to this many edge slo
 constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA
 constexpr int kDefaultL1Hot = 16384;     // labels below this gather through L1 (evict_last)
 
+// Device memory: every allocation of the library is stream-ordered and comes from a memory
+// pool the library owns (one per device, psi_api.cu) -- never the device's default pool, so
+// the caller's allocator (e.g. PyTorch's) is unaffected.  Memory the library frees returns to
+// the system when the last context on the device is destroyed (PSI_POOL_KEEP_GB keeps that
+// much reserved for later builds).
+cudaMemPool_t lib_pool();
+template <class T>
+inline cudaError_t dev_alloc(T** p, size_t bytes, cudaStream_t s) {
+  return cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, lib_pool(), s);
+}
+
 // Device-resident loop state (written by kernels, read back by the host once per iterate).
 struct LoopState {
   long long iter;        // completed sweeps t

@@ -65,7 +65,8 @@ __global__ void k_nf_finish(NfArgs a, const double* part, int nblocks, int init,
   bool fr = a.frozen[c] != 0;
   if (init) {
     a.iters[c] = 0;
-    fr = fr || !(1.0 > eps && max_iters > 0);           // gap_0 = 1 (Alg. 1 line 3)
+    a.gap[c] = 1.0;                                     // gap_0 = 1 (Alg. 1 line 3)
+    fr = fr || !(1.0 > eps && max_iters > 0);
   } else if (!fr) {
     a.iters[c] += 1;
     a.gap[c] = gap;

@@ -66,3 +66,19 @@ def test_reference_arm_under_torchrun_world2():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["ms_per_step"] > 0 and d["higher_is_better"] is True
+
+
+def test_cpu_baseline_runs_the_oracle_proper():
+    """bench.py's cpu_baseline calls oracle.build_operator + oracle.power_psi (the oracle as it
+    stands) on a bounded row-block sample, and reports an oracle time-to-eps (config 1)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import psigen
+    w = psigen.make_config(1)
+    r = bench.cpu_oracle_sample(w, target_edges=20_000, sweeps=2)
+    assert r["kind"] == "oracle" and r["cores"] == 1 and r["value"] > 0
+    assert "oracle.power_psi" in r["sample"]
+    rp1, f1, r1, m1 = bench._row_block(w, 20_000)
+    assert rp1.shape == (w.n + 1,) and rp1[-1] == m1 == len(f1) and m1 >= 20_000 > rp1[r1 - 1]
+    t = bench.oracle_time_to_eps((1,))
+    assert t["config1"]["T"] == 52 and t["config1"]["time_to_eps_s"] > 0

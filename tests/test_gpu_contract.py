@@ -107,3 +107,49 @@ def test_numeric_divergence_reported(gpu):
         assert np.all(g.get_residual_history() == 2.0)     # ||c^T A^t||_1 = 2 for all t
         st, T, gap = g.iterate(1e-9, 50, norm="row")
         assert st == gpu.PSI_OK and T == 1 and gap == 0.0
+
+
+def test_library_pool_and_empty_cache(gpu):
+    """the library allocates from its OWN pool (never the device's default pool):
+    memory it caches after psi_destroy is returned by psi_empty_cache, after which torch can
+    allocate it again."""
+    import torch
+    w = psigen.make_config(4, scale=20)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    free0, _ = torch.cuda.mem_get_info()
+    d = dev(w.row_ptr, w.followers, w.lam, w.mu)
+    with gpu.PsiGraph(*d) as g:
+        g.iterate(w.eps)
+    torch.cuda.synchronize()
+    del d
+    torch.cuda.empty_cache()
+    free1, _ = torch.cuda.mem_get_info()
+    gpu.empty_cache()
+    free2, _ = torch.cuda.mem_get_info()
+    assert free2 >= free1 and free0 - free2 < 64 << 20, (free0, free1, free2)
+    x = torch.empty((free2 - (1 << 30)) // 8, dtype=torch.float64, device="cuda")
+    del x
+    torch.cuda.empty_cache()                       # give it back for the following tests
+
+
+def test_power_nf_zero_iters_is_not_converged(gpu):
+    """Alg. 1 with max_iters = 0 and eps < 1 leaves the loop with gap_0 = 1 > eps
+    (Alg. 1 line 3), i.e. not converged, as psi_iterate reports it."""
+    w = psigen.make_config(0)
+    with gpu.PsiGraph(*dev(w.row_ptr, w.followers, w.lam, w.mu)) as g:
+        st, p, q, it = g.power_nf([3, 5], 1e-9, 0)
+        assert st == gpu.PSI_NOT_CONVERGED and list(it) == [0, 0]
+        st, _, _ = g.iterate(1e-9, 0)
+        assert st == gpu.PSI_NOT_CONVERGED
+        st, p, q, it = g.power_nf([3], 2.0, 0)                 # eps >= 1: gap_0 <= eps
+        assert st == gpu.PSI_OK
+
+
+def test_history_length_counts_stored_entries(gpu):
+    """psi_get_residual_history's len_out is the number of entries written."""
+    w = psigen.make_config(0)
+    with gpu.PsiGraph(*dev(w.row_ptr, w.followers, w.lam, w.mu)) as g:
+        st, T, _ = g.iterate(0.0, 37)
+        h = g.get_residual_history()
+        assert T == 37 and len(h) == 37 and np.all(np.isfinite(h))

@@ -53,10 +53,24 @@ def check_topk(ref, got, ks=(10, 100, 1000)):
                 assert abs(ref[x] - ref[y]) <= 1e-10 * max(ref[x], ref[y]), (k, x, y)
 
 
+def check_scalars(op, info):
+    """The ingest's scalars (psi_get_info) against the oracle's (oracle.graph_scalars):
+    ||B|| by rows / columns (Alg. 2 line 2; reading R1), rho_A (the convergence
+    factor, R14) to 1e-12 relative; N_f, N_g and the leaderless count exactly."""
+    sc = oracle.graph_scalars(op)
+    for k in ("kappa_row", "kappa_col", "rho_A"):
+        assert abs(info[k] - sc[k]) <= 1e-12 * abs(sc[k]), (k, info[k], sc[k])
+    for k in ("n_f", "n_g", "n_leaderless"):
+        assert info[k] == sc[k], (k, info[k], sc[k])
+
+
 def parity(psi, w, norm="row", eps=None, full=True):
     eps = w.eps if eps is None else eps
-    ref = oracle.power_psi(w.row_ptr, w.followers, w.lam, w.mu, eps=eps, norm=norm)
+    op = oracle.build_operator(w.row_ptr, w.followers, w.lam, w.mu)
+    ref = oracle.power_psi(op=op, eps=eps, norm=norm)
     got = gpu_run(psi, w.row_ptr, w.followers, w.lam, w.mu, 0.0, ref.iterations, norm)
+    check_scalars(op, got["info"])
+    del op
     assert got["T"] == ref.iterations
     err = oracle.max_rel_error(ref.psi, got["psi"])
     assert err <= TOL, err
@@ -195,9 +209,39 @@ def test_config2_parity_and_pagerank(gpu):
 
 
 def test_config3_parity(gpu):
+    """Config 3 (Chung-Lu, 5M users, 1e8 edges, leaderless users kept): fixed-count parity,
+    the ingest scalars, and the eps-mode stop (T within one sweep, eps_t history)."""
     w = psigen.make_config(3)
-    ref, got = parity(gpu, w, full=False)
+    ref, got = parity(gpu, w, full=True)
     assert got["info"]["n_leaderless"] > 0
+
+
+def test_kappa_col_counterexample_through_cabi(gpu, driver):
+    """The 4-user graph on which bound (19) fails with the column-sum norm (reading R1,
+    tests/golden/kappa_col_counterexample.json): through the C-ABI every norm gives
+    last_gap = ||B||_norm * eps_T (Alg. 2), the oracle's T and eps_t, and
+    psi_get_info's kappa_row / kappa_col equal the golden values."""
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                    "kappa_col_counterexample.json")))
+    rp, f = psigen.csr_from_edges(g["n"], g["edges"])
+    lam, mu = np.array(g["lam"]), np.array(g["mu"])
+    op = oracle.build_operator(rp, f, lam, mu)
+    for norm, kappa in (("row", g["kappa_row"]), ("col", g["kappa_col"]), ("one", 1.0)):
+        ref = oracle.power_psi(op=op, eps=1e-9, norm=norm)
+        got = gpu_run(gpu, rp, f, lam, mu, 1e-9, 10_000, norm)
+        info = got["info"]
+        check_scalars(op, info)
+        assert abs(info["kappa_row"] - g["kappa_row"]) < g["abs_tol"]
+        assert abs(info["kappa_col"] - g["kappa_col"]) < g["abs_tol"]
+        k = {"row": info["kappa_row"], "col": info["kappa_col"], "one": 1.0}[norm]
+        assert abs(k - kappa) < g["abs_tol"]
+        assert got["T"] == ref.iterations
+        assert got["gap"] == pytest.approx(k * got["hist"][-1], rel=1e-15, abs=0)
+        # eps_t = sum |s_t - s_{t-1}| of rounded iterates (|s| ~ 1): equal up to ~N u
+        np.testing.assert_allclose(got["hist"], ref.history, rtol=1e-12, atol=1e-14)
+        assert abs(got["hist"][0] - g["eps_1"]) < g["abs_tol"]
+        assert oracle.max_rel_error(ref.psi, got["psi"]) <= TOL
 
 
 def test_config4_small_scale_parity(gpu):

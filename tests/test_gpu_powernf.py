@@ -91,7 +91,11 @@ def test_nsystems_config1_matches_power_psi(gpu):
         g.iterate(1e-14)
         psi_v = g.get_psi().cpu().numpy()
     assert st == gpu.PSI_OK and mv > 10 * w.n
-    assert oracle.max_rel_error(psi_v, psi_nf.cpu().numpy()) < 1e-9
+    # both against the oracle's converged Alg. 2 (not against each other): the N-systems
+    # psi stops each origin at ||p - p_old||_1 <= 1e-13, so it is within ~1e-11 of the limit
+    ref = oracle.power_psi(w.row_ptr, w.followers, w.lam, w.mu, eps=1e-15).psi
+    assert oracle.max_rel_error(ref, psi_v) <= 1e-10
+    assert oracle.max_rel_error(ref, psi_nf.cpu().numpy()) < 1e-9
     assert abs(psi_nf.cpu().numpy().sum() - 1.0) < 1e-9
 
 

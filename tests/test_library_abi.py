@@ -64,3 +64,38 @@ def test_no_oracle_import_in_product_package():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
+
+
+def test_binding_rejects_bad_arrays():
+    """the binding validates dtype / shape / contiguity before any C call (a numpy
+    default-int64 followers array would otherwise be read as int32 pairs)."""
+    import numpy as np
+    import paper_2206_09960_b200 as psi
+    rp = np.array([0, 1, 1], dtype=np.int64)
+    f = np.array([1], dtype=np.int32)
+    lam = np.array([0.5, 0.5])
+    mu = np.array([0.5, 0.5])
+    with pytest.raises(TypeError, match="followers"):
+        psi.PsiGraph(rp, f.astype(np.int64), lam, mu)
+    with pytest.raises(TypeError, match="lam"):
+        psi.PsiGraph(rp, f, lam.astype(np.float32), mu)
+    with pytest.raises(ValueError, match="mu"):
+        psi.PsiGraph(rp, f, lam, mu[:1])
+    with pytest.raises(ValueError, match="row_ptr"):
+        psi.PsiGraph(rp[:2], f, lam, mu)
+    with pytest.raises(ValueError, match="contiguous"):
+        psi.PsiGraph(rp, f, np.array([0.5, 9, 0.5, 9])[::2], mu)
+    # outputs: exact dtype and size, writable, contiguous -- never a silent temporary copy
+    import torch
+    with pytest.raises(ValueError, match="shape"):
+        psi._check(torch.empty(3, dtype=torch.float64), "out", "float64", (2,), writable=True)
+    with pytest.raises(TypeError):
+        psi._check(torch.empty(2, dtype=torch.float32), "out", "float64", (2,), writable=True)
+    with pytest.raises(ValueError, match="contiguous"):
+        psi._check(torch.empty(4, dtype=torch.float64)[::2], "out", "float64", (2,), writable=True)
+    ro = np.zeros(2)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError, match="read-only"):
+        psi._check(ro, "out", "float64", (2,), writable=True)
+    ptr, kind, keep = psi._check([0, 1], "x", "int64", (2,))
+    assert kind == psi.PSI_MEM_HOST and keep.dtype == np.int64

@@ -379,3 +379,82 @@ def test_power_nf_converges_to_balance_equations(seed):
     np.testing.assert_allclose(psi, oracle.psi_nsystems(rp, f, lam, mu), rtol=1e-10, atol=1e-16)
     np.testing.assert_allclose(psi, oracle.power_psi(rp, f, lam, mu, eps=1e-15).psi, rtol=1e-10,
                                atol=1e-16)
+
+
+# ------------------------------------------------ ingest scalars (psi_get_info)
+
+@pytest.mark.parametrize("seed", range(12))
+def test_graph_scalars_vs_dense_and_leader_sets(seed):
+    """oracle.graph_scalars (kappa_row / kappa_col / rho_A / N_f / N_g / leaderless count, the
+    values psi_get_info exports) against the dense entry-by-entry A, B of P:171-173
+    (oracle.dense_A_B, an independent construction) and the brute-force leader sets; every row
+    with a leader satisfies rowsum(A)_j + rowsum(B)_j = sum_{i in L(j)} w_i / W_j = 1."""
+    rng = np.random.default_rng(4000 + seed)
+    n = int(rng.integers(5, 60))
+    rp, f, lam, mu = random_graph(rng, n, float(rng.uniform(0.02, 0.3)), leaderless_frac=0.2,
+                                  lam0_frac=0.05 if seed % 3 == 0 else 0.0)
+    op = build_operator(rp, f, lam, mu)
+    sc = oracle.graph_scalars(op)
+    A, B, c, d = oracle.dense_A_B(rp, f, lam, mu)
+    assert sc["kappa_row"] == pytest.approx(B.sum(axis=1).max(), rel=1e-14, abs=0)
+    assert sc["kappa_col"] == pytest.approx(B.sum(axis=0).max(), rel=1e-14, abs=0)
+    assert sc["rho_A"] == pytest.approx(A.sum(axis=1).max(), rel=1e-14, abs=0)
+    L = oracle.leader_sets(rp, f, n)
+    has_lead = np.array([len(x) > 0 for x in L])
+    assert sc["n_g"] == int(has_lead.sum()) and sc["n_leaderless"] == n - sc["n_g"]
+    assert sc["n_f"] == sum(1 for l in range(n) if rp[l + 1] > rp[l])
+    rs = A.sum(axis=1) + B.sum(axis=1)
+    np.testing.assert_allclose(rs[has_lead], 1.0, rtol=1e-14)
+    assert np.all(rs[~has_lead] == 0.0)
+    assert sc["kappa_row"] <= 1.0 + 1e-15 and sc["rho_A"] <= c.max() + 1e-15
+
+
+def test_graph_scalars_hand_values():
+    """Chain 0 -> 1 (0 follows 1), lambda = (0.2, 0.6), mu = (0.3, 0.4): W_0 = 1.0, user 1
+    leaderless; B[0,1] = 0.6, A[0,1] = 0.4 -- all norms read off by hand."""
+    rp, f = csr_from_edges(2, [(0, 1)])
+    op = build_operator(rp, f, np.array([0.2, 0.6]), np.array([0.3, 0.4]))
+    sc = oracle.graph_scalars(op)
+    assert sc == pytest.approx({"kappa_row": 0.6, "kappa_col": 0.6, "rho_A": 0.4, "n_f": 1,
+                                "n_g": 1, "n_leaderless": 1}, abs=1e-16)
+
+
+@pytest.mark.parametrize("chunk", [1, 3, 7, 61])
+def test_edge_blocks_chunking_is_exact(monkeypatch, chunk):
+    """oracle.operator streams huge edge arrays in blocks of ~_CHUNK edges of whole rows (the
+    branch C4/C5 take with _CHUNK = 2^26).  Forcing tiny chunks -- rows longer than a chunk,
+    many blocks -- must give the same W, A^T, B^T (vs their entry definitions) and psi as one
+    block (up to the summation order of W), and psi must
+    obey the sum rule sum psi = 1 - (1/N) sum_{L(n) empty} s_n (derived from Eq. (12))."""
+    import oracle.operator as opmod
+    rng = np.random.default_rng(77)
+    n = 120
+    rp, f, lam, mu = random_graph(rng, n, 0.12, leaderless_frac=0.1)
+    hub = [(i, 0) for i in range(2, n) if i % 2 == 0]       # a row longer than any tiny chunk
+    edges = [(int(j), int(l)) for l in range(n) for j in f[rp[l]:rp[l + 1]]]
+    rp, f = csr_from_edges(n, sorted(set(edges) | set(hub)))
+    base = build_operator(rp, f, lam, mu)
+    r0 = oracle.power_psi(op=base, eps=0.0, max_iters=60)
+    monkeypatch.setattr(opmod, "_CHUNK", chunk)
+    blocks = list(opmod._edge_blocks(rp))
+    assert len(blocks) > 1 and blocks[0][0] == 0 and blocks[-1][1] == len(f)
+    assert all(b[1] == c[0] for b, c in zip(blocks, blocks[1:]))          # contiguous cover
+    assert all(np.array_equal(b[2], np.repeat(np.arange(n), np.diff(rp))[b[0]:b[1]]) for b in blocks)
+    op = build_operator(rp, f, lam, mu)
+    # W_j = sum_{l in L(j)} (lambda_l + mu_l) written out with exactly rounded sums (P:172);
+    # the blocked sums may associate differently, so equal up to rounding
+    import math
+    L = oracle.leader_sets(rp, f, n)
+    W_def = np.array([math.fsum(lam[l] + mu[l] for l in L[j]) for j in range(n)])
+    np.testing.assert_allclose(op["W"], W_def, rtol=4e-16 * n, atol=0)
+    np.testing.assert_allclose(op["W"], base["W"], rtol=4e-16 * n, atol=0)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    Wd = np.where(W_def > 0, W_def, 1.0)
+    np.testing.assert_allclose(op["AT"].data, mu[rows] / Wd[f], rtol=1e-14)     # A[j,i] = mu_i/W_j
+    np.testing.assert_allclose(op["BT"].data, lam[rows] / Wd[f], rtol=1e-14)    # B[j,i] = lam_i/W_j
+    assert np.array_equal(op["AT"].indices, base["AT"].indices)
+    r1 = oracle.power_psi(op=op, eps=0.0, max_iters=60)
+    np.testing.assert_allclose(r1.psi, r0.psi, rtol=1e-13)
+    leaderless = np.bincount(f, minlength=n) == 0
+    r2 = oracle.power_psi(op=op, eps=0.0, max_iters=4000)
+    assert abs(r2.psi.sum() - (1 - r2.s[leaderless].sum() / n)) < 1e-12
