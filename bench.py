@@ -188,39 +188,90 @@ def algorithmic_bytes_per_sweep(n, m, n_g, n_f):
 
 # --------------------------------------------------------------------------- CPU baseline
 
-def cpu_oracle_sample(w, target_edges=20_000_000, sweeps=3):
-    """Time the oracle's Alg. 2 sweep (s <- A^T s + c, SciPy CSR, fp64, 1 core) on a contiguous
-    row block of the same graph with ~target_edges edges; returns edges/s and a description."""
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    import scipy.sparse as sp
-    from oracle.operator import newsfeed_normaliser
-
-    n = w.n
+def _row_block(w, target_edges):
+    """The leaders [0, r1) of the workload's CSR with ~target_edges follow edges, all other rows
+    emptied: a valid follower graph on the same N users (a bounded sample of the workload)."""
     rp = w.row_ptr
     r1 = int(np.searchsorted(rp, min(target_edges, w.m), side="left"))
-    r1 = max(1, min(r1, n))
-    lo, hi = 0, int(rp[r1])
-    W = newsfeed_normaliser(rp, w.followers, w.lam, w.mu)          # setup, not timed
-    rows = np.repeat(np.arange(r1), np.diff(rp[: r1 + 1]))
-    vals = w.mu[rows] / W[w.followers[lo:hi]]
-    AT = sp.csr_matrix((vals, w.followers[lo:hi].astype(np.int32), rp[: r1 + 1].astype(np.int32)),
-                       shape=(r1, n))
-    c = w.mu / (w.lam + w.mu)
-    s = c.copy()
-    times = []
-    for _ in range(sweeps):
-        t0 = time.perf_counter()
-        new = AT @ s + c[:r1]                           # Alg. 2 line 324 on the row block
-        eps_t = float(np.abs(new - s[:r1]).sum())       # line 325
-        s[:r1] = new
-        times.append(time.perf_counter() - t0)
-    t = statistics.median(times)
-    edges = hi - lo
-    return {"value": edges / t / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
-            "ms_per_sweep": t * 1e3,
-            "sample": f"oracle Alg.2 sweep (SciPy CSR fp64, 1 thread) on rows [0,{r1}) = {edges} "
-                      f"edges of the same graph, median of {sweeps} sweeps, {t*1e3:.1f} ms/sweep",
+    r1 = max(1, min(r1, w.n))
+    m1 = int(rp[r1])
+    rp1 = np.concatenate([rp[: r1 + 1], np.full(w.n - r1, m1, dtype=np.int64)])
+    return rp1, w.followers[:m1], r1, m1
+
+
+def cpu_oracle_sample(w, target_edges=20_000_000, sweeps=3, op=None):
+    """The oracle AS IT STANDS (oracle.build_operator + oracle.power_psi: Alg. 2 with explicit
+    SciPy CSR A^T, fp64, 1 core) on a bounded sample of the workload -- its leaders [0, r1) with
+    ~target_edges edges, on all N users -- run for `sweeps` sweeps (eps = 0, fixed count);
+    value = sample edges x sweeps / time of the power_psi call (the operator build is setup;
+    pass `op` to reuse one)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import oracle
+    rp1, f1, r1, m1 = _row_block(w, target_edges)
+    t0 = time.perf_counter()
+    if op is None:
+        op = oracle.build_operator(rp1, f1, w.lam, w.mu)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r = oracle.power_psi(op=op, eps=0.0, max_iters=sweeps)
+    t = (time.perf_counter() - t0) / max(r.iterations, 1)
+    return {"value": m1 / t / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+            "ms_per_sweep": round(t * 1e3, 2), "build_operator_s": round(t_build, 2),
+            "sample": f"oracle.power_psi (Alg. 2, explicit SciPy CSR, fp64, 1 thread) on the "
+                      f"workload's leaders [0,{r1}) = {m1} edges over all {w.n} users, "
+                      f"{r.iterations} sweeps incl. the readout, {t*1e3:.1f} ms per sweep",
             "cpu": _cpu_model(), "host_cpus": os.cpu_count()}
+
+
+def oracle_time_to_eps(configs=(1, 3)):
+    """PAPER.md Table III reports whole solves: the oracle's time-to-eps on
+    whole BASELINE configs that fit a CPU core in seconds (oracle.power_psi, 1 thread)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import oracle
+    import psigen
+    out = {}
+    for k in configs:
+        w = psigen.make_config(k)
+        t0 = time.perf_counter()
+        op = oracle.build_operator(w.row_ptr, w.followers, w.lam, w.mu)
+        tb = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        r = oracle.power_psi(op=op, eps=w.eps)
+        t = time.perf_counter() - t0
+        out[f"config{k}"] = {"T": r.iterations, "time_to_eps_s": round(t, 3),
+                             "build_operator_s": round(tb, 3),
+                             "gteps": round(w.m * (r.iterations + 1) / t / 1e9, 4), "cores": 1}
+        del op, w
+    return out
+
+
+# Measured gather ceilings of this design (profiles/r1/ubench_gather_r1.txt): random 8-byte
+# gathers from an L2-resident vector (k_tiles' edge-stream gathers) and from shared memory
+# (k_heavy's staged segments), per B200, G gathers/s.
+GATHER_L2_GPS = 281.0
+GATHER_SMEM_GPS = 1040.0
+
+
+def gather_ceiling(info, sweep_ms):
+    """The sweep's design ceiling from psi_get_info counts: k_heavy's entries at the measured
+    shared-memory gather rate + the edge stream's gathers at the measured L2 rate (serial,
+    as the kernels run), beside the HBM roofline."""
+    heavy = info["heavy_entries"]
+    stream = info["num_tiles"] * info["tile_edges"] - 0        # edge slots of k_tiles
+    t_ms = heavy / (GATHER_SMEM_GPS * 1e9) * 1e3 + stream / (GATHER_L2_GPS * 1e9) * 1e3
+    return {"heavy_entries": heavy, "stream_gathers": stream,
+            "rates_gps": {"smem": GATHER_SMEM_GPS, "l2": GATHER_L2_GPS,
+                          "source": "profiles/r1/ubench_gather_r1.txt"},
+            "ceiling_sweep_ms": round(t_ms, 4), "frac_of_gather_ceiling": round(t_ms / sweep_ms, 4)}
+
+
+def knobs(info):
+    """Every PSI_* environment override in effect (none by default) and the launch shape the
+    library chose, so a number can be traced to its configuration."""
+    env = {k: v for k, v in sorted(os.environ.items()) if k.startswith("PSI_")}
+    lib = {k: info[k] for k in ("tile_edges", "grid", "block", "hot_smem", "heavy_labels",
+                                "heavy_panels", "n_heavy", "last_solver")}
+    return {"env": env, "library": lib}
 
 
 def _cpu_model():
@@ -239,16 +290,19 @@ def run_reference(args, ws, rank):
     """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
     if rank != 0:
         return None
+    import oracle
     w = make_workload(args.config, seed=0, pinned=False)
+    rp1, f1, _, _ = _row_block(w, args.cpu_edges // 4)
+    op = oracle.build_operator(rp1, f1, w.lam, w.mu)             # setup, once
     per_step = []
     for i in range(args.warmup + args.steps):
-        r = cpu_oracle_sample(w, target_edges=args.cpu_edges, sweeps=1)
+        r = cpu_oracle_sample(w, target_edges=args.cpu_edges // 4, sweeps=1, op=op)
         if i >= args.warmup:
             per_step.append(r)
     val = statistics.median([r["value"] for r in per_step])
     cb = dict(per_step[0])
     cb["value"] = val
-    cb["sample"] = cb["sample"].replace("median of 1 sweeps", f"{args.steps} timed steps")
+    cb["sample"] = cb["sample"] + f"; median of {args.steps} timed steps (one sweep each)"
     ms = statistics.median([r["ms_per_sweep"] for r in per_step])
     return {"metric": METRIC, "value": val, "unit": "GTEPS", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
@@ -321,13 +375,16 @@ def run_ours(args, ws, rank, local):
 
     g = psi.PsiGraph(*d_in)
     info = g.info()
+    psi_dev = torch.empty(n, dtype=torch.float64, device=dev)
 
     # ---- warm-up
     for _ in range(args.warmup):
         g.iterate(eps)
+        g.get_psi(out=psi_dev)
     torch.cuda.synchronize()
 
-    # ---- timed region: K solves to eps
+    # ---- timed region: K solves to eps, each with the readout's scatter of psi back to the
+    # caller's labels (psi_get_psi into a device buffer: the k_unpermute of row a5)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     Ts = []
     with ClockSampler(local) as clk:
@@ -336,6 +393,7 @@ def run_ours(args, ws, rank, local):
         e0.record(stream)
         for _ in range(args.steps):
             st, T, gap = g.iterate(eps)
+            g.get_psi(out=psi_dev)
             Ts.append(T)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -349,9 +407,19 @@ def run_ours(args, ws, rank, local):
     value = edges_all / (ms_total * 1e-3) / 1e9
     per_sweep = 3 if info["n_heavy"] > 0 else 2
     if g.info()["last_solver"] == 1:          # persistent small-graph solver: one launch per solve
-        launches = len(Ts)
-    else:
-        launches = sum(per_sweep * (t + 1) + 1 for t in Ts)
+        launches = 2 * len(Ts)
+    else:                                     # init + 3 per sweep and readout + unpermute
+        launches = sum(per_sweep * (t + 1) + 2 for t in Ts)
+    trace = None
+    if rank == 0:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from launch_trace import trace as _trace
+            trace = _trace(g, eps, psi_dev)
+            trace["what"] = ("CUPTI (torch.profiler) over one timed step: kernels launched and "
+                             "CUDA runtime calls made by psi_iterate + psi_get_psi")
+        except Exception as e:   # never lose the main line over the evidence
+            trace = {"error": repr(e)}
 
     # ---- per-launch device time of the sweep kernels: CUDA events on the library's stream
     # around every k_tiles / k_fix launch (psi_time_sweep, direct launches, 20 sweeps)
@@ -379,6 +447,8 @@ def run_ours(args, ws, rank, local):
     achieved = bsweep / (sweep_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": _traffic_from_profiles("sweep", args.config),
+            "traffic_source": _traffic_from_profiles("source", args.config),
+            "gather": gather_ceiling(info, sweep_ms),
             "kernel": "one sweep = k_heavy + k_tiles<sweep> + k_fix<sweep>; each launch timed "
                       "with CUDA events on the library stream (psi_time_sweep, 20 sweeps)",
             "k_heavy_ms": round(heavy_ms, 4), "k_tiles_ms": round(tiles_ms, 4),
@@ -394,7 +464,8 @@ def run_ours(args, ws, rank, local):
            "data": "synthetic (psigen, seed = rank)", "config": _config_dict(args, w),
            "time_to_eps_ms": round(ms_step, 4), "iterations_T": T,
            "ingest_ms": round(info["ingest_ms"], 2), "gpu_launches": launches,
-           "roofline": roof, "clocks": clk.summary(),
+           "roofline": roof, "clocks": clk.summary(), "launch_trace": trace,
+           "knobs": knobs(info),
            "pagerank": {"what": "psi_pagerank: PageRank power method, Eq. (22), alpha = 0.85, "
                                 "same graph, eps and kernels (SURVEY 8(f) row 1)",
                         "time_to_eps_ms": round(pr_ms, 3), "iterations_T": pr_T,
@@ -423,12 +494,64 @@ def run_ours(args, ws, rank, local):
             out["table_iii_style"] = paper_comparison(dev)
         except Exception as e:  # never lose the main line over the side measurement
             out["table_iii_style"] = {"error": repr(e)}
+    if rank == 0 and not args.no_configs:
+        try:
+            out["configs"] = configs_side(dev, [k for k in (1, 2, 3, 4) if k != args.config])
+        except Exception as e:  # never lose the main line over the side measurement
+            out["configs"] = {"error": repr(e)}
+        torch.cuda.empty_cache()
     if rank == 0 and not args.no_cpu:
         try:
             out["cpu_baseline"] = cpu_oracle_sample(w, target_edges=args.cpu_edges)
+            out["cpu_baseline"]["oracle_time_to_eps"] = oracle_time_to_eps((1, 3))
         except Exception as e:  # never lose the GPU line over the baseline
             out["cpu_baseline"] = {"value": None, "error": repr(e)}
     return out if rank == 0 else None
+
+
+def configs_side(dev, configs):
+    """Every other BASELINE.json config on this GPU (the paper's timings span all its datasets,
+    P:476-479): time-to-eps (median of 5 solves + readout, after 3 warm-ups), the sweep time
+    (psi_time_sweep, 20 sweeps) and its fraction of the HBM roofline."""
+    import torch
+    import paper_2206_09960_b200 as psi
+    import psigen
+    peak, _ = _peaks()
+    rows = []
+    for k in configs:
+        w = psigen.make_config(k)
+        d = [torch.from_numpy(a).to(dev) for a in (w.row_ptr, w.followers, w.lam, w.mu)]
+        out = torch.empty(w.n, dtype=torch.float64, device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with psi.PsiGraph(*d) as g:
+            for _ in range(3):
+                g.iterate(w.eps)
+                g.get_psi(out=out)
+            ts = []
+            for _ in range(5):
+                torch.cuda.synchronize()
+                e0.record()
+                _, T, _ = g.iterate(w.eps)
+                g.get_psi(out=out)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            g.time_sweep(3)
+            hv, ti, fx = g.time_sweep(20)
+            inf = g.info()
+        sweep = hv + ti + fx
+        byt = algorithmic_bytes_per_sweep(w.n, w.m, inf["n_g"], inf["n_f"])
+        t = statistics.median(ts)
+        rows.append({"config": k, "N": w.n, "M": w.m, "eps": w.eps, "T": T,
+                     "time_to_eps_ms": round(t, 4), "solve_gteps": round(w.m * (T + 1) / t / 1e6, 2),
+                     "sweep_ms": round(sweep, 4), "k_heavy_ms": round(hv, 4),
+                     "k_tiles_ms": round(ti, 4), "k_fix_ms": round(fx, 4),
+                     "sweep_gteps": round(w.m / sweep / 1e6, 2), "B_sweep": byt,
+                     "hbm_frac": round(byt / (sweep * 1e-3) / 1e9 / peak, 4),
+                     "solver": inf["last_solver"], "ingest_ms": round(inf["ingest_ms"], 2)})
+        del d, out
+        torch.cuda.empty_cache()
+    return rows
 
 
 def batch_side(w, dev, config, single_sweep_ms, k=4):
@@ -511,6 +634,7 @@ def main(argv=None):
     ap.add_argument("--cpu-edges", type=int, default=20_000_000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-batch", action="store_true", help="skip the 4-profile batch side line")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1-C4 side record")
     args = ap.parse_args(argv)
     ws, rank, local = dist_env()
     if args.impl == "reference":

@@ -91,6 +91,7 @@ typedef struct psi_info {
                              heavy rows), 2 = direct launches (PSI_GRAPH=0) */
   int64_t n_profiles;     /* activity profiles of the context (1, or k of psi_build_graph_batch) */
   int64_t tile_edges;     /* edges per tile of the sweep: 1024 with heavy rows, else 512 */
+  int64_t overlapped;     /* 1: k_heavy and k_tiles run concurrently (the overlapped plan) */
 } psi_info;
 
 /*
@@ -256,8 +257,10 @@ psi_status psi_nsystems(psi_ctx* ctx, double eps, int64_t max_iters, double* psi
  * sweep's kernels, bracketed by CUDA events on the context's stream: *heavy_ms = staged
  * shared-memory sums of the heavy rows (k_heavy; 0 if the graph has no heavy rows),
  * *tiles_ms = edge-stream gather + epilogue (k_tiles), *fix_ms = split rows + eps_t
- * reduction + stop rule (k_fix).  Any output pointer may be NULL.  Leaves no psi (call
- * psi_iterate afterwards).  PSI_E_INVALID_ARG if ctx is NULL or sweeps < 1. */
+ * reduction + stop rule (k_fix).  With the overlapped plan (psi_info.overlapped = 1:
+ * k_heavy and k_tiles run concurrently, one CTA of each per SM) the pair is timed as one:
+ * *heavy_ms = 0 and *tiles_ms = k_heavy || k_tiles.  Any output pointer may be NULL.  Leaves
+ * no psi (call psi_iterate afterwards).  PSI_E_INVALID_ARG if ctx is NULL or sweeps < 1. */
 psi_status psi_time_sweep(psi_ctx* ctx, int64_t sweeps, double* heavy_ms, double* tiles_ms,
                           double* fix_ms);
 

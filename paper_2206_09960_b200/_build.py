@@ -34,6 +34,8 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
     os.makedirs(os.path.dirname(lib), exist_ok=True)
     tmp = lib + f".tmp{os.getpid()}"
     extra = ["-DPSI_CHECKS"] if checked else []
+    # experiment builds only (never set by build() / the tests): e.g. PSI_NVCC_EXTRA=-DPSI_EXP_...
+    extra += os.environ.get("PSI_NVCC_EXTRA", "").split()
     cmd = [NVCC, *FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

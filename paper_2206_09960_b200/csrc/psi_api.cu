@@ -95,7 +95,9 @@ struct psi_ctx {
   long long pr_T = 0;
   double pr_alpha = 0.0;
   double* hhot = nullptr;        // [n_heavy] heavy rows' sums over followers < H (k_heavy)
+  double* scold = nullptr;       // [n_heavy] their edge-stream sums (overlapped sweep only)
   int heavy_grid = 0;
+  int heavy_block = 0;
   size_t heavy_smem = 0;
   // multi-profile batch (psi_build_graph_batch, psi_batch.cu); sweep state of one group
   struct Batch {
@@ -206,7 +208,8 @@ void free_ctx(psi_ctx* c) {
   void* ptrs[] = {c->g.edges, c->g.tile_row, c->g.a0, c->g.a1, c->g.g, c->g.wt, c->g.d1,
                   c->g.lam, c->g.psi, c->g.old_of_new, c->g.split, c->x[0], c->x[1],
                   c->p_in, c->p_out, c->eps_part1, c->eps_part2, c->history, c->st, c->prm,
-                  c->hhot, c->g.h_ent, c->g.h_loff, c->g.h_prow, c->g.h_rslot, c->g.h_wslot};
+                  c->hhot, c->g.h_ent, c->g.h_loff, c->g.h_prow, c->g.h_rslot, c->g.h_wslot,
+                  c->scold, c->g.hsplit};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
   for (auto e : c->b.exec) if (e) cudaGraphExecDestroy(e);
@@ -258,6 +261,11 @@ SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   A.st_last = getenv("PSI_ST_LAST") ? atoi(getenv("PSI_ST_LAST")) : 0;
   A.n_heavy = (int)c->g.n_heavy;
   A.hhot = c->hhot;
+  A.ovl = c->g.ovl;
+  A.scold = c->scold;
+  A.hsplit = c->g.hsplit;
+  A.heavy.seg_shift = c->g.heavy_seg_shift;
+  A.heavy.slots = c->g.heavy_slots;
   A.heavy.ent = c->g.h_ent;
   A.heavy.loff = c->g.h_loff;
   A.heavy.prow = c->g.h_prow;
@@ -283,6 +291,36 @@ cudaError_t add_kernel(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode
   void* kp[2] = {args, n_extra};
   p.kernelParams = kp;
   return cudaGraphAddKernelNode(node, g, dep, ndep, &p);
+}
+
+// The kernel nodes of one sweep (or the readout) after `dep` (may be NULL): k_heavy -> k_tiles
+// -> k_fix.  With the overlapped plan k_tiles hangs on k_heavy by a programmatic edge from its
+// launch-completion port (k_tiles starts once every k_heavy CTA has begun, so one CTA of each
+// shares every SM) and k_fix waits for both.
+cudaError_t add_sweep_nodes(psi_ctx* c, cudaGraph_t g, const cudaGraphNode_t* dep, SweepArgs* A,
+                            bool readout, cudaGraphNode_t* last) {
+  const bool hv = c->g.n_heavy > 0;
+  cudaGraphNode_t nh{}, nt{};
+  cudaError_t e;
+  if (hv && (e = add_kernel(g, &nh, dep, dep ? 1 : 0, heavy_kernel_ptr(c->g.heavy_warps),
+                            c->heavy_grid, c->heavy_block, A, nullptr, c->heavy_smem)) != cudaSuccess)
+    return e;
+  if (hv && c->g.ovl) {
+    if ((e = add_kernel(g, &nt, nullptr, 0, readout ? c->tc.readout : c->tc.sweep, c->grid1,
+                        c->tc.block, A, nullptr, c->tc.smem)) != cudaSuccess)
+      return e;
+    cudaGraphEdgeData ed{};
+    ed.from_port = cudaGraphKernelNodePortLaunchCompletion;
+    ed.type = cudaGraphDependencyTypeProgrammatic;
+    if ((e = cudaGraphAddDependencies_v2(g, &nh, &nt, &ed, 1)) != cudaSuccess) return e;
+    cudaGraphNode_t both[2] = {nh, nt};
+    return add_kernel(g, last, both, 2, fix_kernel_ptr(readout), c->grid2, kFixBlock, A, nullptr);
+  }
+  if ((e = add_kernel(g, &nt, hv ? &nh : dep, (hv || dep) ? 1 : 0,
+                      readout ? c->tc.readout : c->tc.sweep, c->grid1, c->tc.block, A, nullptr,
+                      c->tc.smem)) != cudaSuccess)
+    return e;
+  return add_kernel(g, last, &nt, 1, fix_kernel_ptr(readout), c->grid2, kFixBlock, A, nullptr);
 }
 
 // The PageRank variant of the sweep arguments: the same kernels with Eq. (22)'s constants.
@@ -317,31 +355,54 @@ psi_status build_graph_exec(psi_ctx* c, bool pagerank = false) {
   cp.conditional.size = 1;
   API_CK(cudaGraphAddNode(&n_while, graph, &n_init, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
-  cudaGraphNode_t b0, b1, b2, n_r0;
-  const bool hv = c->g.n_heavy > 0;
-  if (hv)
-    API_CK(add_kernel(body, &b0, nullptr, 0, heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock, &A,
-                      nullptr, c->heavy_smem));
-  API_CK(add_kernel(body, &b1, hv ? &b0 : nullptr, hv ? 1 : 0, c->tc.sweep, c->grid1, c->tc.block,
-                    &A, nullptr, c->tc.smem));
-  API_CK(add_kernel(body, &b2, &b1, 1, fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr));
-
-  if (!pagerank) {
-    if (hv)
-      API_CK(add_kernel(graph, &n_r0, &n_while, 1, heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock,
-                        &A, nullptr, c->heavy_smem));
-    API_CK(add_kernel(graph, &n_r1, hv ? &n_r0 : &n_while, 1, c->tc.readout, c->grid1,
-                      c->tc.block, &A, nullptr, c->tc.smem));
-    API_CK(add_kernel(graph, &n_r2, &n_r1, 1, fix_kernel_ptr(true), c->grid2, kFixBlock, &A, nullptr));
-  }
+  cudaGraphNode_t b2;
+  API_CK(add_sweep_nodes(c, body, nullptr, &A, false, &b2));
+  if (!pagerank) API_CK(add_sweep_nodes(c, graph, &n_while, &A, true, &n_r2));
+  (void)n_r1;
   API_CK(cudaGraphInstantiate(&exec, graph, 0));
   return PSI_OK;
 }
 
 cudaError_t launch(void* fn, int grid, int block, SweepArgs* A, int* extra, cudaStream_t s,
-                   size_t smem = 0) {
+                   size_t smem = 0, bool programmatic = false) {
   void* kp[2] = {A, extra};
-  return cudaLaunchKernel(fn, dim3(grid), dim3(block), kp, smem, s);
+  if (!programmatic) return cudaLaunchKernel(fn, dim3(grid), dim3(block), kp, smem, s);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, kp);
+}
+
+// PSI_OVL_SERIAL=1 (measurement only): the overlapped plan's kernels launched one after the
+// other, to time k_heavy and k_tiles of that plan separately
+bool ovl_serial() {
+  const char* e = getenv("PSI_OVL_SERIAL");
+  return e && e[0] == '1';
+}
+
+// One sweep (or the readout) as direct launches on the context stream: k_heavy -> k_tiles ->
+// k_fix; with the overlapped plan k_tiles is launched programmatically, so it starts once
+// every k_heavy CTA has begun and runs beside it (griddepcontrol, psi_heavy.cu / psi_sweep.cu).
+cudaError_t launch_sweep(psi_ctx* c, SweepArgs* A, bool readout, cudaEvent_t mid = nullptr,
+                         cudaEvent_t after_tiles = nullptr) {
+  const bool hv = c->g.n_heavy > 0;
+  cudaError_t e;
+  if (hv && (e = launch(heavy_kernel_ptr(c->g.heavy_warps), c->heavy_grid, c->heavy_block, A,
+                        nullptr, c->stream, c->heavy_smem)) != cudaSuccess)
+    return e;
+  if (mid && (e = cudaEventRecord(mid, c->stream)) != cudaSuccess) return e;
+  if ((e = launch(readout ? c->tc.readout : c->tc.sweep, c->grid1, c->tc.block, A, nullptr,
+                  c->stream, c->tc.smem, hv && c->g.ovl && !ovl_serial())) != cudaSuccess)
+    return e;
+  if (after_tiles && (e = cudaEventRecord(after_tiles, c->stream)) != cudaSuccess) return e;
+  return launch(fix_kernel_ptr(readout), c->grid2, kFixBlock, A, nullptr, c->stream);
 }
 
 // Direct stream launches of the same kernels (no CUDA graph, no conditional node): used by
@@ -360,21 +421,13 @@ psi_status iterate_direct(psi_ctx* c, bool pagerank = false) {
   const long long max_iters = c->h_prm->max_iters;
   bool cont = c->h_prm->gap0 > eps && max_iters > 0;
   while (cont) {
-    if (c->g.n_heavy > 0)
-      API_CK(launch(heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock, &A, nullptr, c->stream,
-                    c->heavy_smem));
-    API_CK(launch(c->tc.sweep, c->grid1, c->tc.block, &A, nullptr, c->stream, c->tc.smem));
-    API_CK(launch(fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr, c->stream));
+    API_CK(launch_sweep(c, &A, false));
     API_CK(cudaMemcpyAsync(c->h_st, c->st, sizeof(LoopState), cudaMemcpyDeviceToHost, c->stream));
     API_CK(cudaStreamSynchronize(c->stream));
     cont = !(c->h_st->status & 1) && c->h_st->gap > eps && c->h_st->iter < max_iters;
   }
   if (pagerank) return PSI_OK;
-  if (c->g.n_heavy > 0)
-    API_CK(launch(heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock, &A, nullptr, c->stream,
-                  c->heavy_smem));
-  API_CK(launch(c->tc.readout, c->grid1, c->tc.block, &A, nullptr, c->stream, c->tc.smem));
-  API_CK(launch(fix_kernel_ptr(true), c->grid2, kFixBlock, &A, nullptr, c->stream));
+  API_CK(launch_sweep(c, &A, true));
   return PSI_OK;
 }
 
@@ -788,7 +841,7 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
 
   // Iteration buffers.
-  c->tc = tiles_config(c->g.ntiles, n, c->g.tile);
+  c->tc = tiles_config(c->g.ntiles, n, c->g.tile, c->g.ovl != 0);
   c->grid1 = c->tc.grid;
   {
     // Hot prefix of x kept in L2 (evict_last) in BOTH ping-pong buffers: PSI_HOT_MB per
@@ -807,14 +860,20 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
       if (atoi(e) > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
   }
   c->grid2 = fix_grid(c->g.nsplit);
+  if (c->g.ovl)                                       // + k_fix's pass over the heavy rows
+    c->grid2 = std::max(c->grid2, (int)std::min<long long>((c->g.n_heavy + kFixBlock - 1) / kFixBlock,
+                                                            148LL * 8));
   if (c->g.n_heavy > 0) {
     int dev = 0, sms = 0;
     B_CK(cudaGetDevice(&dev));
     B_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     c->heavy_grid = std::max(1, std::min(sms, c->g.npanels));
-    c->heavy_smem = heavy_smem_bytes(c->g.nseg);
-    B_CK(cudaFuncSetAttribute(heavy_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)c->heavy_smem));
+    c->heavy_smem = heavy_smem_bytes(c->g.nseg, c->g.heavy_seg_shift, c->g.heavy_slots,
+                                     c->g.heavy_warps);
+    c->heavy_block = 32 * (c->g.heavy_warps + 1);
+    B_CK(cudaFuncSetAttribute(heavy_kernel_ptr(c->g.heavy_warps),
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->heavy_smem));
+    if (c->g.ovl) B_CK(dev_alloc(&c->scold, (size_t)c->g.n_heavy * sizeof(double), c->stream));
     B_CK(dev_alloc(&c->hhot, (size_t)c->g.n_heavy * sizeof(double), c->stream));
     B_CK(cudaMemsetAsync(c->hhot, 0, (size_t)c->g.n_heavy * sizeof(double), c->stream));
   }
@@ -1013,6 +1072,7 @@ psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
   out->last_solver = c->last_solver;
   out->n_profiles = c->g.nprof;
   out->tile_edges = c->g.tile;
+  out->overlapped = (c->g.ovl && c->g.n_heavy > 0) ? 1 : 0;
   return PSI_OK;
 }
 
@@ -1043,19 +1103,17 @@ psi_status psi_time_sweep(psi_ctx* c, int64_t sweeps, double* heavy_ms, double* 
   double t0 = 0, t1 = 0, t2 = 0;
   psi_status rc = PSI_OK;
   const bool hv = c->g.n_heavy > 0;
+  // overlapped plan: k_heavy and k_tiles run concurrently, so the pair is timed as one (tiles_ms)
+  // and heavy_ms is 0 -- no event may sit between the two launches (it would serialise them)
+  const bool ovl = hv && c->g.ovl && !ovl_serial();
   for (int64_t k = 0; k < sweeps && rc == PSI_OK; ++k) {
     float a = 0, b = 0, d = 0;
     if (cudaEventRecord(e[0], c->stream) != cudaSuccess ||
-        (hv && launch(heavy_kernel_ptr(), c->heavy_grid, kHeavyBlock, &A, nullptr, c->stream,
-                      c->heavy_smem) != cudaSuccess) ||
-        cudaEventRecord(e[1], c->stream) != cudaSuccess ||
-        launch(c->tc.sweep, c->grid1, c->tc.block, &A, nullptr, c->stream, c->tc.smem) != cudaSuccess ||
-        cudaEventRecord(e[2], c->stream) != cudaSuccess ||
-        launch(fix_kernel_ptr(false), c->grid2, kFixBlock, &A, nullptr, c->stream) != cudaSuccess ||
+        launch_sweep(c, &A, false, ovl ? nullptr : e[1], e[2]) != cudaSuccess ||
         cudaEventRecord(e[3], c->stream) != cudaSuccess ||
         cudaEventSynchronize(e[3]) != cudaSuccess ||
-        cudaEventElapsedTime(&d, e[0], e[1]) != cudaSuccess ||
-        cudaEventElapsedTime(&a, e[1], e[2]) != cudaSuccess ||
+        (!ovl && cudaEventElapsedTime(&d, e[0], e[1]) != cudaSuccess) ||
+        cudaEventElapsedTime(&a, ovl ? e[0] : e[1], e[2]) != cudaSuccess ||
         cudaEventElapsedTime(&b, e[2], e[3]) != cudaSuccess)
       rc = fail(PSI_E_CUDA, "psi_time_sweep: %s", cudaGetErrorString(cudaGetLastError()));
     t0 += d;

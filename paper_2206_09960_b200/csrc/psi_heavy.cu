@@ -69,36 +69,25 @@ __device__ __forceinline__ void ld_stream8(const unsigned* p, unsigned (&w)[8]) 
                : "l"(p));
 }
 
-// One warp's pass over one list (panel, warp, segment) chunk: 8 entries per lane, gathers
-// from the staged segment, runs of equal slots summed in registers and across lanes (a
-// segmented scan), each finished run added once to its slot sum (owned by this warp).
-// predicated shared-memory read-modify-write (no branch: runs end at data-dependent lanes)
-__device__ __forceinline__ void sadd_if(bool p, const double* base, unsigned idx, double v) {
-  asm volatile(
-      "{\n"
-      ".reg .pred q;\n"
-      ".reg .f64 t;\n"
-      "setp.ne.u32 q, %0, 0;\n"
-      "@q ld.shared.f64 t, [%1];\n"
-      "@q add.rn.f64 t, t, %2;\n"
-      "@q st.shared.f64 [%1], t;\n"
-      "}\n" :: "r"((unsigned)p), "r"(smem_u32(base) + idx * 8u), "d"(v) : "memory");
-}
-
 // One warp's pass over one chunk of a list (panel, warp, segment): 8 entries per lane,
 // gathers from the staged segment, runs of equal slots summed in registers (inclusive run
 // sums) and across lanes (a segmented scan), each finished run added once to its slot sum
-// (owned by this warp) -- branch-free.
+// (owned by this warp) -- branch-free.  A slot has ONE run per list (the entries of a list
+// are grouped by slot), so the run ends of a chunk -- at most nine per lane: seven inside
+// the lane, its tail, and lane 0's flush of the run carried in from the previous chunk --
+// all touch distinct slot sums: their read-modify-writes are issued as one batch of loads
+// followed by one batch of stores, instead of nine dependent load-add-store chains.
 __device__ __forceinline__ void process_chunk(const unsigned (&w)[8], const double* seg,
                                               double* rowsum, int lane, double& carry,
-                                              unsigned& carry_slot) {
+                                              unsigned& carry_slot, int sh, unsigned junk) {
   unsigned sl[8];
   double acc[8];
+  const unsigned omask = (1u << sh) - 1u;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    sl[k] = w[k] >> kSegShift;
-    PSI_ASSERT(sl[k] <= (unsigned)kHeavySlots);
-    acc[k] = seg[w[k] & (kSeg - 1)];
+    sl[k] = w[k] >> sh;
+    PSI_ASSERT(sl[k] <= junk);
+    acc[k] = seg[w[k] & omask];
   }
   bool single = true;
 #pragma unroll
@@ -112,8 +101,6 @@ __device__ __forceinline__ void process_chunk(const unsigned (&w)[8], const doub
   // = a segmented inclusive scan of the lane's tail run with resets f_l = !(single_l && cont_l).
   const unsigned prev_last = __shfl_up_sync(kFull, sl[7], 1);
   const bool cont = lane == 0 ? (sl[0] == carry_slot) : (sl[0] == prev_last);
-  // the run carried from the previous chunk ended at the chunk boundary
-  sadd_if(lane == 0 && !cont && carry_slot != kHeavySlots, rowsum, carry_slot, carry);
   int f = !(single && cont);
   double val = acc[7];
 #pragma unroll
@@ -128,45 +115,70 @@ __device__ __forceinline__ void process_chunk(const unsigned (&w)[8], const doub
   const double out = f ? val : val + carry;          // chain reaching back to the carry
   double in = __shfl_up_sync(kFull, out, 1);
   if (lane == 0) in = carry;
-  // runs ending inside the lane; the first one (head) continues a run from earlier lanes
-  // when cont
+  const bool next_cont = __shfl_down_sync(kFull, cont, 1);
+  // run ends: k < 7 inside the lane (the first one, the head, continues a run from earlier
+  // lanes when cont), 7 = the lane's tail when the next lane starts another slot, 8 = the
+  // carried run that ended at the chunk boundary (lane 0)
+  bool pr[9];
+  unsigned ix[9];
   bool head = true;
 #pragma unroll
   for (int k = 0; k < 7; ++k) {
     const bool b = sl[k] != sl[k + 1];
-    sadd_if(b, rowsum, sl[k], acc[k] + ((head && cont) ? in : 0.0));
+    pr[k] = b;
+    ix[k] = sl[k];
+    acc[k] += (head && cont) ? in : 0.0;
     head = head && !b;
   }
-  // the tail run ends at the lane boundary when the next lane starts another slot
-  const bool next_cont = __shfl_down_sync(kFull, cont, 1);
-  sadd_if(lane < 31 && !next_cont, rowsum, sl[7], out);
+  pr[7] = lane < 31 && !next_cont;
+  ix[7] = sl[7];
+  acc[7] = out;
+  pr[8] = lane == 0 && !cont && carry_slot != junk;
+  ix[8] = carry_slot;
+  double old[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) old[k] = pr[k] ? rowsum[ix[k]] : 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (pr[k]) rowsum[ix[k]] = old[k] + acc[k];
+  if (pr[8]) rowsum[ix[8]] = old[8] + carry;
   carry = __shfl_sync(kFull, out, 31);
   carry_slot = __shfl_sync(kFull, sl[7], 31);
   __syncwarp();
 }
 
 __device__ __forceinline__ void load_chunk(const unsigned* base, unsigned c, unsigned e, int lane,
-                                           unsigned (&w)[8]) {
+                                           unsigned (&w)[8], unsigned null_entry) {
   const unsigned pos = c + lane * 8;
   if (pos < e) {
     ld_stream8(base + pos, w);                        // lists are padded to 8 words
   } else {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) w[k] = kNullEntry;
+    for (int k = 0; k < 8; ++k) w[k] = null_entry;
   }
 }
 
-__global__ void __launch_bounds__(kHeavyBlock, 1) k_heavy(SweepArgs A) {
+// HW consumer warps + 1 producer warp.  HW = kHeavyWarps with the serial plan (the kernel owns
+// the SM); HW = kOvlWarps with the overlapped one (k_tiles shares the SM, PSI_OVERLAP).
+template <int HW>
+__global__ void __launch_bounds__(32 * (HW + 1), 1) k_heavy(SweepArgs A) {
   extern __shared__ __align__(128) unsigned char hsm[];
   const HeavyPlan& H = A.heavy;
   const int nseg = H.nseg;
-  double* stage_buf = reinterpret_cast<double*>(hsm);                 // [kHeavyStages][kSeg]
-  double* rowsum = stage_buf + kHeavyStages * kSeg;                    // [kHeavySlots + 2]
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(rowsum + kHeavySlots + 2);
+  const int sh = H.seg_shift;
+  const int SEG = 1 << sh;                                            // labels per segment
+  const unsigned junk = (unsigned)H.slots;                            // padding slot
+  const unsigned null_entry = junk << sh;
+  double* stage_buf = reinterpret_cast<double*>(hsm);                 // [kHeavyStages][SEG]
+  double* rowsum = stage_buf + kHeavyStages * SEG;                    // [slots + 2]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(rowsum + H.slots + 2);
   unsigned long long* empty = full + kHeavyStages;
   int* ring = reinterpret_cast<int*>(empty + kHeavyStages);           // [8] panel ids
   unsigned* offs = reinterpret_cast<unsigned*>(ring + 8);             // [warps][nseg + 1]
 
+  // a programmatically dependent k_tiles (overlapped sweep) may launch once every CTA is here:
+  // it then lands beside this CTA on the same SM (no-op without a dependent)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long t = A.st->iter;
   const double* __restrict__ xs = (t & 1) ? A.x1 : A.x0;             // x_{t-1} (x_T: readout)
@@ -174,13 +186,13 @@ __global__ void __launch_bounds__(kHeavyBlock, 1) k_heavy(SweepArgs A) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < kHeavyStages; ++i) {
       mbar_init(full + i, 1);
-      mbar_init(empty + i, kHeavyWarps);
+      mbar_init(empty + i, HW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == kHeavyWarps) {
+  if (warp == HW) {
     // ---- producer: claims panels dynamically (deterministic result: a panel's sums do not
     // depend on which CTA computes it) and streams x_{t-1}[s*kSeg, (s+1)*kSeg) for each.
     if (lane == 0) {
@@ -198,8 +210,8 @@ __global__ void __launch_bounds__(kHeavyBlock, 1) k_heavy(SweepArgs A) {
           if (done) {
             mbar_arrive(full + st);                   // no bytes: consumers read ring = -1
           } else {
-            mbar_expect_tx(full + st, kSeg * 8);
-            bulk_g2s(stage_buf + (size_t)st * kSeg, xs + (size_t)s * kSeg, kSeg * 8, full + st, pol);
+            mbar_expect_tx(full + st, SEG * 8);
+            bulk_g2s(stage_buf + (size_t)st * SEG, xs + ((size_t)s << sh), SEG * 8, full + st, pol);
           }
         }
         if (done) break;
@@ -216,11 +228,11 @@ __global__ void __launch_bounds__(kHeavyBlock, 1) k_heavy(SweepArgs A) {
     const int p = ring[k & 7];
     if (p < 0) break;
     PSI_ASSERT(p < H.npanels);
-    const int* ws = H.wslot + (size_t)p * (kHeavyWarps + 1);
+    const int* ws = H.wslot + (size_t)p * (HW + 1);
     const int sl0 = ws[warp], sl1 = ws[warp + 1];
     for (int i = sl0 + lane; i < sl1; i += 32) rowsum[i] = 0.0;
     // this warp's lists of the panel are contiguous: (p, warp, s = 0 .. nseg-1)
-    const long long* lo = H.loff + ((size_t)p * kHeavyWarps + warp) * nseg;
+    const long long* lo = H.loff + ((size_t)p * HW + warp) * nseg;
     const long long base = lo[0];
     for (int i = lane; i <= nseg; i += 32) my_offs[i] = (unsigned)(lo[i] - base);
     __syncwarp();
@@ -230,12 +242,12 @@ __global__ void __launch_bounds__(kHeavyBlock, 1) k_heavy(SweepArgs A) {
     unsigned c_n = 0;
     while (s_n < nseg && c_n >= my_offs[s_n + 1]) c_n = my_offs[++s_n];
     unsigned w_n[8];
-    if (s_n < nseg) load_chunk(wst, c_n, my_offs[s_n + 1], lane, w_n);
+    if (s_n < nseg) load_chunk(wst, c_n, my_offs[s_n + 1], lane, w_n, null_entry);
     for (int s = 0; s < nseg; ++s, ++q) {
       const int st = q % kHeavyStages;
       if (s > 0) mbar_wait(full + st, (q / kHeavyStages) & 1u);
-      const double* seg = stage_buf + (size_t)st * kSeg;
-      unsigned carry_slot = kHeavySlots;      // open run carried across chunks of the list
+      const double* seg = stage_buf + (size_t)st * SEG;
+      unsigned carry_slot = junk;             // open run carried across chunks of the list
       double carry = 0.0;
       while (s_n == s) {
         unsigned w[8];
@@ -246,34 +258,36 @@ __global__ void __launch_bounds__(kHeavyBlock, 1) k_heavy(SweepArgs A) {
           ++s_n;
           if (s_n < nseg) c_n = my_offs[s_n];
         }
-        if (s_n < nseg) load_chunk(wst, c_n, my_offs[s_n + 1], lane, w_n);
-        process_chunk(w, seg, rowsum, lane, carry, carry_slot);
+        if (s_n < nseg) load_chunk(wst, c_n, my_offs[s_n + 1], lane, w_n, null_entry);
+        process_chunk(w, seg, rowsum, lane, carry, carry_slot, sh, junk);
       }
-      if (lane == 0 && carry_slot != kHeavySlots) rowsum[carry_slot] += carry;
+      if (lane == 0 && carry_slot != junk) rowsum[carry_slot] += carry;
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + st);
     }
     // ---- panel end: row sums = slot sums in slot order
-    asm volatile("bar.sync 1, %0;" :: "r"(kHeavyWarps * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" :: "r"(HW * 32) : "memory");
     const int r0 = H.prow[p], r1 = H.prow[p + 1];
-    for (int r = r0 + (int)threadIdx.x; r < r1; r += kHeavyWarps * 32) {
+    for (int r = r0 + (int)threadIdx.x; r < r1; r += HW * 32) {
       const int2 sn = H.rslot[r];
-      PSI_ASSERT(r < A.n_heavy && sn.x >= 0 && sn.x + sn.y <= kHeavySlots);
+      PSI_ASSERT(r < A.n_heavy && sn.x >= 0 && sn.x + sn.y <= H.slots);
       double S = 0.0;
       for (int j = 0; j < sn.y; ++j) S += rowsum[sn.x + j];
       A.hhot[r] = S;
     }
-    asm volatile("bar.sync 1, %0;" :: "r"(kHeavyWarps * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" :: "r"(HW * 32) : "memory");
   }
 }
 
 }  // namespace
 
-void* heavy_kernel_ptr() { return (void*)k_heavy; }
+void* heavy_kernel_ptr(int warps) {
+  return warps == kOvlWarps ? (void*)k_heavy<kOvlWarps> : (void*)k_heavy<kHeavyWarps>;
+}
 
-size_t heavy_smem_bytes(int nseg) {
-  return (size_t)kHeavyStages * kSeg * 8 + (kHeavySlots + 2) * 8 + 2 * kHeavyStages * 8 + 8 * 4 +
-         (size_t)kHeavyWarps * (nseg + 1) * 4;
+size_t heavy_smem_bytes(int nseg, int seg_shift, int slots, int warps) {
+  return ((size_t)kHeavyStages << seg_shift) * 8 + (size_t)(slots + 2) * 8 + 2 * kHeavyStages * 8 +
+         8 * 4 + (size_t)warps * (nseg + 1) * 4;
 }
 
 }  // namespace psi

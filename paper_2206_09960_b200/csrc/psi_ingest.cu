@@ -515,12 +515,12 @@ __global__ void k_row_fill_long(RowFillArgs R, const int* list, int nlist) {
   }
 }
 
-// warp per heavy row: entry keys (list << kEntBits) | (slot << kSegShift) | (label % kSeg);
-// list = (panel * kHeavyWarps + owner warp of the slot) * nseg + segment.  The i-th hot
+// warp per heavy row: entry keys (list << kEntBits) | (slot << sh) | (label % 2^sh);
+// list = (panel * warps + owner warp of the slot) * nseg + segment.  The i-th hot
 // follower of row r goes to slot rslot[r].x + i % rslot[r].y (round-robin virtual rows).
 __global__ void k_heavy_keys(const int* hot, const long long* hoff, const int2* rslot,
                              const int* row_panel, const int* pslot_base, const unsigned char* slot_warp,
-                             int n_heavy, int nseg, unsigned long long* keys) {
+                             int n_heavy, int nseg, int sh, int warps, unsigned long long* keys) {
   const int lane = threadIdx.x & 31;
   WARP_STRIDE(r, n_heavy) {
     const long long b = hoff[r], e = hoff[r + 1];
@@ -531,8 +531,8 @@ __global__ void k_heavy_keys(const int* hot, const long long* hoff, const int2* 
       const unsigned lab = (unsigned)hot[q];
       const int slot = sn.x + (int)((q - b) % sn.y);
       const unsigned long long list =
-          ((unsigned long long)p * kHeavyWarps + slot_warp[base + slot]) * nseg + (lab >> kSegShift);
-      keys[q] = (list << kEntBits) | ((unsigned long long)slot << kSegShift) | (lab & (kSeg - 1));
+          ((unsigned long long)p * warps + slot_warp[base + slot]) * nseg + (lab >> sh);
+      keys[q] = (list << kEntBits) | ((unsigned long long)slot << sh) | (lab & ((1u << sh) - 1));
     }
   }
 }
@@ -562,6 +562,74 @@ __global__ void k_heavy_fill(const unsigned long long* keys, long long nk, const
     const unsigned long long k = keys[i];
     const long long L = (long long)(k >> kEntBits);
     ent[loff[L] + (i - lstart[L])] = (unsigned)(k & ((1ull << kEntBits) - 1));
+  }
+}
+
+// Bank-aware order inside every run of the staged-segment plan's lists.  k_heavy's gather
+// instruction k of a chunk takes the k-th entry of 32 lanes -- list positions 256 c + 8 l + k
+// -- and reads shared-memory word (entry & (2^sh - 1)) of a staged segment: 16 eight-byte bank
+// pairs; each half-warp (a block of 128 list positions) costs as many wavefronts as lanes on
+// its busiest pair.  The sums only need a slot's entries contiguous (one run per list), in any
+// order: inside every 128-position block, each run's entries are laid out greedily, every
+// position taking the run's remaining entry whose bank pair that instruction has used least
+// in the block.  Measured: 5.5 -> 4.6 wavefronts per gather instruction at C5 (ideal 2);
+// reordering whole runs as well gained nothing in a model of this greedy.
+// A run keeps its order where it crosses a block boundary (so every block is independent:
+// one lane per block, a warp per list) and when it is longer than 32.  Deterministic.
+constexpr int kBalBlock = 128;
+__global__ void __launch_bounds__(kBalBlock) k_heavy_balance(const unsigned* in, unsigned* out,
+                                                             const long long* loff,
+                                                             const long long* lstart,
+                                                             long long nlists, int sh) {
+  __shared__ unsigned long long cnt[8][kBalBlock];   // 16 four-bit counters per instruction k
+  const int t = threadIdx.x, lane = t & 31;
+  WARP_STRIDE(L, nlists) {
+    const long long b = loff[L], e_pad = loff[L + 1];
+    const int len_l = (int)(lstart[L + 1] - lstart[L]);
+    const unsigned* src = in + b;
+    unsigned* dst = out + b;
+    for (long long i = b + len_l + lane; i < e_pad; i += 32) out[i] = in[i];   // null padding
+    const int nblk = (len_l + 127) >> 7;
+    for (int B = lane; B < nblk; B += 32) {
+      const int q0 = B << 7, q1 = min(q0 + 128, len_l);
+      for (int k = 0; k < 8; ++k) cnt[k][t] = 0ull;
+      auto count = [&](int q, unsigned w) {
+        const unsigned long long c = cnt[q & 7][t];
+        const unsigned bk = w & 15;
+        if (((c >> (4 * bk)) & 15ull) < 15ull) cnt[q & 7][t] = c + (1ull << (4 * bk));
+      };
+      int q = q0;
+      if (q0 > 0) {                                   // the tail of a run from the last block
+        const unsigned sl = src[q0 - 1] >> sh;
+        while (q < q1 && (src[q] >> sh) == sl) { dst[q] = src[q]; count(q, src[q]); ++q; }
+      }
+      while (q < q1) {                                // runs starting in this block
+        const unsigned sl = src[q] >> sh;
+        int r = q + 1;
+        while (r < len_l && (src[r] >> sh) == sl) ++r;
+        const int in_blk = min(r, q1) - q;            // entries placed inside the block
+        if (r - q > 32) {
+          for (int i = 0; i < in_blk; ++i) { dst[q + i] = src[q + i]; count(q + i, src[q + i]); }
+        } else {
+          unsigned w[32];
+          for (int j = 0; j < in_blk; ++j) w[j] = src[q + j];
+          unsigned used = 0;
+          for (int i = 0; i < in_blk; ++i) {
+            const unsigned long long c = cnt[(q + i) & 7][t];
+            int bj = 0, bv = 1 << 30;
+            for (int j = 0; j < in_blk; ++j) {
+              if ((used >> j) & 1u) continue;
+              const int v = (int)((c >> (4 * (w[j] & 15))) & 15ull);
+              if (v < bv) { bv = v; bj = j; }
+            }
+            used |= 1u << bj;
+            dst[q + i] = w[bj];
+            count(q + i, w[bj]);
+          }
+        }
+        q = min(r, q1);                               // the rest belongs to the next block
+      }
+    }
   }
 }
 
@@ -603,7 +671,7 @@ __global__ void k_tile_rows(const int* rp, int n_act, int ntiles, int tile, int*
     const long long e = k * (long long)tile;
     int lo = 0, hi = n_act;                 // first row r with rp[r] >= e
     while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
+      const int mid = lo + ((hi - lo) >> 1);      // no int overflow for n_act > 2^30
       if ((long long)rp[mid] < e) lo = mid + 1; else hi = mid;
     }
     tile_row[k] = lo;
@@ -624,9 +692,9 @@ __global__ void k_split_fill(const int* rows, long long ns, const int* rp, int t
 
 // ------------------------------------------------------------------ host helpers
 
-// RAII device buffer for temporaries, stream-ordered (cudaMallocAsync from the device's
-// default pool; psi_build_graph raises the pool's release threshold so repeated ingests
-// reuse the memory instead of re-mapping it)
+// RAII device buffer for temporaries, stream-ordered (dev_alloc: the library's own pool,
+// which keeps freed temporaries reserved while a build runs, so the ingest's phases reuse
+// each other's memory instead of re-mapping it)
 thread_local cudaStream_t g_tmp_stream = nullptr;
 struct Tmp {
   void* p = nullptr;
@@ -634,7 +702,7 @@ struct Tmp {
   void reset() { if (p) cudaFreeAsync(p, g_tmp_stream); p = nullptr; }
   cudaError_t alloc(size_t bytes) {
     reset();
-    return cudaMallocAsync(&p, bytes ? bytes : 16, g_tmp_stream);
+    return dev_alloc(&p, bytes ? bytes : 16, g_tmp_stream);
   }
   template <class T> T* as() const { return (T*)p; }
 };
@@ -727,12 +795,14 @@ int env_int(const char* name, int dflt) {
 
 namespace {
 
-// Heavy-row plan (psi_heavy.cu): panels of <= kHeavySlots slots and ~e_panel hot entries,
+// Heavy-row plan (psi_heavy.cu): panels of <= out.heavy_slots slots and ~e_panel hot entries,
 // virtual rows of <= vmax entries, contiguous slot ranges per consumer warp balanced by
 // entries; then the entry lists (panel, segment, warp) sorted by (slot, label).
 int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcnt, Tmp& hoff,
                      cudaStream_t s, char* msg, size_t msg_len) {
   const int nseg = out.nseg;
+  const int sh = out.heavy_seg_shift;
+  const int HW = out.heavy_warps, SLOTS = out.heavy_slots;
   std::vector<long long> hc(NH);
   IG_CK(cudaMemcpyAsync(hc.data(), hcnt.p, (size_t)NH * sizeof(long long), cudaMemcpyDeviceToHost, s));
   // the hot followers of each row stay in input order: the entries are sorted by
@@ -744,7 +814,7 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long pps = std::max(1, env_int("PSI_HEAVY_PPS", kDefaultHeavyPPS));
   const long long e_panel = std::max<long long>((n_ent + pps * sms - 1) / (pps * sms), 32768);
-  const long long vmax = std::max<long long>(e_panel / (2 * kHeavyWarps), 64);
+  const long long vmax = std::max<long long>(e_panel / (2 * HW), 64);
   std::vector<int> prow{0}, row_panel(NH), pslot_base{0}, wslot;
   std::vector<int2> rslot(NH);
   std::vector<unsigned char> slot_warp;
@@ -754,17 +824,17 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
     const int slots = (int)slot_w.size();
     long long T = 0;
     for (long long x : slot_w) T += x;
-    std::vector<int> ws(kHeavyWarps + 1, slots);
+    std::vector<int> ws(HW + 1, slots);
     ws[0] = 0;
     long long acc = 0;
     int w = 1;
-    for (int k = 0; k < slots && w < kHeavyWarps; ++k) {
+    for (int k = 0; k < slots && w < HW; ++k) {
       acc += slot_w[k];
-      while (w < kHeavyWarps && acc * kHeavyWarps >= T * w) ws[w++] = k + 1;
+      while (w < HW && acc * HW >= T * w) ws[w++] = k + 1;
     }
     int owner = 0;
     for (int k = 0; k < slots; ++k) {
-      while (owner + 1 < kHeavyWarps && ws[owner + 1] <= k) ++owner;
+      while (owner + 1 < HW && ws[owner + 1] <= k) ++owner;
       slot_warp.push_back((unsigned char)owner);
     }
     wslot.insert(wslot.end(), ws.begin(), ws.end());
@@ -775,8 +845,8 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   };
   for (int r = 0; r < NH; ++r) {
     long long nv = hc[r] > 0 ? (hc[r] + vmax - 1) / vmax : 0;
-    if (nv > kHeavySlots) nv = kHeavySlots;
-    if (r > prow.back() && ((long long)slot_w.size() + nv > kHeavySlots || p_ent + hc[r] > e_panel))
+    if (nv > SLOTS) nv = SLOTS;
+    if (r > prow.back() && ((long long)slot_w.size() + nv > SLOTS || p_ent + hc[r] > e_panel))
       close_panel(r);
     rslot[r] = make_int2((int)slot_w.size(), (int)nv);
     row_panel[r] = (int)prow.size() - 1;
@@ -788,15 +858,15 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   out.npanels = npanels;
   out.heavy_entries = n_ent;
 
-  IG_CK(cudaMallocAsync(&out.h_prow, prow.size() * sizeof(int), s));
-  IG_CK(cudaMallocAsync(&out.h_rslot, (size_t)NH * sizeof(int2), s));
-  IG_CK(cudaMallocAsync(&out.h_wslot, wslot.size() * sizeof(int), s));
+  IG_CK(dev_alloc(&out.h_prow, prow.size() * sizeof(int), s));
+  IG_CK(dev_alloc(&out.h_rslot, (size_t)NH * sizeof(int2), s));
+  IG_CK(dev_alloc(&out.h_wslot, wslot.size() * sizeof(int), s));
   IG_CK(cudaMemcpyAsync(out.h_prow, prow.data(), prow.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   IG_CK(cudaMemcpyAsync(out.h_rslot, rslot.data(), (size_t)NH * sizeof(int2), cudaMemcpyHostToDevice, s));
   IG_CK(cudaMemcpyAsync(out.h_wslot, wslot.data(), wslot.size() * sizeof(int), cudaMemcpyHostToDevice, s));
 
-  const long long nlists = (long long)npanels * nseg * kHeavyWarps;
-  IG_CK(cudaMallocAsync(&out.h_loff, (size_t)(nlists + 1) * sizeof(long long), s));
+  const long long nlists = (long long)npanels * nseg * HW;
+  IG_CK(dev_alloc(&out.h_loff, (size_t)(nlists + 1) * sizeof(long long), s));
   Tmp keys, keys2, rpan, psb, sw, lstart, plen, scan_tmp, sort_tmp;
   IG_CK(keys.alloc((size_t)std::max<long long>(n_ent, 1) * 8));
   IG_CK(keys2.alloc((size_t)std::max<long long>(n_ent, 1) * 8));
@@ -809,17 +879,17 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
     IG_CK(cudaMemcpyAsync(sw.p, slot_warp.data(), slot_warp.size(), cudaMemcpyHostToDevice, s));
   k_heavy_keys<<<grid_for((long long)NH * 32, 256), 256, 0, s>>>(
       hot.as<int>(), hoff.as<long long>(), out.h_rslot, rpan.as<int>(), psb.as<int>(),
-      sw.as<unsigned char>(), NH, nseg, keys.as<unsigned long long>());
+      sw.as<unsigned char>(), NH, nseg, sh, HW, keys.as<unsigned long long>());
   int end_bit = kEntBits;
   while ((1LL << (end_bit - kEntBits)) <= nlists) ++end_bit;
   cub::DoubleBuffer<unsigned long long> kb(keys.as<unsigned long long>(), keys2.as<unsigned long long>());
   if (n_ent > 0) {
     size_t tb = 0;
-    // by (list, slot) only: the offset bits below kSegShift need no order (stable sort keeps
+    // by (list, slot) only: the offset bits below sh need no order (stable sort keeps
     // the hot-list order inside a slot's run -- fixed, so the sums stay deterministic)
-    IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, (int)n_ent, kSegShift, end_bit, s));
+    IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, (int)n_ent, sh, end_bit, s));
     IG_CK(sort_tmp.alloc(tb));
-    IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp.p, tb, kb, (int)n_ent, kSegShift, end_bit, s));
+    IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp.p, tb, kb, (int)n_ent, sh, end_bit, s));
   }
   IG_CK(lstart.alloc((size_t)(nlists + 1) * sizeof(long long)));
   IG_CK(plen.alloc((size_t)(nlists + 1) * sizeof(long long)));
@@ -835,10 +905,19 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   long long total = 0;
   IG_CK(cudaMemcpyAsync(&total, out.h_loff + nlists, sizeof(long long), cudaMemcpyDeviceToHost, s));
   IG_CK(cudaStreamSynchronize(s));
-  IG_CK(cudaMallocAsync(&out.h_ent, (size_t)std::max<long long>(total, 4) * sizeof(unsigned), s));
-  k_fill_u32<<<grid_for(total, 256), 256, 0, s>>>(out.h_ent, total, kNullEntry);
+  IG_CK(dev_alloc(&out.h_ent, (size_t)std::max<long long>(total, 4) * sizeof(unsigned), s));
+  k_fill_u32<<<grid_for(total, 256), 256, 0, s>>>(out.h_ent, total, (unsigned)SLOTS << sh);
   k_heavy_fill<<<grid_for(n_ent, 256), 256, 0, s>>>(kb.Current(), n_ent, lstart.as<long long>(),
                                                    out.h_loff, out.h_ent);
+  if (env_int("PSI_HEAVY_BALANCE", 1) != 0) {
+    unsigned* bal = nullptr;
+    IG_CK(dev_alloc(&bal, (size_t)std::max<long long>(total, 4) * sizeof(unsigned), s));
+    k_heavy_balance<<<grid_for(nlists * 32, kBalBlock, 148 * 64), kBalBlock, 0, s>>>(
+        out.h_ent, bal, out.h_loff, lstart.as<long long>(), nlists, sh);
+    IG_CK(cudaGetLastError());
+    IG_CK(cudaFreeAsync(out.h_ent, s));
+    out.h_ent = bal;
+  }
   IG_CK(cudaStreamSynchronize(s));
   IG_CK(cudaGetLastError());
   return PSI_OK;
@@ -904,6 +983,14 @@ __global__ void k_permute_b(const int* old_of_new, long long n, int n_act, int p
   }
 }
 
+// overlapped sweep: bit r = heavy row r is a split row (finished by k_fix's split path)
+__global__ void k_heavy_split_bits(const int4* split, long long ns, int n_heavy, unsigned* bits) {
+  GRID_STRIDE(i, ns) {
+    const int r = split[i].x;
+    if (r < n_heavy) atomicOr(bits + (r >> 5), 1u << (r & 31));
+  }
+}
+
 __global__ void k_long_split_flags(const int4* split, long long ns, unsigned char* flag) {
   GRID_STRIDE(i, ns) flag[i] = (split[i].z - split[i].y) > kLongSpan;
 }
@@ -916,10 +1003,10 @@ int batch_vectors(IngestOut& out, long long n, int NA, int nprof, const int* rp,
   out.ngroups = G;
   const size_t nb = (size_t)G * n * kBP * sizeof(double);
   const size_t ab = (size_t)G * std::max(NA, 1) * kBP * sizeof(double);
-  IG_CK(cudaMallocAsync(&out.b_a0, nb, s));
-  IG_CK(cudaMallocAsync(&out.b_psi, nb, s));
+  IG_CK(dev_alloc(&out.b_a0, nb, s));
+  IG_CK(dev_alloc(&out.b_psi, nb, s));
   for (double** q : {&out.b_a1, &out.b_g, &out.b_wt, &out.b_d1, &out.b_lam})
-    IG_CK(cudaMallocAsync(q, ab, s));
+    IG_CK(dev_alloc(q, ab, s));
   for (double* q : {out.b_a0, out.b_psi}) IG_CK(cudaMemsetAsync(q, 0, nb, s));
   for (double* q : {out.b_a1, out.b_g, out.b_wt, out.b_d1, out.b_lam}) IG_CK(cudaMemsetAsync(q, 0, ab, s));
   Tmp K;
@@ -946,7 +1033,7 @@ int batch_vectors(IngestOut& out, long long n, int NA, int nprof, const int* rp,
 int make_tiling(const int* rp_new, int NA, long long m_pad, int tile, cudaStream_t s, int** tile_row,
                 int4** split, int* nsplit, int* nsplit_long, char* msg, size_t msg_len) {
   const int ntiles = (int)(m_pad / tile);
-  IG_CK(cudaMallocAsync(tile_row, (size_t)(ntiles + 1) * sizeof(int), s));
+  IG_CK(dev_alloc(tile_row, (size_t)(ntiles + 1) * sizeof(int), s));
   k_tile_rows<<<grid_for(ntiles + 1, 256), 256, 0, s>>>(rp_new, NA, ntiles, tile, *tile_row);
   Tmp fl, rows, ns, sel_tmp;
   IG_CK(fl.alloc((size_t)(NA > 0 ? NA : 1)));
@@ -968,7 +1055,7 @@ int make_tiling(const int* rp_new, int NA, long long m_pad, int tile, cudaStream
   }
   *nsplit = (int)hs;
   *nsplit_long = 0;
-  IG_CK(cudaMallocAsync(split, (size_t)(hs > 0 ? hs : 1) * sizeof(int4), s));
+  IG_CK(dev_alloc(split, (size_t)(hs > 0 ? hs : 1) * sizeof(int4), s));
   if (hs > 0) {
     k_split_fill<<<grid_for(hs, 256), 256, 0, s>>>(rows.as<int>(), hs, rp_new, tile, *split);
     // rows spanning more than kLongSpan tiles first (summed by a warp each in k_fix)
@@ -1091,9 +1178,9 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
         wt_old.as<double>(), d_old.as<double>(), first_leader.as<int>(), kmax, cnt);
     long long nlong = long_segments(loff.as<int>(), nullptr, N, kShort, s, longu);
     if (m <= kPowerNfMaxEdges) {       // keep the leader lists for Power-NF (psi_powernf.cu)
-      IG_CK(cudaMallocAsync(&out.nf_loff, (size_t)(n + 1) * sizeof(int), s));
-      IG_CK(cudaMallocAsync(&out.nf_leaders, (size_t)std::max<long long>(m, 1) * sizeof(int), s));
-      IG_CK(cudaMallocAsync(&out.nf_lm, (size_t)n * sizeof(double2), s));
+      IG_CK(dev_alloc(&out.nf_loff, (size_t)(n + 1) * sizeof(int), s));
+      IG_CK(dev_alloc(&out.nf_leaders, (size_t)std::max<long long>(m, 1) * sizeof(int), s));
+      IG_CK(dev_alloc(&out.nf_lm, (size_t)n * sizeof(double2), s));
       IG_CK(cudaMemcpyAsync(out.nf_loff, loff.p, (size_t)(n + 1) * sizeof(int), cudaMemcpyDeviceToDevice, s));
       if (m > 0)
         IG_CK(cudaMemcpyAsync(out.nf_leaders, vals.Current(), (size_t)m * sizeof(int),
@@ -1145,7 +1232,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   }
 
   if (out.nf_loff) {
-    IG_CK(cudaMallocAsync(&out.nf_wt, (size_t)n * sizeof(double), s));
+    IG_CK(dev_alloc(&out.nf_wt, (size_t)n * sizeof(double), s));
     IG_CK(cudaMemcpyAsync(out.nf_wt, wt_old.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
   tr.mark("transpose+normalisers");
@@ -1153,7 +1240,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   Tmp cls, new_of_old, key, sel, flag8, nsel, stage_tmp, sort_tmp2, sorted;
   IG_CK(cls.alloc((size_t)n));
   IG_CK(new_of_old.alloc((size_t)n * sizeof(int)));
-  IG_CK(cudaMallocAsync(&out.old_of_new, (size_t)n * sizeof(int), s));
+  IG_CK(dev_alloc(&out.old_of_new, (size_t)n * sizeof(int), s));
   k_classify<<<grid_for(n, 256), 256, 0, s>>>(rp, nlead.as<int>(), N, cls.as<unsigned char>(),
                                               new_of_old.as<int>(), ccount);
   unsigned long long h[16];
@@ -1170,17 +1257,25 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   out.n_hot = (long long)h[8 + C_HOT];
 
   // heavy rows (psi_heavy.cu): active users with >= heavy_min active followers, labelled
-  // first; their followers with label < H = nseg * kSeg are summed by k_heavy from staged
-  // shared-memory segments.  Disabled for graphs smaller than one segment.
+  // first; their followers with label < H = nseg << seg_shift are summed by k_heavy from
+  // staged shared-memory segments.  Disabled for graphs smaller than one segment.  The
+  // overlapped sweep (PSI_OVERLAP=1) uses the smaller plan shape of psi_internal.cuh.
+  out.ovl = env_int("PSI_OVERLAP", 0) != 0 ? 1 : 0;
+  if (out.ovl) {
+    out.heavy_seg_shift = kOvlSegShift;
+    out.heavy_slots = kOvlSlots;
+    out.heavy_warps = kOvlWarps;
+  }
+  const int kSegR = 1 << out.heavy_seg_shift;   // labels per staged segment
   long long h_default = kMinHeavyLabels;
   while (h_default * 2 <= n / 32 && h_default < kMaxHeavyLabels) h_default *= 2;
-  int nseg = env_int("PSI_HEAVY_LABELS", (int)h_default) / kSeg;
+  int nseg = env_int("PSI_HEAVY_LABELS", (int)h_default) / kSegR;
   // on by default only where it measured faster (C5 yes, C4 no); PSI_HEAVY=1/0
   // forces it on/off
   const int heavy_env = env_int("PSI_HEAVY", -1);
   if (heavy_env == 0 || (heavy_env < 0 && n < kDefaultHeavyMinN)) nseg = 0;
   if (nprof > 1) nseg = 0;                     // the batch sweep has no staged-segment path
-  nseg = (int)std::min<long long>(std::min(nseg, kMaxHeavySegs), (n + 1) / kSeg);
+  nseg = (int)std::min<long long>(std::min(nseg, kMaxHeavySegs), (n + 1) / kSegR);
   if (nseg > 0) {
     Tmp act;
     IG_CK(act.alloc((size_t)n * sizeof(int)));
@@ -1206,7 +1301,8 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   }
   if (out.n_heavy == 0) nseg = 0;
   out.nseg = nseg;
-  const int Hs = nseg * kSeg;                 // staged labels [0, Hs)
+  if (nseg == 0) out.ovl = 0;
+  const int Hs = nseg * kSegR;                // staged labels [0, Hs)
 
   IG_CK(key.alloc((size_t)n * 8));
   IG_CK(sel.alloc((size_t)n * 8));
@@ -1274,7 +1370,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   // ---- 6. relabelled edge stream over active rows, folded constants
   const int NA = (int)out.n_act;
   Tmp cntr, K, rp_new;
-  IG_CK(cudaMallocAsync(&out.kinv, (size_t)(NA > 0 ? NA : 1) * sizeof(double), s));
+  IG_CK(dev_alloc(&out.kinv, (size_t)(NA > 0 ? NA : 1) * sizeof(double), s));
   IG_CK(cntr.alloc((size_t)(NA + 1) * sizeof(int)));
   IG_CK(K.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(double)));
   IG_CK(rp_new.alloc((size_t)(NA + 1) * sizeof(int)));
@@ -1332,7 +1428,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   out.ntiles = (int)(((long long)m_act + out.tile - 1) / out.tile);
   const long long m_pad = (long long)out.ntiles * out.tile;
   {
-    IG_CK(cudaMallocAsync(&out.edges, (size_t)(m_pad > 0 ? m_pad : 4) * sizeof(unsigned), s));
+    IG_CK(dev_alloc(&out.edges, (size_t)(m_pad > 0 ? m_pad : 4) * sizeof(unsigned), s));
     int* ed = (int*)out.edges;
     if (NA > 0) {
       RowFillArgs R{rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
@@ -1358,14 +1454,14 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
 
   tr.mark("heavy plan");
   const size_t na_b = (size_t)(NA > 0 ? NA : 1) * sizeof(double);
-  IG_CK(cudaMallocAsync(&out.a0, (size_t)n * sizeof(double), s));
-  IG_CK(cudaMallocAsync(&out.wt, (size_t)n * sizeof(double), s));
-  IG_CK(cudaMallocAsync(&out.psi, (size_t)n * sizeof(double), s));
-  IG_CK(cudaMallocAsync(&out.a1, na_b, s));
-  IG_CK(cudaMallocAsync(&out.g, na_b, s));
-  IG_CK(cudaMallocAsync(&out.d1, na_b, s));
-  IG_CK(cudaMallocAsync(&out.lam, na_b, s));
-  IG_CK(cudaMallocAsync(&out.nlead, (size_t)n * sizeof(int), s));
+  IG_CK(dev_alloc(&out.a0, (size_t)n * sizeof(double), s));
+  IG_CK(dev_alloc(&out.wt, (size_t)n * sizeof(double), s));
+  IG_CK(dev_alloc(&out.psi, (size_t)n * sizeof(double), s));
+  IG_CK(dev_alloc(&out.a1, na_b, s));
+  IG_CK(dev_alloc(&out.g, na_b, s));
+  IG_CK(dev_alloc(&out.d1, na_b, s));
+  IG_CK(dev_alloc(&out.lam, na_b, s));
+  IG_CK(dev_alloc(&out.nlead, (size_t)n * sizeof(int), s));
   k_permute_vectors<<<grid_for(n, 256), 256, 0, s>>>(
       out.old_of_new, N, NA, a_old.as<double>(), g_old.as<double>(), wt_old.as<double>(),
       d_old.as<double>(), lam, K.as<double>(), (double)n, nlead.as<int>(), out.a0, out.a1, out.g,
@@ -1385,6 +1481,14 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     int rc4 = make_tiling(rp_new.as<int>(), NA, (long long)out.ntiles * out.tile, out.tile, s, &out.tile_row,
                           &out.split, &out.nsplit, &out.nsplit_long, msg, msg_len);
     if (rc4 != PSI_OK) return rc4;
+    if (out.ovl && out.n_heavy > 0) {
+      const size_t words = (size_t)(out.n_heavy / 32 + 1);
+      IG_CK(dev_alloc(&out.hsplit, words * sizeof(unsigned), s));
+      IG_CK(cudaMemsetAsync(out.hsplit, 0, words * sizeof(unsigned), s));
+      if (out.nsplit > 0)
+        k_heavy_split_bits<<<grid_for(out.nsplit, 256), 256, 0, s>>>(out.split, out.nsplit,
+                                                                     (int)out.n_heavy, out.hsplit);
+    }
     if (nprof > 1) {
       // as many tiles as hold the m_act real edge words: the last one is never all padding
       out.b_ntiles = (int)(((long long)out.m_act + kTileB - 1) / kTileB);

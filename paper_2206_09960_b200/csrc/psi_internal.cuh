@@ -48,13 +48,18 @@ constexpr int kTile = kBlock * kEpt;     // 1024 edges per tile (512 for graphs 
 constexpr int kFixBlock = 256;           // threads per CTA of the split-row fix-up kernel
 constexpr int kLongSpan = 16;            // split rows over more tiles are summed by a warp
 constexpr unsigned kRowFlag = 0x80000000u;
-// staged-segment heavy-row kernel (psi_heavy.cu)
+// staged-segment heavy-row kernel (psi_heavy.cu).  Two plan shapes: the serial sweep (k_heavy
+// then k_tiles, one SM each in turn) and the overlapped one (PSI_OVERLAP: k_heavy and k_tiles
+// co-resident on every SM, so each gets a smaller share of shared memory and registers).
 constexpr int kSegShift = 13;
-constexpr int kSeg = 1 << kSegShift;     // labels of x per TMA-staged segment (64 KB)
+constexpr int kSeg = 1 << kSegShift;     // labels of x per TMA-staged segment (64 KB), serial plan
 constexpr int kHeavySlots = 8192;        // slot sums per panel (+ a junk slot for padding)
-constexpr int kEntBits = 27;             // entry word: slot (14 bits) << kSegShift | offset
+constexpr int kEntBits = 27;             // entry word: slot (<= 14 bits) << seg_shift | offset
 constexpr unsigned kNullEntry = (unsigned)kHeavySlots << kSegShift;
 constexpr int kHeavyWarps = 16;          // consumer warps (+ 1 producer warp)
+constexpr int kOvlSegShift = 12;         // overlapped plan: 4096-label (32 KB) segments,
+constexpr int kOvlSlots = 4096;          //   4096 slots per panel,
+constexpr int kOvlWarps = 8;             //   8 consumer warps
 constexpr int kHeavyStages = 2;          // TMA ring depth (per-segment cost is fixed)
 constexpr int kHeavyBlock = 32 * (kHeavyWarps + 1);
 constexpr int kDefaultHeavyMin = 64;     // rows with >= this many active followers are heavy
@@ -109,7 +114,9 @@ struct HeavyPlan {
   const int2* rslot;         // [n_heavy] (first slot, number of slots) of each heavy row
   const int* wslot;          // [npanels * (kHeavyWarps + 1)] slot range of each warp
   int npanels;
-  int nseg;                  // staged labels H = nseg * kSeg
+  int nseg;                  // staged labels H = nseg << seg_shift
+  int seg_shift;             // labels per segment = 1 << seg_shift
+  int slots;                 // slot sums per panel; slot index `slots` is the padding junk
 };
 
 // Everything one sweep / readout launch needs (passed by value; frozen in the graph).
@@ -149,6 +156,11 @@ struct SweepArgs {
   const LoopParams* prm;
   cudaGraphConditionalHandle cond;
   int use_cond;              // 1 inside the CUDA graph; 0 for direct stream launches
+  // overlapped sweep (PSI_OVERLAP): k_heavy runs concurrently with k_tiles, so k_tiles leaves
+  // heavy rows' edge-stream sums in scold and k_fix finishes them with hhot
+  int ovl;
+  double* scold;             // [n_heavy]
+  const unsigned* hsplit;    // [n_heavy / 32 + 1] bit r: heavy row r is a split row (k_fix's)
 };
 
 // ---- launchers (psi_sweep.cu)
@@ -161,11 +173,11 @@ struct TilesCfg {                    // launch shape of k_tiles (sweep and reado
   void* solve;                       // k_solve<groups>: the persistent small-graph solver
   int solve_max_grid;                // co-resident CTAs of k_solve (cooperative launch bound)
 };
-TilesCfg tiles_config(int ntiles, long long n, int tile);   // tile: 512 or 1024 edges
+TilesCfg tiles_config(int ntiles, long long n, int tile, bool ovl = false);  // tile: 512 or 1024
 int fix_grid(int nsplit);            // CTAs of the fix-up kernel
 void* fix_kernel_ptr(bool readout);
-void* heavy_kernel_ptr();            // psi_heavy.cu
-size_t heavy_smem_bytes(int nseg);
+void* heavy_kernel_ptr(int warps);   // psi_heavy.cu: kHeavyWarps or kOvlWarps consumer warps
+size_t heavy_smem_bytes(int nseg, int seg_shift, int slots, int warps);
 void* init_kernel_ptr();
 
 // ---- ingest (psi_ingest.cu)
@@ -199,6 +211,9 @@ struct IngestOut {
   // heavy rows (labels [0, n_heavy)): followers < H served by k_heavy (HeavyPlan)
   long long n_heavy = 0, heavy_entries = 0;
   int nseg = 0, npanels = 0;
+  int heavy_seg_shift = kSegShift, heavy_slots = kHeavySlots, heavy_warps = kHeavyWarps;
+  int ovl = 0;                // overlapped plan (PSI_OVERLAP)
+  unsigned* hsplit = nullptr; // [n_heavy / 32 + 1] heavy rows that are split rows (ovl only)
   unsigned* h_ent = nullptr;
   long long* h_loff = nullptr;
   int* h_prow = nullptr;

@@ -192,7 +192,11 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
     unsigned fl = 0;
 #pragma unroll
     for (int q = 0; q < kEpt; ++q) {
+#ifdef PSI_EXP_GMASK                                     // experiment builds: x confined to L2
+      const unsigned lab = (w[q] & kLabelMask) & (unsigned)(PSI_EXP_GMASK);
+#else
       const unsigned lab = w[q] & kLabelMask;
+#endif
       PSI_ASSERT((double)lab <= A.n_users);             // sentinel label n holds x = 0
       fl |= (w[q] >> 31) << q;
       if (lab < hs) v[q] = hot[lab];
@@ -273,7 +277,13 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
       const int r = f0 + i;
       PSI_ASSERT(r < A.n_act && i < (TB * kEpt));
       double Sr = sm.rowsum[i];
-      if (r < A.n_heavy) Sr += A.hhot[r];               // followers < H (k_heavy)
+      if (r < A.n_heavy) {
+        if (A.ovl) {                     // k_heavy is still running: k_fix finishes the row
+          A.scold[r] = Sr;
+          continue;
+        }
+        Sr += A.hhot[r];                                 // followers < H (k_heavy)
+      }
       if (READOUT) {
         A.psi[r] = (ld_stream(A.d + r, pf) + ld_stream(A.lam + r, pf) * Sr) / A.n_users;
       } else {
@@ -295,6 +305,9 @@ template <bool READOUT, int G, int TB>
 __global__ void __launch_bounds__(TB * G, (1024 / (TB * G)) > 0 ? 1024 / (TB * G) : 1) k_tiles(SweepArgs A) {
   extern __shared__ __align__(16) unsigned char dsm[];   // [G x TileSmem][hot cache]
   tiles_body<READOUT, G, false, TB>(A, dsm, A.st->iter, A.eps_part1);
+  // overlapped sweep: launched programmatically beside k_heavy (psi_api.cu); complete only
+  // after it, so whatever follows k_tiles in stream order also follows k_heavy
+  if (A.ovl) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // Split rows, eps_t and the stop rule (k_fix), as a device function of any block size >= 32
@@ -338,6 +351,12 @@ __device__ __forceinline__ void fix_body(const SweepArgs& A, long long t, double
     double S = __ldcg(A.p_out + sp.y);
     for (int k = sp.y + 1; k <= sp.z; ++k) S += __ldcg(A.p_in + k);
     finish(sp.x, S);
+  }
+  if (A.ovl) {
+    // overlapped sweep: the heavy rows k_tiles completed inside a tile (their edge-stream sum
+    // in scold) are finished here, once k_heavy's hhot exists; split heavy rows were above
+    for (int r = blockIdx.x * NT + tid; r < A.n_heavy; r += gridDim.x * NT)
+      if (!((__ldg(A.hsplit + (r >> 5)) >> (r & 31)) & 1u)) finish(r, __ldcg(A.scold + r));
   }
   if (READOUT) return;
 
@@ -509,7 +528,19 @@ int env_int(const char* name, int dflt) {
 
 // Launch shape of the sweep/readout kernel.  Defaults from the C5 measurements in
 // DESIGN.md §12; PSI_GROUPS / PSI_SMEM_HOT / PSI_L1_HOT override them (tuning only).
-TilesCfg tiles_config(int ntiles, long long n, int tile) {
+TilesCfg tiles_config(int ntiles, long long n, int tile, bool ovl) {
+  if (ovl) {
+    // overlapped sweep: one k_tiles CTA beside one k_heavy CTA on every SM -- 4 groups of
+    // 128 threads (1024-edge tiles) and a 2048-label shared-memory hot cache
+    TilesCfg c = cfg_for<4, 128>(ntiles, n, env_int("PSI_OVL_SMEM_HOT", 2048),
+                                 env_int("PSI_L1_HOT", kDefaultL1Hot));
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (c.grid > sms) c.grid = sms;
+    c.solve = nullptr;
+    return c;
+  }
   const int hot = env_int("PSI_SMEM_HOT", kDefaultSmemHot);
   const int l1 = env_int("PSI_L1_HOT", kDefaultL1Hot);
   if (tile == 512) {

@@ -284,6 +284,9 @@ def test_repeated_iterate_on_one_context(gpu):
     {"PSI_HEAVY": "1", "PSI_HEAVY_MIN": "2", "PSI_HEAVY_LABELS": "24576"},   # nearly every row heavy
     {"PSI_HEAVY": "1", "PSI_HEAVY_MIN": "16"},              # default H, more heavy rows
     {"PSI_HEAVY": "1"},                                     # library defaults, forced on
+    {"PSI_HEAVY": "1", "PSI_OVERLAP": "1"},                 # k_heavy || k_tiles (overlapped plan)
+    {"PSI_HEAVY": "1", "PSI_OVERLAP": "1", "PSI_HEAVY_MIN": "2", "PSI_HEAVY_LABELS": "24576"},
+    {"PSI_HEAVY": "1", "PSI_OVERLAP": "0"},                 # serial plan
 ])
 def test_heavy_rows_parity(gpu, env, monkeypatch):
     """psi_build_graph reads the heavy-row knobs; every split of the work between k_heavy
@@ -298,6 +301,8 @@ def test_heavy_rows_parity(gpu, env, monkeypatch):
     else:
         assert info["n_heavy"] > 0 and info["heavy_entries"] > 0 and info["heavy_panels"] > 0
         assert info["tile_edges"] == 1024
+        if "PSI_OVERLAP" in env:
+            assert info["overlapped"] == int(env["PSI_OVERLAP"])
 
 
 def test_heavy_hub_many_slots(gpu, monkeypatch):

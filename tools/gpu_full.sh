@@ -10,6 +10,6 @@ timeout 1200 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$T
 cat gpurun_out/bench_$TAG.json
 if [ "${NCU:-1}" = "1" ]; then
 PSI_GRAPH=0 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv \
-  --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-batch \
+  --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-batch --no-configs \
   > gpurun_out/ncu_launch_$TAG.log 2>&1; echo ncu_launch=$?
 fi
