@@ -577,58 +577,70 @@ __global__ void k_heavy_fill(const unsigned long long* keys, long long nk, const
 // A run keeps its order where it crosses a block boundary (so every block is independent:
 // one lane per block, a warp per list) and when it is longer than 32.  Deterministic.
 constexpr int kBalBlock = 128;
+// blocks of 128 positions of every list (the balance kernel's work items)
+__global__ void k_list_blocks(const long long* lstart, long long nlists, long long* nb) {
+  GRID_STRIDE(L, nlists) nb[L] = (lstart[L + 1] - lstart[L] + 127) >> 7;
+}
+// one thread per (list, 128-position block): bs = exclusive scan of the blocks per list
 __global__ void __launch_bounds__(kBalBlock) k_heavy_balance(const unsigned* in, unsigned* out,
                                                              const long long* loff,
                                                              const long long* lstart,
+                                                             const long long* bs,
                                                              long long nlists, int sh) {
   __shared__ unsigned long long cnt[8][kBalBlock];   // 16 four-bit counters per instruction k
-  const int t = threadIdx.x, lane = t & 31;
-  WARP_STRIDE(L, nlists) {
-    const long long b = loff[L], e_pad = loff[L + 1];
+  const int t = threadIdx.x;
+  const long long total = bs[nlists];
+  GRID_STRIDE(gb, total) {
+    long long lo = 0, hi = nlists;                   // list L: bs[L] <= gb < bs[L + 1]
+    while (hi - lo > 1) {
+      const long long mid = lo + ((hi - lo) >> 1);
+      if (bs[mid] <= gb) lo = mid; else hi = mid;
+    }
+    const long long L = lo;
+    const long long b = loff[L];
     const int len_l = (int)(lstart[L + 1] - lstart[L]);
     const unsigned* src = in + b;
     unsigned* dst = out + b;
-    for (long long i = b + len_l + lane; i < e_pad; i += 32) out[i] = in[i];   // null padding
-    const int nblk = (len_l + 127) >> 7;
-    for (int B = lane; B < nblk; B += 32) {
-      const int q0 = B << 7, q1 = min(q0 + 128, len_l);
-      for (int k = 0; k < 8; ++k) cnt[k][t] = 0ull;
-      auto count = [&](int q, unsigned w) {
-        const unsigned long long c = cnt[q & 7][t];
-        const unsigned bk = w & 15;
-        if (((c >> (4 * bk)) & 15ull) < 15ull) cnt[q & 7][t] = c + (1ull << (4 * bk));
-      };
-      int q = q0;
-      if (q0 > 0) {                                   // the tail of a run from the last block
-        const unsigned sl = src[q0 - 1] >> sh;
-        while (q < q1 && (src[q] >> sh) == sl) { dst[q] = src[q]; count(q, src[q]); ++q; }
-      }
-      while (q < q1) {                                // runs starting in this block
-        const unsigned sl = src[q] >> sh;
-        int r = q + 1;
-        while (r < len_l && (src[r] >> sh) == sl) ++r;
-        const int in_blk = min(r, q1) - q;            // entries placed inside the block
-        if (r - q > 32) {
-          for (int i = 0; i < in_blk; ++i) { dst[q + i] = src[q + i]; count(q + i, src[q + i]); }
-        } else {
-          unsigned w[32];
-          for (int j = 0; j < in_blk; ++j) w[j] = src[q + j];
-          unsigned used = 0;
-          for (int i = 0; i < in_blk; ++i) {
-            const unsigned long long c = cnt[(q + i) & 7][t];
-            int bj = 0, bv = 1 << 30;
-            for (int j = 0; j < in_blk; ++j) {
-              if ((used >> j) & 1u) continue;
-              const int v = (int)((c >> (4 * (w[j] & 15))) & 15ull);
-              if (v < bv) { bv = v; bj = j; }
-            }
-            used |= 1u << bj;
-            dst[q + i] = w[bj];
-            count(q + i, w[bj]);
+    const int B = (int)(gb - bs[L]);
+    const int q0 = B << 7, q1 = min(q0 + 128, len_l);
+    if (q1 == len_l)                                  // the list's null padding stays last
+      for (long long i = b + len_l; i < loff[L + 1]; ++i) out[i] = in[i];
+    for (int k = 0; k < 8; ++k) cnt[k][t] = 0ull;
+    auto count = [&](int q, unsigned w) {
+      const unsigned long long c = cnt[q & 7][t];
+      const unsigned bk = w & 15;
+      if (((c >> (4 * bk)) & 15ull) < 15ull) cnt[q & 7][t] = c + (1ull << (4 * bk));
+    };
+    int q = q0;
+    if (q0 > 0) {                                     // the tail of a run from the last block
+      const unsigned sl = src[q0 - 1] >> sh;
+      while (q < q1 && (src[q] >> sh) == sl) { dst[q] = src[q]; count(q, src[q]); ++q; }
+    }
+    while (q < q1) {                                  // runs starting in this block
+      const unsigned sl = src[q] >> sh;
+      int r = q + 1;
+      while (r < len_l && (src[r] >> sh) == sl) ++r;
+      const int in_blk = min(r, q1) - q;              // entries placed inside the block
+      if (r - q > 32) {
+        for (int i = 0; i < in_blk; ++i) { dst[q + i] = src[q + i]; count(q + i, src[q + i]); }
+      } else {
+        unsigned w[32];
+        for (int j = 0; j < in_blk; ++j) w[j] = src[q + j];
+        unsigned used = 0;
+        for (int i = 0; i < in_blk; ++i) {
+          const unsigned long long c = cnt[(q + i) & 7][t];
+          int bj = 0, bv = 1 << 30;
+          for (int j = 0; j < in_blk; ++j) {
+            if ((used >> j) & 1u) continue;
+            const int v = (int)((c >> (4 * (w[j] & 15))) & 15ull);
+            if (v < bv) { bv = v; bj = j; }
           }
+          used |= 1u << bj;
+          dst[q + i] = w[bj];
+          count(q + i, w[bj]);
         }
-        q = min(r, q1);                               // the rest belongs to the next block
       }
+      q = min(r, q1);                                 // the rest belongs to the next block
     }
   }
 }
@@ -912,8 +924,20 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   if (env_int("PSI_HEAVY_BALANCE", 1) != 0) {
     unsigned* bal = nullptr;
     IG_CK(dev_alloc(&bal, (size_t)std::max<long long>(total, 4) * sizeof(unsigned), s));
-    k_heavy_balance<<<grid_for(nlists * 32, kBalBlock, 148 * 64), kBalBlock, 0, s>>>(
-        out.h_ent, bal, out.h_loff, lstart.as<long long>(), nlists, sh);
+    Tmp nb, bs, bscan;
+    IG_CK(nb.alloc((size_t)(nlists + 1) * sizeof(long long)));
+    IG_CK(bs.alloc((size_t)(nlists + 1) * sizeof(long long)));
+    IG_CK(cudaMemsetAsync(nb.as<long long>() + nlists, 0, sizeof(long long), s));
+    k_list_blocks<<<grid_for(nlists, 256), 256, 0, s>>>(lstart.as<long long>(), nlists,
+                                                        nb.as<long long>());
+    size_t bb = 0;
+    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, bb, nb.as<long long>(), bs.as<long long>(),
+                                        nlists + 1, s));
+    IG_CK(bscan.alloc(bb));
+    IG_CK(cub::DeviceScan::ExclusiveSum(bscan.p, bb, nb.as<long long>(), bs.as<long long>(),
+                                        nlists + 1, s));
+    k_heavy_balance<<<grid_for((n_ent >> 7) + nlists, kBalBlock, 148 * 64), kBalBlock, 0, s>>>(
+        out.h_ent, bal, out.h_loff, lstart.as<long long>(), bs.as<long long>(), nlists, sh);
     IG_CK(cudaGetLastError());
     IG_CK(cudaFreeAsync(out.h_ent, s));
     out.h_ent = bal;
