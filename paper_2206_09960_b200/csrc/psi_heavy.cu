@@ -101,21 +101,21 @@ __device__ __forceinline__ void process_chunk(const unsigned (&w)[8], const doub
   // = a segmented inclusive scan of the lane's tail run with resets f_l = !(single_l && cont_l).
   const unsigned prev_last = __shfl_up_sync(kFull, sl[7], 1);
   const bool cont = lane == 0 ? (sl[0] == carry_slot) : (sl[0] == prev_last);
-  int f = !(single && cont);
+  // segment starts from one ballot (no flag shuffles): lane l's segment starts at the highest
+  // reset lane <= l, so a Kogge-Stone step adds lane l-o's partial iff l-o >= that start
+  const unsigned fmask = __ballot_sync(kFull, !(single && cont));
+  const unsigned below = fmask & (0xffffffffu >> (31 - lane));     // reset lanes <= lane
+  const int start = below ? 31 - __clz(below) : -1;
   double val = acc[7];
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const double v2 = __shfl_up_sync(kFull, val, o);
-    const int f2 = __shfl_up_sync(kFull, f, o);
-    if (lane >= o) {
-      val = f ? val : val + v2;
-      f |= f2;
-    }
+    if (lane - o >= start && lane >= o) val += v2;
   }
-  const double out = f ? val : val + carry;          // chain reaching back to the carry
+  const double out = start >= 0 ? val : val + carry;  // chain reaching back to the carry
   double in = __shfl_up_sync(kFull, out, 1);
   if (lane == 0) in = carry;
-  const bool next_cont = __shfl_down_sync(kFull, cont, 1);
+  const bool next_cont = (__ballot_sync(kFull, cont) >> ((lane + 1) & 31)) & 1u;
   // run ends: k < 7 inside the lane (the first one, the head, continues a run from earlier
   // lanes when cont), 7 = the lane's tail when the next lane starts another slot, 8 = the
   // carried run that ended at the chunk boundary (lane 0)

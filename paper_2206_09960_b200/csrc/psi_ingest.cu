@@ -561,7 +561,8 @@ __global__ void k_heavy_fill(const unsigned long long* keys, long long nk, const
   GRID_STRIDE(i, nk) {
     const unsigned long long k = keys[i];
     const long long L = (long long)(k >> kEntBits);
-    ent[loff[L] + (i - lstart[L])] = (unsigned)(k & ((1ull << kEntBits) - 1));
+    const unsigned w = (unsigned)(k & ((1ull << kEntBits) - 1));
+    ent[loff[L] + (i - lstart[L])] = w;
   }
 }
 

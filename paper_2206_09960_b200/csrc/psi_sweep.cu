@@ -199,10 +199,17 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
 #endif
       PSI_ASSERT((double)lab <= A.n_users);             // sentinel label n holds x = 0
       fl |= (w[q] >> 31) << q;
+#if defined(PSI_EXP_ONELOAD)                // experiment builds: one global load variant,
+      if (lab < hs) v[q] = hot[lab];          // the L2 policy chosen per lane
+      else v[q] = COH ? __ldcg(xs + lab)
+                      : (PSI_EXP_ONELOAD == 1 ? ld_hint_na(xs + lab, lab < hot_lim ? pl : pf)
+                                              : ld_hint(xs + lab, lab < hot_lim ? pl : pf));
+#else
       if (lab < hs) v[q] = hot[lab];
       else if (lab < l1_lim) v[q] = ldx<COH>(xs + lab, pl, 0);
       else if (lab >= single_lo) v[q] = ldx<COH>(xs + lab, pf, 1);
       else v[q] = ldx<COH>(xs + lab, lab < hot_lim ? pl : pf, 2);
+#endif
     }
     if (tid == 0)
       sm.next_flag = (k + 1 >= ntiles) ? 1 : (int)(ld_stream(A.edges + (size_t)(k + 1) * (TB * kEpt), pf) >> 31);
@@ -222,21 +229,23 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
       if ((fl >> q) & 1u) run = 0.0;
       run += v[q];
     }
-    // scan element: (has flag, partial of the row open at the thread's end)
-    int f_in = nf > 0;
+    // scan element: (has flag, partial of the row open at the thread's end).  Flags and flag
+    // counts come from ballots (no integer shuffles): a lane's segment starts at the highest
+    // flagged lane <= it, so a Kogge-Stone step adds lane l-o's partial iff l-o >= that start;
+    // the inclusive count of row flags is summed over the 4 bit planes of nf (0..8).
+    const unsigned le = 0xffffffffu >> (31 - lane);                 // lanes <= this one
+    const unsigned below = __ballot_sync(kFull, nf > 0) & le;
+    const int start = below ? 31 - __clz(below) : -1;
+    int n_in = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) n_in += __popc(__ballot_sync(kFull, (nf >> b) & 1) & le) << b;
     double v_in = run;            // tail if a flag was seen, total otherwise
-    int n_in = nf;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int n2 = __shfl_up_sync(kFull, n_in, o);
       const double v2 = __shfl_up_sync(kFull, v_in, o);
-      const int f2 = __shfl_up_sync(kFull, f_in, o);
-      if (lane >= o) {
-        n_in += n2;
-        if (!f_in) v_in += v2;
-        f_in |= f2;
-      }
+      if (lane >= o && lane - o >= start) v_in += v2;
     }
+    const int f_in = start >= 0;
     if (lane == 31) { sm.wv[warp] = v_in; sm.wf[warp] = f_in; sm.wn[warp] = n_in; }
     if (G == 1) __syncthreads(); else group_bar<TB>(1 + grp);
     const int next_flag = sm.next_flag;
