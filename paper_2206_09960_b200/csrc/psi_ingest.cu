@@ -252,8 +252,14 @@ __global__ void k_norm_long(const int* list, int nlist, const int* loff, const i
   }
 }
 
+// 1/Wt per user, once (the column sums below gather it per edge instead of dividing per edge:
+// the same rounded reciprocals, so the same sums)
+__global__ void k_recip(const double* wt, long long n, double* iw) {
+  GRID_STRIDE(i, n) iw[i] = 1.0 / wt[i];
+}
+
 // column sums of B = lambda_i sum_{j in F(i)} 1/W_j: thread per short leader row ...
-__global__ void k_kappa_col_short(const int* rp, const int* idx, const double* wt,
+__global__ void k_kappa_col_short(const int* rp, const int* idx, const double* iw,
                                   const double* lam, int n, unsigned long long* kmax) {
   for (long long base = blockIdx.x * (long long)blockDim.x; base < n;
        base += (long long)gridDim.x * blockDim.x) {
@@ -263,7 +269,7 @@ __global__ void k_kappa_col_short(const int* rp, const int* idx, const double* w
       const int b = rp[i], e = rp[i + 1];
       if (e > b && e - b <= kShort) {
         double s = 0.0;
-        for (int q = b; q < e; ++q) s += 1.0 / wt[idx[q]];
+        for (int q = b; q < e; ++q) s += iw[idx[q]];
         m = dbits(lam[i] * s);
       }
     }
@@ -274,13 +280,13 @@ __global__ void k_kappa_col_short(const int* rp, const int* idx, const double* w
 
 // ... and a warp per long one
 __global__ void k_kappa_col_long(const int* list, int nlist, const int* rp, const int* idx,
-                                 const double* wt, const double* lam, unsigned long long* kmax) {
+                                 const double* iw, const double* lam, unsigned long long* kmax) {
   const int lane = threadIdx.x & 31;
   WARP_STRIDE(k, nlist) {
     const int i = list[k];
     const int b = rp[i], e = rp[i + 1];
     double s = 0.0;
-    for (int q = b + lane; q < e; q += 32) s += 1.0 / wt[idx[q]];
+    for (int q = b + lane; q < e; q += 32) s += iw[idx[q]];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
     if (lane == 0) atomicMax(kmax + 2, dbits(lam[i] * s));
@@ -1218,12 +1224,17 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
           longu.as<int>(), (int)nlong, loff.as<int>(), vals.Current(), lm.as<double2>(),
           a_old.as<double>(), g_old.as<double>(), wt_old.as<double>(), d_old.as<double>(),
           first_leader.as<int>(), kmax);
-    k_kappa_col_short<<<grid_for(n, 256), 256, 0, s>>>(rp, idx_in, wt_old.as<double>(), lam, N, kmax);
-    nlong = long_segments(rp, nullptr, N, kShort, s, longu);
-    if (nlong < 0) IG_CK(cudaErrorMemoryAllocation);
-    if (nlong > 0)
-      k_kappa_col_long<<<grid_for(nlong * 32, 256), 256, 0, s>>>(longu.as<int>(), (int)nlong, rp,
-                                                                 idx_in, wt_old.as<double>(), lam, kmax);
+    {
+      Tmp iw;
+      IG_CK(iw.alloc((size_t)n * sizeof(double)));
+      k_recip<<<grid_for(n, 256), 256, 0, s>>>(wt_old.as<double>(), n, iw.as<double>());
+      k_kappa_col_short<<<grid_for(n, 256), 256, 0, s>>>(rp, idx_in, iw.as<double>(), lam, N, kmax);
+      nlong = long_segments(rp, nullptr, N, kShort, s, longu);
+      if (nlong < 0) IG_CK(cudaErrorMemoryAllocation);
+      if (nlong > 0)
+        k_kappa_col_long<<<grid_for(nlong * 32, 256), 256, 0, s>>>(longu.as<int>(), (int)nlong, rp,
+                                                                   idx_in, iw.as<double>(), lam, kmax);
+    }
     if (nprof > 1) {
       // the constants (a, g, Wt, d) and ||B||_row of every profile, old labels, same kernels
       IG_CK(bold.alloc((size_t)nprof * 4 * n * sizeof(double)));

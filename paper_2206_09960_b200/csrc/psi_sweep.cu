@@ -298,7 +298,8 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
       } else {
         const unsigned long long px = (unsigned)r < hot_lim ? pl : pf;
         const double xn = fma(ld_stream(A.g + r, pf), Sr, ld_stream(acon + r, pf));
-        eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - ldx<COH>(xs + r, px, 2));
+        const double xp = ldx<COH>(xs + r, px, 2);
+        eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - xp);
         st_hint(xd + r, xn, st_last ? px : pf);
       }
     }
