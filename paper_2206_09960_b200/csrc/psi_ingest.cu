@@ -324,6 +324,30 @@ __global__ void k_classify(const int* rp, const int* nlead, int n, unsigned char
 //   stage 2: single-leader users whose leader is labelled, key = label(leader) << 32 | u
 //   stage 3: remaining single-leader users (cycles), key = leader << 32 | u
 //   stage 4: follower-less users, key = u
+// one level of the single-leader relabel over the still-unlabelled single-leader users only
+// (pend, ascending user ids): ready = the leader has a label -> key label(leader) << 32 | u
+__global__ void k_level_keys(const int* pend, long long np, const int* first_leader,
+                             const int* new_of_old, unsigned long long* key, unsigned char* ready,
+                             unsigned char* keep) {
+  GRID_STRIDE(i, np) {
+    const int u = pend[i];
+    const int lab = new_of_old[first_leader[u]];
+    key[i] = ((unsigned long long)(lab >= 0 ? lab : 0) << 32) | (unsigned)u;
+    ready[i] = lab >= 0;
+    keep[i] = lab < 0;
+  }
+}
+__global__ void k_cycle_keys(const int* pend, long long np, const int* first_leader,
+                             unsigned long long* key) {
+  GRID_STRIDE(i, np) {
+    const int u = pend[i];
+    key[i] = ((unsigned long long)first_leader[u] << 32) | (unsigned)u;
+  }
+}
+__global__ void k_single_flags(const unsigned char* cls, int n, unsigned char* flag) {
+  GRID_STRIDE(u, n) flag[u] = cls[u] == C_SINGLE;
+}
+
 __global__ void k_stage_keys(int stage, const unsigned char* cls, const int* nlead,
                              const int* first_leader, const int* new_of_old, int n,
                              unsigned long long* key, unsigned char* flag) {
@@ -1349,6 +1373,16 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   IG_CK(cub::DeviceSelect::Flagged(nullptr, sel_bytes, key.as<unsigned long long>(),
                                    flag8.as<unsigned char>(), sel.as<unsigned long long>(),
                                    nsel.as<long long>(), N, s));
+  {
+    // the level loop also selects int lists (user ids, a counting iterator): room for those too
+    size_t b_it = 0, b_int = 0;
+    cub::CountingInputIterator<int> it0(0);
+    IG_CK(cub::DeviceSelect::Flagged(nullptr, b_it, it0, flag8.as<unsigned char>(), (int*)nullptr,
+                                     nsel.as<long long>(), N, s));
+    IG_CK(cub::DeviceSelect::Flagged(nullptr, b_int, (const int*)nullptr, flag8.as<unsigned char>(),
+                                     (int*)nullptr, nsel.as<long long>(), N, s));
+    sel_bytes = std::max(sel_bytes, std::max(b_it, b_int));
+  }
   IG_CK(stage_tmp.alloc(sel_bytes));
   IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, sel.as<unsigned long long>(),
                                        sorted.as<unsigned long long>(), N, 32, 64, s));
@@ -1388,12 +1422,60 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   if ((rc = run_stage(0, true, &c)) != PSI_OK) return rc;          // hot, by leader count
   if ((rc = run_stage(1, false, &c)) != PSI_OK) return rc;         // leaderless active
   out.single_lo = base;                                            // single-leader users follow
-  while (true) {                                                   // single-leader, by level
-    if ((rc = run_stage(2, true, &c)) != PSI_OK) return rc;
-    if (c == 0) break;
-    ++levels;
+  {
+    // single-leader users level by level (stage 2 of k_stage_keys), each level scanning only
+    // the users still unlabelled (a pass over all n per level cost ~0.5 ms x ~50 levels at
+    // C5); same keys, same stable order, so the same labels
+    Tmp pend, pend2, rdy, kp;
+    IG_CK(pend.alloc((size_t)n * sizeof(int)));
+    IG_CK(pend2.alloc((size_t)n * sizeof(int)));
+    IG_CK(rdy.alloc((size_t)n));
+    IG_CK(kp.alloc((size_t)n));
+    k_single_flags<<<grid_for(n, 256), 256, 0, s>>>(cls.as<unsigned char>(), N, flag8.as<unsigned char>());
+    cub::CountingInputIterator<int> it(0);
+    size_t b0 = sel_bytes;
+    IG_CK(cub::DeviceSelect::Flagged(stage_tmp.p, b0, it, flag8.as<unsigned char>(), pend.as<int>(),
+                                     nsel.as<long long>(), N, s));
+    long long np = 0;
+    IG_CK(cudaMemcpyAsync(&np, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+    while (np > 0) {
+      k_level_keys<<<grid_for(np, 256), 256, 0, s>>>(pend.as<int>(), np, first_leader.as<int>(),
+                                                    new_of_old.as<int>(), key.as<unsigned long long>(),
+                                                    rdy.as<unsigned char>(), kp.as<unsigned char>());
+      size_t b1 = sel_bytes;
+      IG_CK(cub::DeviceSelect::Flagged(stage_tmp.p, b1, key.as<unsigned long long>(),
+                                       rdy.as<unsigned char>(), sel.as<unsigned long long>(),
+                                       nsel.as<long long>(), (int)np, s));
+      long long cl = 0;
+      IG_CK(cudaMemcpyAsync(&cl, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+      IG_CK(cudaStreamSynchronize(s));
+      if (cl == 0) break;
+      size_t b2 = sort_bytes;
+      IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp2.p, b2, sel.as<unsigned long long>(),
+                                           sorted.as<unsigned long long>(), (int)cl, 32, 64, s));
+      k_assign<<<grid_for(cl, 256), 256, 0, s>>>(sorted.as<unsigned long long>(), cl, base,
+                                                new_of_old.as<int>(), out.old_of_new);
+      base += (int)cl;
+      ++levels;
+      size_t b3 = sel_bytes;
+      IG_CK(cub::DeviceSelect::Flagged(stage_tmp.p, b3, pend.as<int>(), kp.as<unsigned char>(),
+                                       pend2.as<int>(), nsel.as<long long>(), (int)np, s));
+      IG_CK(cudaMemcpyAsync(&np, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+      IG_CK(cudaStreamSynchronize(s));
+      std::swap(pend.p, pend2.p);
+    }
+    if (np > 0) {                                      // leftovers (cycles), stage 3's keys
+      k_cycle_keys<<<grid_for(np, 256), 256, 0, s>>>(pend.as<int>(), np, first_leader.as<int>(),
+                                                    sel.as<unsigned long long>());
+      size_t b2 = sort_bytes;
+      IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp2.p, b2, sel.as<unsigned long long>(),
+                                           sorted.as<unsigned long long>(), (int)np, 32, 64, s));
+      k_assign<<<grid_for(np, 256), 256, 0, s>>>(sorted.as<unsigned long long>(), np, base,
+                                                new_of_old.as<int>(), out.old_of_new);
+      base += (int)np;
+    }
   }
-  if ((rc = run_stage(3, true, &c)) != PSI_OK) return rc;          // leftovers (cycles)
   if (base != out.n_act) {
     snprintf(msg, msg_len, "internal: relabel covered %d of %lld active users", base, out.n_act);
     return PSI_E_CUDA;
