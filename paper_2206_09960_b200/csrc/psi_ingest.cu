@@ -557,12 +557,18 @@ __global__ void k_heavy_keys(const int* hot, const long long* hoff, const int2* 
     const int2 sn = rslot[r];
     const int p = row_panel[r];
     const int base = pslot_base[p];
+    // the i-th hot follower goes to slot k = i % nv (round robin); its key is written at the
+    // row's position off_k + i / nv, so the row's keys are in slot order and a stable sort by
+    // list alone leaves every list grouped by slot (rows, hence slots, ascend within a list)
+    const long long h = e - b, qv = h / sn.y, rv = h % sn.y;
     for (long long q = b + lane; q < e; q += 32) {
       const unsigned lab = (unsigned)hot[q];
-      const int slot = sn.x + (int)((q - b) % sn.y);
+      const long long i = q - b, k = i % sn.y;
+      const int slot = sn.x + (int)k;
       const unsigned long long list =
           ((unsigned long long)p * warps + slot_warp[base + slot]) * nseg + (lab >> sh);
-      keys[q] = (list << kEntBits) | ((unsigned long long)slot << sh) | (lab & ((1u << sh) - 1));
+      keys[b + k * qv + (k < rv ? k : rv) + i / sn.y] =
+          (list << kEntBits) | ((unsigned long long)slot << sh) | (lab & ((1u << sh) - 1));
     }
   }
 }
@@ -842,11 +848,14 @@ namespace {
 // virtual rows of <= vmax entries, contiguous slot ranges per consumer warp balanced by
 // entries; then the entry lists (panel, segment, warp) sorted by (slot, label).
 int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcnt, Tmp& hoff,
-                     cudaStream_t s, char* msg, size_t msg_len) {
+                     cudaStream_t s, Trace& tr, char* msg, size_t msg_len) {
   const int nseg = out.nseg;
   const int sh = out.heavy_seg_shift;
   const int HW = out.heavy_warps, SLOTS = out.heavy_slots;
-  std::vector<long long> hc(NH);
+  // host buffers of the plan are thread_local and keep their capacity: fresh multi-MB vectors
+  // cost ~1 page fault per 4 KB on every build (~40 ms at C5, measured)
+  static thread_local std::vector<long long> hc;
+  hc.resize(NH);
   IG_CK(cudaMemcpyAsync(hc.data(), hcnt.p, (size_t)NH * sizeof(long long), cudaMemcpyDeviceToHost, s));
   // the hot followers of each row stay in input order: the entries are sorted by
   // (list, slot, label) below, and the round-robin virtual-row split only needs a fixed order
@@ -858,47 +867,55 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   const long long pps = std::max(1, env_int("PSI_HEAVY_PPS", kDefaultHeavyPPS));
   const long long e_panel = std::max<long long>((n_ent + pps * sms - 1) / (pps * sms), 32768);
   const long long vmax = std::max<long long>(e_panel / (2 * HW), 64);
-  std::vector<int> prow{0}, row_panel(NH), pslot_base{0}, wslot;
-  std::vector<int2> rslot(NH);
-  std::vector<unsigned char> slot_warp;
-  std::vector<long long> slot_w;
+  static thread_local std::vector<int> prow, row_panel, pslot_base, wslot;
+  static thread_local std::vector<int2> rslot;
+  static thread_local std::vector<unsigned char> slot_warp;
+  prow.assign(1, 0);
+  pslot_base.assign(1, 0);
+  wslot.clear();
+  row_panel.resize(NH);
+  rslot.resize(NH);
+  slot_warp.clear();
+  slot_warp.reserve((size_t)NH + (size_t)(n_ent / vmax) + 1);
+  std::vector<long long> slot_w(SLOTS);          // entries of each slot of the open panel
+  std::vector<int> ws(HW + 1);
+  int nslots = 0;
   long long p_ent = 0;
   auto close_panel = [&](int r_end) {
-    const int slots = (int)slot_w.size();
     long long T = 0;
-    for (long long x : slot_w) T += x;
-    std::vector<int> ws(HW + 1, slots);
+    for (int k = 0; k < nslots; ++k) T += slot_w[k];
+    std::fill(ws.begin(), ws.end(), nslots);
     ws[0] = 0;
     long long acc = 0;
     int w = 1;
-    for (int k = 0; k < slots && w < HW; ++k) {
+    for (int k = 0; k < nslots && w < HW; ++k) {
       acc += slot_w[k];
       while (w < HW && acc * HW >= T * w) ws[w++] = k + 1;
     }
-    int owner = 0;
-    for (int k = 0; k < slots; ++k) {
-      while (owner + 1 < HW && ws[owner + 1] <= k) ++owner;
-      slot_warp.push_back((unsigned char)owner);
-    }
+    for (int o = 0; o < HW; ++o) slot_warp.insert(slot_warp.end(), ws[o + 1] - ws[o], (unsigned char)o);
     wslot.insert(wslot.end(), ws.begin(), ws.end());
     prow.push_back(r_end);
-    pslot_base.push_back(pslot_base.back() + slots);
-    slot_w.clear();
+    pslot_base.push_back(pslot_base.back() + nslots);
+    nslots = 0;
     p_ent = 0;
   };
   for (int r = 0; r < NH; ++r) {
-    long long nv = hc[r] > 0 ? (hc[r] + vmax - 1) / vmax : 0;
+    const long long h = hc[r];
+    long long nv = h > 0 ? (h + vmax - 1) / vmax : 0;
     if (nv > SLOTS) nv = SLOTS;
-    if (r > prow.back() && ((long long)slot_w.size() + nv > SLOTS || p_ent + hc[r] > e_panel))
-      close_panel(r);
-    rslot[r] = make_int2((int)slot_w.size(), (int)nv);
+    if (r > prow.back() && (nslots + nv > SLOTS || p_ent + h > e_panel)) close_panel(r);
+    rslot[r] = make_int2(nslots, (int)nv);
     row_panel[r] = (int)prow.size() - 1;
-    for (long long k = 0; k < nv; ++k) slot_w.push_back(hc[r] / nv + (k < hc[r] % nv ? 1 : 0));
-    p_ent += hc[r];
+    if (nv > 0) {
+      const long long q = h / nv, rem = h % nv;  // slot k of the row: q (+1 for k < rem) entries
+      for (long long k = 0; k < nv; ++k) slot_w[nslots++] = q + (k < rem ? 1 : 0);
+    }
+    p_ent += h;
   }
   close_panel(NH);
   const int npanels = (int)prow.size() - 1;
   out.npanels = npanels;
+  tr.mark("  heavy: host panel plan");
   out.heavy_entries = n_ent;
 
   IG_CK(dev_alloc(&out.h_prow, prow.size() * sizeof(int), s));
@@ -928,12 +945,14 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   cub::DoubleBuffer<unsigned long long> kb(keys.as<unsigned long long>(), keys2.as<unsigned long long>());
   if (n_ent > 0) {
     size_t tb = 0;
-    // by (list, slot) only: the offset bits below sh need no order (stable sort keeps
-    // the hot-list order inside a slot's run -- fixed, so the sums stay deterministic)
-    IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, (int)n_ent, sh, end_bit, s));
+    // by list only: k_heavy_keys wrote every row's keys in slot order and rows ascend within a
+    // list, so the stable sort leaves each list grouped by slot, each slot's entries in the
+    // hot-list order (fixed, so the sums stay deterministic) -- 3 radix passes instead of 5
+    IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, kb, (int)n_ent, kEntBits, end_bit, s));
     IG_CK(sort_tmp.alloc(tb));
-    IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp.p, tb, kb, (int)n_ent, sh, end_bit, s));
+    IG_CK(cub::DeviceRadixSort::SortKeys(sort_tmp.p, tb, kb, (int)n_ent, kEntBits, end_bit, s));
   }
+  tr.mark("  heavy: keys + sort");
   IG_CK(lstart.alloc((size_t)(nlists + 1) * sizeof(long long)));
   IG_CK(plen.alloc((size_t)(nlists + 1) * sizeof(long long)));
   k_list_start<<<grid_for(nlists + 1, 256), 256, 0, s>>>(kb.Current(), n_ent, nlists,
@@ -952,6 +971,7 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
   k_fill_u32<<<grid_for(total, 256), 256, 0, s>>>(out.h_ent, total, (unsigned)SLOTS << sh);
   k_heavy_fill<<<grid_for(n_ent, 256), 256, 0, s>>>(kb.Current(), n_ent, lstart.as<long long>(),
                                                    out.h_loff, out.h_ent);
+  tr.mark("  heavy: lists + fill");
   if (env_int("PSI_HEAVY_BALANCE", 1) != 0) {
     unsigned* bal = nullptr;
     IG_CK(dev_alloc(&bal, (size_t)std::max<long long>(total, 4) * sizeof(unsigned), s));
@@ -1565,7 +1585,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   }
   tr.mark("edge stream");
   if (NH > 0) {
-    int rc2 = build_heavy_plan(out, NH, n_hot_ent, hot, hcnt, hoff, s, msg, msg_len);
+    int rc2 = build_heavy_plan(out, NH, n_hot_ent, hot, hcnt, hoff, s, tr, msg, msg_len);
     if (rc2 != PSI_OK) return rc2;
   }
   hot.reset();
