@@ -1,4 +1,5 @@
-"""Every kernel (ingest, k_heavy, k_tiles, k_fix, readout, PageRank, Power-NF, unpermute) run by
+"""Every kernel (ingest, k_heavy, k_tiles, k_fix, readout, PageRank, Power-NF, unpermute; the
+serial and the overlapped plan) run by
 the device bounds-checked build (lib/libpsi_checked.so, -DPSI_CHECKS: label, row, slot, panel
 and leader indices are checked and trap on a violation) -- the stand-in for compute-sanitizer,
 which is closed on the GPU pool."""
@@ -22,4 +23,4 @@ def test_checked_build_runs_every_kernel(gpu):
                          capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "PSI_CHECKS" not in out.stdout + out.stderr
-    assert out.stdout.count("sum(psi)=") == 3
+    assert out.stdout.count("sum(psi)=") == 4 and "overlapped=1" in out.stdout

@@ -16,7 +16,8 @@ def main():
     import psigen
     os.environ["PSI_HEAVY"] = "1"
     os.environ["PSI_HEAVY_MIN"] = "8"
-    for cfg, scale in ((1, None), (5, 15), (3, 14)):
+    for cfg, scale, ovl in ((1, None, "0"), (5, 15, "0"), (3, 14, "0"), (5, 15, "1")):
+        os.environ["PSI_OVERLAP"] = ovl         # the overlapped plan's kernels too (last pass)
         w = psigen.make_config(cfg, scale=scale)
         dev = [torch.from_numpy(a).cuda() for a in (w.row_ptr, w.followers, w.lam, w.mu)]
         with psi.PsiGraph(*dev) as g:
@@ -32,7 +33,8 @@ def main():
             info = g.info()
         with psi.PsiGraph(w.row_ptr, w.followers, w.lam, w.mu) as g:   # host inputs
             g.iterate(w.eps)
-        print(f"config {cfg}: n={w.n} m={w.m} heavy={info['n_heavy']} sum(psi)={float(p.sum()):.12f}",
+        print(f"config {cfg}: n={w.n} m={w.m} heavy={info['n_heavy']} overlapped={info['overlapped']} "
+              f"sum(psi)={float(p.sum()):.12f}",
               flush=True)
 
 
