@@ -92,6 +92,10 @@ typedef struct psi_info {
   int64_t n_profiles;     /* activity profiles of the context (1, or k of psi_build_graph_batch) */
   int64_t tile_edges;     /* edges per tile of the sweep: 1024 with heavy rows, else 512 */
   int64_t overlapped;     /* 1: k_heavy and k_tiles run concurrently (the overlapped plan) */
+  int64_t sliced_ell;     /* 1: the sweep runs on the sliced-ELL layout (k_sell), 0: tiles */
+  int64_t sell_long_rows; /* rows summed in pieces by whole warps (stream length > lmax) */
+  int64_t sell_pieces;    /* their pieces */
+  int64_t sell_words;     /* index words of the slices (padding included) */
 } psi_info;
 
 /*

@@ -64,7 +64,9 @@ class psi_info(ctypes.Structure):
                 ("n_heavy", ctypes.c_int64), ("heavy_entries", ctypes.c_int64),
                 ("heavy_panels", ctypes.c_int64), ("heavy_labels", ctypes.c_int64),
                 ("last_solver", ctypes.c_int64), ("n_profiles", ctypes.c_int64),
-                ("tile_edges", ctypes.c_int64), ("overlapped", ctypes.c_int64)]
+                ("tile_edges", ctypes.c_int64), ("overlapped", ctypes.c_int64),
+                ("sliced_ell", ctypes.c_int64), ("sell_long_rows", ctypes.c_int64),
+                ("sell_pieces", ctypes.c_int64), ("sell_words", ctypes.c_int64)]
 
 
 _lib = None

@@ -96,6 +96,8 @@ struct psi_ctx {
   double pr_alpha = 0.0;
   double* hhot = nullptr;        // [n_heavy] heavy rows' sums over followers < H (k_heavy)
   double* scold = nullptr;       // [n_heavy] their edge-stream sums (overlapped sweep only)
+  double* ppart = nullptr;       // k_sell: long-row piece sums, their epochs, window eps_t
+  double* epsw = nullptr;
   int heavy_grid = 0;
   int heavy_block = 0;
   size_t heavy_smem = 0;
@@ -209,7 +211,9 @@ void free_ctx(psi_ctx* c) {
                   c->g.lam, c->g.psi, c->g.old_of_new, c->g.split, c->x[0], c->x[1],
                   c->p_in, c->p_out, c->eps_part1, c->eps_part2, c->history, c->st, c->prm,
                   c->hhot, c->g.h_ent, c->g.h_loff, c->g.h_prow, c->g.h_rslot, c->g.h_wslot,
-                  c->scold, c->g.hsplit};
+                  c->scold, c->g.hsplit, c->ppart, c->epsw, c->g.s_words,
+                  c->g.s_off, c->g.s_ipos, c->g.s_wrow, c->g.s_wstep, c->g.s_lrow, c->g.s_lp0, c->g.s_piece,
+                  c->g.s_lwords};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, c->stream);
   for (auto e : c->b.exec) if (e) cudaGraphExecDestroy(e);
@@ -277,6 +281,30 @@ SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   A.prm = c->prm;
   A.cond = cond;
   A.use_cond = 1;
+  if (c->g.sell) {
+    // the sliced-ELL sweep: no tiles, no split rows, eps_t partials per window (k_fix)
+    A.use_sell = 1;
+    A.nsplit = A.nsplit_long = 0;
+    A.grid1 = 0;
+    SellPlan& P = A.sell;
+    P.words = c->g.s_words;
+    P.soff = c->g.s_off;
+    P.ipos = c->g.s_ipos;
+    P.wrow = c->g.s_wrow;
+    P.wstep = c->g.s_wstep;
+    P.nwin = c->g.sell_nwin;
+    P.wmax = 1 << c->g.sell_shift;
+    P.lrow = c->g.s_lrow;
+    P.lp0 = c->g.s_lp0;
+    P.piece = c->g.s_piece;
+    P.lwords = c->g.s_lwords;
+    P.npieces = c->g.sell_npieces;
+    P.ppart = c->ppart;
+    P.epsw = c->epsw;
+    P.nwords = c->g.sell_words;
+    P.nlwords = c->g.sell_lwords;
+    P.nlong = c->g.sell_nlong;
+  }
   return A;
 }
 
@@ -841,7 +869,8 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
 
   // Iteration buffers.
-  c->tc = tiles_config(c->g.ntiles, n, c->g.tile, c->g.ovl != 0);
+  c->tc = c->g.sell ? sell_config(n, c->g.sell_shift)
+                    : tiles_config(c->g.ntiles, n, c->g.tile, c->g.ovl != 0);
   c->grid1 = c->tc.grid;
   {
     // Hot prefix of x kept in L2 (evict_last) in BOTH ping-pong buffers: PSI_HOT_MB per
@@ -860,6 +889,14 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
       if (atoi(e) > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
   }
   c->grid2 = fix_grid(c->g.nsplit);
+  if (c->g.sell) {
+    // k_fix finishes the long rows (thread each) and reduces the windows' eps_t partials (a
+    // few per thread), then the stop rule
+    c->grid2 = std::max(1, std::min(148, (std::max(c->g.sell_nwin, c->g.sell_nlong) + kFixBlock - 1) /
+                                             kFixBlock));
+    B_CK(dev_alloc(&c->ppart, (size_t)std::max(c->g.sell_npieces, 1) * sizeof(double), c->stream));
+    B_CK(dev_alloc(&c->epsw, (size_t)std::max(c->g.sell_nwin, 1) * sizeof(double), c->stream));
+  }
   if (c->g.ovl)                                       // + k_fix's pass over the heavy rows
     c->grid2 = std::max(c->grid2, (int)std::min<long long>((c->g.n_heavy + kFixBlock - 1) / kFixBlock,
                                                             148LL * 8));
@@ -1073,6 +1110,10 @@ psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
   out->n_profiles = c->g.nprof;
   out->tile_edges = c->g.tile;
   out->overlapped = (c->g.ovl && c->g.n_heavy > 0) ? 1 : 0;
+  out->sliced_ell = c->g.sell;
+  out->sell_long_rows = c->g.sell_nlong;
+  out->sell_pieces = c->g.sell_npieces;
+  out->sell_words = c->g.sell_words;
   return PSI_OK;
 }
 

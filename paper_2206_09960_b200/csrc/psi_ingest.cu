@@ -1070,6 +1070,296 @@ __global__ void k_long_split_flags(const int4* split, long long ns, unsigned cha
   GRID_STRIDE(i, ns) flag[i] = (split[i].z - split[i].y) > kLongSpan;
 }
 
+// ------------------------------------------------------------------ 8. sliced-ELL layout
+// (SellPlan, psi_internal.cuh; swept by k_sell).  Windows are runs of 32-row blocks, cut where
+// the cumulative stream length crosses a multiple of `ecap` edges or the row count reaches
+// 2^shift, so one window is a bounded work item.  Sort key of active row r inside window w:
+// w << 32 | (2047 - d') << 11 | (r - first row of w), d' = stream length (0 for long rows and
+// the padding rows of the last block) -- descending length, ascending row on ties.
+__global__ void k_sell_deg(const int* rp, int NA, long long na_pad, int lmax, int* dd,
+                           unsigned char* lflag) {
+  GRID_STRIDE(i, na_pad) {
+    int d = 0;
+    if (i < NA) {
+      d = rp[i + 1] - rp[i];
+      const bool lg = d > lmax;
+      lflag[i] = lg ? 1 : 0;
+      if (lg) d = 0;
+    }
+    dd[i] = d;
+  }
+}
+
+__global__ void k_sell_blocksum(const int* dd, long long nblk, long long* bsum) {
+  GRID_STRIDE(b, nblk) {
+    long long t = 0;
+    for (int j = 0; j < 32; ++j) t += dd[b * 32 + j];
+    bsum[b] = t;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) bsum[nblk] = 0;
+}
+
+// block b starts a window: the first block, every 2^shift rows, or where the edges before it
+// cross a multiple of ecap (pre = exclusive prefix of the block sums)
+__global__ void k_sell_wflag(const long long* pre, long long nblk, int shift, long long ecap,
+                             int* flag) {
+  GRID_STRIDE(b, nblk) {
+    const bool f = b == 0 || ((b << 5) & ((1LL << shift) - 1)) == 0 ||
+                   pre[b] / ecap != pre[b - 1] / ecap;
+    flag[b] = f ? 1 : 0;
+  }
+}
+
+__global__ void k_sell_wrow(const int* flag, const int* wid, long long nblk, int* wrow) {
+  GRID_STRIDE(b, nblk) if (flag[b]) wrow[wid[b] - 1] = (int)(b << 5);
+}
+
+__global__ void k_sell_keys(const int* dd, const int* wid, const int* wrow, long long na_pad,
+                            unsigned long long* keys) {
+  GRID_STRIDE(i, na_pad) {
+    const int w = wid[i >> 5] - 1;
+    const unsigned long long loc = (unsigned long long)(i - wrow[w]);
+    keys[i] = ((unsigned long long)w << 32) | ((unsigned long long)(2047 - dd[i]) << 11) | loc;
+  }
+}
+
+// sorted position i -> (slice i / 32, lane i % 32): its row (for the fill) and, per row, its
+// position inside its window (ipos: where k_sell leaves the row's sum; 0xffff for long rows,
+// which k_fix finishes from their pieces); the width of every slice is the length of its
+// first (longest) row
+__global__ void k_sell_perm(const unsigned long long* sorted, long long na_pad, const int* wrow,
+                            unsigned short* ipos, int* row_of_pos, unsigned* width) {
+  GRID_STRIDE(i, na_pad) {
+    const unsigned long long k = sorted[i];
+    const int w = (int)(k >> 32);
+    const int d = 2047 - (int)((k >> 11) & 2047u);
+    const int r = wrow[w] + (int)(k & 2047u);
+    ipos[r] = d > 0 ? (unsigned short)(i - wrow[w]) : (unsigned short)0xffff;
+    row_of_pos[i] = d > 0 ? r : -1;
+    if ((i & 31) == 0) width[i >> 5] = (unsigned)d;
+  }
+}
+
+// window w's index block: wstep[w] .. wstep[w + 1] steps (its slices' widths summed, rounded up
+// to a multiple of 8); ksteps[w] = the steps of its slices
+__global__ void k_sell_wsteps(const unsigned* soff, const int* wrow, int nwin, unsigned* ksteps) {
+  GRID_STRIDE(w, nwin) {
+    const unsigned k = soff[wrow[w + 1] >> 5] - soff[wrow[w] >> 5];
+    ksteps[w] = (k + 7u) & ~7u;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ksteps[nwin] = 0;
+}
+
+__global__ void k_fill_u32v(unsigned* p, long long n, unsigned v) { GRID_STRIDE(i, n) p[i] = v; }
+
+// warp per slice: lane l writes its row's followers (flag bit cleared) as steps k0 .. k0+d-1 of
+// its stream through the window, step k at word ((k / 8) * 32 + l) * 8 + k % 8 of the window's
+// block (one 32-byte load per lane per 8 steps in k_sell); the sentinel label below a shorter
+// row's end
+__global__ void k_sell_fill(const int* row_of_pos, const unsigned* soff, long long nslices,
+                            const int* wid, const int* wrow, const unsigned* wstep, const int* rp,
+                            const unsigned* edges, unsigned pad, unsigned* words) {
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(s, nslices) {
+    const unsigned o0 = soff[s], wd = soff[s + 1] - o0;
+    if (wd == 0) continue;
+    const int w = wid[s] - 1;
+    const unsigned k0 = o0 - soff[wrow[w] >> 5];
+    const int r = row_of_pos[s * 32 + lane];
+    int b = 0, d = 0;
+    if (r >= 0) {
+      b = rp[r];
+      d = rp[r + 1] - b;
+    }
+    unsigned* out = words + (size_t)wstep[w] * 32;
+    for (unsigned j = 0; j < wd; ++j) {
+      const unsigned k = k0 + j;
+      out[((size_t)(k >> 3) * 32 + lane) * 8 + (k & 7)] = (int)j < d ? (edges[b + j] & ~kRowFlag) : pad;
+    }
+  }
+}
+
+// long row i: its length and number of pieces
+__global__ void k_sell_long_len(const int* lrow, int nlong, const int* rp, int plen, long long* len,
+                                int* np) {
+  GRID_STRIDE(i, nlong) {
+    const int r = lrow[i];
+    const int d = rp[r + 1] - rp[r];
+    len[i] = d;
+    np[i] = (d + plen - 1) / plen;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) { len[nlong] = 0; np[nlong] = 0; }
+}
+
+// warp per long row: copy its followers (flag cleared) and write its pieces
+__global__ void k_sell_long_fill(const int* lrow, int nlong, const int* rp, const unsigned* edges,
+                                 const long long* loff, const int* lp0, int plen, unsigned* lwords,
+                                 int2* piece) {
+  const int lane = threadIdx.x & 31;
+  WARP_STRIDE(i, nlong) {
+    const int r = lrow[i];
+    const int b = rp[r], d = rp[r + 1] - b;
+    const long long o = loff[i];
+    for (int j = lane; j < d; j += 32) lwords[o + j] = edges[b + j] & ~kRowFlag;
+    for (int q = lane; q * plen < d; q += 32)
+      piece[lp0[i] + q] = make_int2((int)(o + (long long)q * plen), min(plen, d - q * plen));
+  }
+}
+
+// Sliced-ELL copy of the edge stream (rows rp / flagged words edges, NA rows) for k_sell.
+int build_sell(IngestOut& out, const int* rp, int NA, long long n, cudaStream_t s, char* msg,
+               size_t msg_len) {
+  const int shift = out.sell_shift;
+  const long long nblk = ((long long)NA + 31) / 32;
+  const long long na_pad = nblk * 32;
+  const long long nsl = nblk;
+  const long long ecap = (long long)out.sell_kcap * 32;
+  out.sell_nslices = nsl;
+  IG_CK(dev_alloc(&out.s_ipos, (size_t)std::max(na_pad, 1LL) * sizeof(unsigned short), s));
+  IG_CK(dev_alloc(&out.s_off, (size_t)(nsl + 1) * sizeof(unsigned), s));
+  Tmp dd, bsum, pre, wflag, wid, keys, sorted, lflag, rop, width, tmp, cnt;
+  IG_CK(dd.alloc((size_t)std::max(na_pad, 1LL) * sizeof(int)));
+  IG_CK(bsum.alloc((size_t)(nblk + 1) * sizeof(long long)));
+  IG_CK(pre.alloc((size_t)(nblk + 1) * sizeof(long long)));
+  IG_CK(wflag.alloc((size_t)std::max(nblk, 1LL) * sizeof(int)));
+  IG_CK(wid.alloc((size_t)std::max(nblk, 1LL) * sizeof(int)));
+  IG_CK(keys.alloc((size_t)std::max(na_pad, 1LL) * 8));
+  IG_CK(sorted.alloc((size_t)std::max(na_pad, 1LL) * 8));
+  IG_CK(lflag.alloc((size_t)std::max(NA, 1)));
+  IG_CK(rop.alloc((size_t)std::max(na_pad, 1LL) * sizeof(int)));
+  IG_CK(width.alloc((size_t)(nsl + 1) * sizeof(unsigned)));
+  IG_CK(cnt.alloc(sizeof(long long)));
+  IG_CK(cudaMemsetAsync(width.p, 0, (size_t)(nsl + 1) * sizeof(unsigned), s));
+  int nwin = 0;
+  long long nlong = 0;
+  if (na_pad > 0) {
+    k_sell_deg<<<grid_for(na_pad, 256), 256, 0, s>>>(rp, NA, na_pad, out.sell_lmax, dd.as<int>(),
+                                                     lflag.as<unsigned char>());
+    k_sell_blocksum<<<grid_for(nblk, 256), 256, 0, s>>>(dd.as<int>(), nblk, bsum.as<long long>());
+    size_t tb = 0;
+    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, bsum.as<long long>(), pre.as<long long>(),
+                                        nblk + 1, s));
+    size_t tb2 = 0;
+    IG_CK(cub::DeviceScan::InclusiveSum(nullptr, tb2, wflag.as<int>(), wid.as<int>(), nblk, s));
+    IG_CK(tmp.alloc(std::max(tb, tb2)));
+    IG_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, bsum.as<long long>(), pre.as<long long>(),
+                                        nblk + 1, s));
+    k_sell_wflag<<<grid_for(nblk, 256), 256, 0, s>>>(pre.as<long long>(), nblk, shift, ecap,
+                                                     wflag.as<int>());
+    IG_CK(cub::DeviceScan::InclusiveSum(tmp.p, tb2, wflag.as<int>(), wid.as<int>(), nblk, s));
+    IG_CK(cudaMemcpyAsync(&nwin, wid.as<int>() + nblk - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+  }
+  out.sell_nwin = nwin;
+  IG_CK(dev_alloc(&out.s_wrow, (size_t)(nwin + 1) * sizeof(int), s));
+  {
+    const int end_row = (int)na_pad;
+    IG_CK(cudaMemcpyAsync(out.s_wrow + nwin, &end_row, sizeof(int), cudaMemcpyHostToDevice, s));
+  }
+  if (na_pad > 0) {
+    k_sell_wrow<<<grid_for(nblk, 256), 256, 0, s>>>(wflag.as<int>(), wid.as<int>(), nblk, out.s_wrow);
+    k_sell_keys<<<grid_for(na_pad, 256), 256, 0, s>>>(dd.as<int>(), wid.as<int>(), out.s_wrow, na_pad,
+                                                      keys.as<unsigned long long>());
+    int wbits = 1;
+    while ((1LL << wbits) < nwin) ++wbits;
+    size_t tb = 0;
+    IG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.as<unsigned long long>(),
+                                         sorted.as<unsigned long long>(), (int)na_pad, 0,
+                                         32 + wbits, s));
+    IG_CK(tmp.alloc(tb));
+    IG_CK(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.as<unsigned long long>(),
+                                         sorted.as<unsigned long long>(), (int)na_pad, 0,
+                                         32 + wbits, s));
+    k_sell_perm<<<grid_for(na_pad, 256), 256, 0, s>>>(sorted.as<unsigned long long>(), na_pad,
+                                                      out.s_wrow, out.s_ipos, rop.as<int>(),
+                                                      width.as<unsigned>());
+  }
+  {
+    size_t tb = 0;
+    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, width.as<unsigned>(), out.s_off, nsl + 1, s));
+    IG_CK(tmp.alloc(tb));
+    IG_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, width.as<unsigned>(), out.s_off, nsl + 1, s));
+  }
+  // window index blocks (steps rounded up to 8 per window)
+  IG_CK(dev_alloc(&out.s_wstep, (size_t)(nwin + 1) * sizeof(unsigned), s));
+  unsigned tot32 = 0;
+  {
+    Tmp ks;
+    IG_CK(ks.alloc((size_t)(nwin + 1) * sizeof(unsigned)));
+    k_sell_wsteps<<<grid_for(nwin + 1, 256), 256, 0, s>>>(out.s_off, out.s_wrow, nwin, ks.as<unsigned>());
+    size_t tb = 0;
+    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, ks.as<unsigned>(), out.s_wstep, nwin + 1, s));
+    IG_CK(tmp.alloc(tb));
+    IG_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, ks.as<unsigned>(), out.s_wstep, nwin + 1, s));
+    IG_CK(cudaMemcpyAsync(&tot32, out.s_wstep + nwin, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+  }
+  // long rows
+  Tmp lrow_all;
+  IG_CK(lrow_all.alloc((size_t)std::max(NA, 1) * sizeof(int)));
+  if (NA > 0) {
+    cub::CountingInputIterator<int> it(0);
+    size_t tb = 0;
+    IG_CK(cub::DeviceSelect::Flagged(nullptr, tb, it, lflag.as<unsigned char>(), lrow_all.as<int>(),
+                                     cnt.as<long long>(), NA, s));
+    IG_CK(tmp.alloc(tb));
+    IG_CK(cub::DeviceSelect::Flagged(tmp.p, tb, it, lflag.as<unsigned char>(), lrow_all.as<int>(),
+                                     cnt.as<long long>(), NA, s));
+    IG_CK(cudaMemcpyAsync(&nlong, cnt.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  }
+  IG_CK(cudaStreamSynchronize(s));
+  out.sell_words = (long long)tot32 * 32;
+  out.sell_nlong = (int)nlong;
+  IG_CK(dev_alloc(&out.s_words, (size_t)std::max(out.sell_words, 1LL) * sizeof(unsigned), s));
+  if (out.sell_words > 0)
+    k_fill_u32v<<<grid_for(out.sell_words, 256), 256, 0, s>>>(out.s_words, out.sell_words, (unsigned)n);
+  if (nsl > 0)
+    k_sell_fill<<<grid_for(nsl * 32, 256), 256, 0, s>>>(rop.as<int>(), out.s_off, nsl, wid.as<int>(),
+                                                        out.s_wrow, out.s_wstep, rp, out.edges,
+                                                        (unsigned)n, out.s_words);
+  IG_CK(dev_alloc(&out.s_lrow, (size_t)std::max(nlong, 1LL) * sizeof(int), s));
+  IG_CK(dev_alloc(&out.s_lp0, (size_t)(nlong + 1) * sizeof(int), s));
+  if (nlong > 0)
+    IG_CK(cudaMemcpyAsync(out.s_lrow, lrow_all.p, (size_t)nlong * sizeof(int),
+                          cudaMemcpyDeviceToDevice, s));
+  else
+    IG_CK(cudaMemsetAsync(out.s_lp0, 0, sizeof(int), s));
+  long long nlw = 0;
+  int npieces = 0;
+  if (nlong > 0) {
+    Tmp len, loff, np;
+    IG_CK(len.alloc((size_t)(nlong + 1) * sizeof(long long)));
+    IG_CK(loff.alloc((size_t)(nlong + 1) * sizeof(long long)));
+    IG_CK(np.alloc((size_t)(nlong + 1) * sizeof(int)));
+    k_sell_long_len<<<grid_for(nlong, 256), 256, 0, s>>>(out.s_lrow, (int)nlong, rp, out.sell_piece,
+                                                         len.as<long long>(), np.as<int>());
+    size_t tb = 0;
+    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, len.as<long long>(), loff.as<long long>(),
+                                        nlong + 1, s));
+    size_t tb2 = 0;
+    IG_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb2, np.as<int>(), out.s_lp0, nlong + 1, s));
+    IG_CK(tmp.alloc(std::max(tb, tb2)));
+    IG_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, len.as<long long>(), loff.as<long long>(),
+                                        nlong + 1, s));
+    IG_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, np.as<int>(), out.s_lp0, nlong + 1, s));
+    IG_CK(cudaMemcpyAsync(&nlw, loff.as<long long>() + nlong, sizeof(long long),
+                          cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaMemcpyAsync(&npieces, out.s_lp0 + nlong, sizeof(int), cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+    IG_CK(dev_alloc(&out.s_lwords, (size_t)std::max(nlw, 1LL) * sizeof(unsigned), s));
+    IG_CK(dev_alloc(&out.s_piece, (size_t)std::max(npieces, 1) * sizeof(int2), s));
+    k_sell_long_fill<<<grid_for(nlong * 32, 256), 256, 0, s>>>(out.s_lrow, (int)nlong, rp,
+                                                               out.edges, loff.as<long long>(),
+                                                               out.s_lp0, out.sell_piece,
+                                                               out.s_lwords, out.s_piece);
+  }
+  out.sell_lwords = nlw;
+  out.sell_npieces = npieces;
+  IG_CK(cudaGetLastError());
+  IG_CK(cudaStreamSynchronize(s));
+  return PSI_OK;
+}
+
 int batch_vectors(IngestOut& out, long long n, int NA, int nprof, const int* rp, const int* idx,
                   const int* new_of_old, const int* longr, long long nlongr, const double* bold,
                   const double* lam, cudaStream_t s, char* msg, size_t msg_len) {
@@ -1505,6 +1795,15 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   key.reset(); sel.reset(); sorted.reset(); flag8.reset(); stage_tmp.reset(); sort_tmp2.reset();
 
   tr.mark("relabel");
+  // The sweep's layout: the sliced-ELL copy of the edge stream (k_sell) for single-profile
+  // graphs with heavy rows (C4/C5: measured faster than the tiles), the
+  // edge-balanced tiles (k_tiles, and k_solve for small graphs) otherwise; PSI_SELL=0/1 forces
+  // the tiles / the sliced-ELL layout (not with the overlapped plan or a batch).
+  {
+    const int se = env_int("PSI_SELL", -1);
+    out.sell = (out.n_act > 0 && nprof == 1 && !out.ovl && (se == 1 || (se < 0 && out.n_heavy > 0)))
+                   ? 1 : 0;
+  }
   // ---- 6. relabelled edge stream over active rows, folded constants
   const int NA = (int)out.n_act;
   Tmp cntr, K, rp_new;
@@ -1577,7 +1876,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     }
     // rows keep their followers in input order: the sweep's sums have a fixed order either
     // way, and a per-row sort bought nothing measurable
-    if (m_act > 0) {
+    if (m_act > 0 && !out.sell) {          // (the sliced-ELL copy needs no flags)
       k_flag_rows<<<grid_for(NA, 256), 256, 0, s>>>(rp_new.as<int>(), NA, m_act, m_pad, N,
                                                     out.edges);
     }
@@ -1616,9 +1915,12 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   // ---- 7. edge tiles: first row of every tile, rows spanning tiles (and, for a batch
   // context, the same for the batch sweep's 512-edge tiles)
   {
-    int rc4 = make_tiling(rp_new.as<int>(), NA, (long long)out.ntiles * out.tile, out.tile, s, &out.tile_row,
-                          &out.split, &out.nsplit, &out.nsplit_long, msg, msg_len);
-    if (rc4 != PSI_OK) return rc4;
+    int rc4 = PSI_OK;
+    if (!out.sell) {
+      rc4 = make_tiling(rp_new.as<int>(), NA, (long long)out.ntiles * out.tile, out.tile, s,
+                        &out.tile_row, &out.split, &out.nsplit, &out.nsplit_long, msg, msg_len);
+      if (rc4 != PSI_OK) return rc4;
+    }
     if (out.ovl && out.n_heavy > 0) {
       const size_t words = (size_t)(out.n_heavy / 32 + 1);
       IG_CK(dev_alloc(&out.hsplit, words * sizeof(unsigned), s));
@@ -1637,6 +1939,21 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   }
   IG_CK(cudaGetLastError());
   tr.mark("tiles");
+  // ---- 8. sliced-ELL layout of the same edge stream (k_sell); the stream itself is then
+  // no longer needed
+  {
+    if (out.sell) {
+      out.sell_shift = std::min(std::max(env_int("PSI_SELL_SHIFT", kSellShift), 5), 10);
+      out.sell_kcap = std::max(env_int("PSI_SELL_KCAP", kSellKcap), 1);
+      out.sell_lmax = std::min(std::max(env_int("PSI_SELL_LMAX", kSellLmax), 1), 2047);
+      out.sell_piece = std::max(env_int("PSI_SELL_PIECE", kSellPiece), 32);
+      int rc5 = build_sell(out, rp_new.as<int>(), NA, n, s, msg, msg_len);
+      if (rc5 != PSI_OK) return rc5;
+      IG_CK(cudaFreeAsync(out.edges, s));
+      out.edges = nullptr;
+      tr.mark("sliced-ELL");
+    }
+  }
   return PSI_OK;
 }
 

@@ -73,6 +73,12 @@ constexpr int kDefaultGroups = 8;        // tile groups (of kBlock threads) per 
 constexpr long long kCoopEdges = 1LL << 23;  // k_solve up to this many edge slots (PSI_COOP_TILES: tiles)
 constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA
 constexpr int kDefaultL1Hot = 16384;     // labels below this gather through L1 (evict_last)
+// sliced-ELL sweep (k_sell, SellPlan)
+constexpr int kSellWarps = 32;           // warps per k_sell CTA (one CTA per SM)
+constexpr int kSellShift = 8;            // rows per window <= 256 (sort scope and smem sums)
+constexpr int kSellKcap = 256;           // window cut after ~256 x 32 stream edges
+constexpr int kSellLmax = 1024;          // longer stream rows are summed in pieces by warps
+constexpr int kSellPiece = 4096;         // followers per piece of a long row
 
 // Device memory: every allocation of the library is stream-ordered and comes from a memory
 // pool the library owns (one per device, psi_api.cu) -- never the device's default pool, so
@@ -93,6 +99,7 @@ struct LoopState {
   unsigned int done;     // CTA arrival counter of the fix-up kernel
   int status;            // bit 0: non-finite epsilon_t
   unsigned heavy_next;   // next panel of k_heavy to claim (reset by k_fix / k_init)
+  unsigned sell_next;    // next work item of k_sell to claim (reset by k_fix / k_init)
 };
 
 // Per-call parameters (host writes them before every graph launch).
@@ -117,6 +124,38 @@ struct HeavyPlan {
   int nseg;                  // staged labels H = nseg << seg_shift
   int seg_shift;             // labels per segment = 1 << seg_shift
   int slots;                 // slot sums per panel; slot index `slots` is the padding junk
+};
+
+// Device view of the sliced-ELL layout of the edge stream (built by psi_ingest.cu, swept by
+// k_sell in psi_sweep.cu).  Active rows are cut into windows of whole 32-row
+// blocks (at most 2^shift rows, and about kcap * 32 stream edges, so every window is a bounded
+// work item); inside a window the rows are sorted by stream length (descending) and dealt out
+// 32 at a time to slices: lane l of slice s owns one row.  A lane streams the whole window in
+// one loop of K = sum of its slices' widths steps (step k = follower k - start of the slice
+// containing k of its row in that slice; a shorter row's tail holds the sentinel label n,
+// x[n] = 0), step k at words[(wstep[w] + (k / 8) * 8) * 32 + l * 8 + k % 8]: one 32-byte load
+// per lane and 8 steps, 1 KB contiguous per warp.  Rows longer than lmax ("long rows")
+// are not in the slices: they are cut into pieces of at most `piece` followers, each summed by
+// one warp of k_sell (lwords -> ppart), and finished by k_fix (piece sums in piece order).
+struct SellPlan {
+  const unsigned* words;      // slice-major; inside a slice j-major: [j][32 lanes]
+  const unsigned* soff;       // [nslices + 1] first step of slice s (= rows 32s..) if the
+                              // windows were unpadded: slice ends inside a window
+  const unsigned* wstep;      // [nwin + 1] first step of window w's index block (multiple of 8)
+  const unsigned short* ipos; // [n_act pad 32] position of row r in its window's sorted order
+                              // (0xffff: a long row)
+  const int* wrow;            // [nwin + 1] first row of window w (a multiple of 32)
+  int nwin;
+  int wmax;                   // rows per window at most (= 2^shift: the warp's smem sums)
+  const int* lrow;            // [nlong] long rows (ascending)
+  const int* lp0;             // [nlong + 1] pieces of long row i: lp0[i] .. lp0[i + 1]
+  const int2* piece;          // [npieces] (first word in lwords, length)
+  const unsigned* lwords;     // long rows' follower labels, row after row
+  int npieces;
+  int nlong;
+  double* ppart;              // [npieces] piece sums of the current launch
+  double* epsw;               // [nwin] eps_t partial of every window
+  long long nwords, nlwords;  // sizes (PSI_CHECKS bounds)
 };
 
 // Everything one sweep / readout launch needs (passed by value; frozen in the graph).
@@ -161,6 +200,9 @@ struct SweepArgs {
   int ovl;
   double* scold;             // [n_heavy]
   const unsigned* hsplit;    // [n_heavy / 32 + 1] bit r: heavy row r is a split row (k_fix's)
+  // sliced-ELL sweep (k_sell) instead of the edge-balanced tiles (k_tiles)
+  int use_sell;
+  SellPlan sell;
 };
 
 // ---- launchers (psi_sweep.cu)
@@ -174,6 +216,7 @@ struct TilesCfg {                    // launch shape of k_tiles (sweep and reado
   int solve_max_grid;                // co-resident CTAs of k_solve (cooperative launch bound)
 };
 TilesCfg tiles_config(int ntiles, long long n, int tile, bool ovl = false);  // tile: 512 or 1024
+TilesCfg sell_config(long long n, int shift);  // k_sell (sweep + readout); no persistent solver
 int fix_grid(int nsplit);            // CTAs of the fix-up kernel
 void* fix_kernel_ptr(bool readout);
 void* heavy_kernel_ptr(int warps);   // psi_heavy.cu: kHeavyWarps or kOvlWarps consumer warps
@@ -220,6 +263,20 @@ struct IngestOut {
   int2* h_rslot = nullptr;
   int* h_wslot = nullptr;
   int relabel_levels = 0;
+  // sliced-ELL layout (SellPlan; sell = 0: the sweep runs on the tiles); PSI_SELL_SHIFT /
+  // _LMAX / _PIECE override the window, long-row and piece sizes (tests and tuning)
+  int sell = 0, sell_shift = 0, sell_lmax = 0, sell_piece = kSellPiece, sell_kcap = kSellKcap;
+  int sell_nwin = 0, sell_nlong = 0, sell_npieces = 0;
+  long long sell_nslices = 0, sell_words = 0, sell_lwords = 0;
+  unsigned* s_words = nullptr;
+  unsigned* s_off = nullptr;
+  unsigned short* s_ipos = nullptr;
+  int* s_wrow = nullptr;
+  unsigned* s_wstep = nullptr;
+  int* s_lrow = nullptr;
+  int* s_lp0 = nullptr;
+  int2* s_piece = nullptr;
+  unsigned* s_lwords = nullptr;
   double kappa_row = 0, kappa_col = 0, rho_A = 0;
   long long n_f = 0, n_g = 0, n_leaderless = 0;
   int relabeled = 0;

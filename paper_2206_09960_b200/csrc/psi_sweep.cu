@@ -97,6 +97,13 @@ __device__ __forceinline__ double ld_l1last(const double* p, unsigned long long 
                : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
+// 256-bit streaming load of 8 index words (sm_100 .v8): read once per sweep; L2 evict_first
+__device__ __forceinline__ void ld_stream8(const unsigned* p, unsigned (&w)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                 "=r"(w[6]), "=r"(w[7])
+               : "l"(p));
+}
 // named barrier over one TB-thread tile group of the CTA (id 0 is __syncthreads)
 template <int TB>
 __device__ __forceinline__ void group_bar(int id) {
@@ -320,6 +327,158 @@ __global__ void __launch_bounds__(TB * G, (1024 / (TB * G)) > 0 ? 1024 / (TB * G
   if (A.ovl) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- sliced-ELL sweep (k_sell)
+// Persistent CTAs of independent warps; work items are claimed one at a time from a device
+// counter (LoopState::sell_next): first the pieces of the long rows, then the windows (each of
+// bounded size, SellPlan).  A piece: 32 lanes x 8 followers per step, summed by a fixed shuffle
+// tree into ppart.  A window:
+//   1. lane l streams the window's slices, accumulating its row's gathers x_{t-1}[word] in
+//      order (one coalesced 128-byte index load + one gather per step, 8 gathers in flight and
+//      the next 8 index words loaded meanwhile) and storing the sum at the row's sorted
+//      position in the warp's shared-memory sums at every slice end;
+//   2. runs the row-order epilogue over the window (coalesced, as k_tiles') for every row but
+//      the long ones (k_fix finishes those from their pieces), and writes the window's eps_t
+//      partial to epsw[w] (reduced in a fixed order by k_fix).
+// No segmented scans, no flags, no tile barriers: every short row is summed by one lane.
+// Deterministic: every sum has a fixed order whatever warp runs an item.
+template <bool READOUT>
+__global__ void __launch_bounds__(kSellWarps * 32, 1) k_sell(SweepArgs A) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const SellPlan& P = A.sell;
+  const unsigned hs = (unsigned)A.hot_smem;
+  double* hot = reinterpret_cast<double*>(dsm);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* Sw = hot + ((hs + 1) & ~1u) + (size_t)warp * P.wmax;
+  const long long t = A.st->iter;
+  const double* __restrict__ xs = (t & 1) ? A.x1 : A.x0;    // x_{t-1}
+  double* __restrict__ xd = (t & 1) ? A.x0 : A.x1;          // x_t
+  const unsigned long long pf = pol_evict_first(), pl = pol_evict_last();
+  const unsigned hot_lim = (unsigned)A.hot_lim;
+  const unsigned l1_lim = (unsigned)A.l1_lim;
+  const unsigned single_lo = (unsigned)A.single_lo;
+  const double* __restrict__ acon = (t == 0 && A.a_first) ? A.a_first : A.a;
+
+  for (unsigned i = threadIdx.x; i < hs; i += blockDim.x) hot[i] = __ldcg(xs + i);
+  __syncthreads();
+
+  // one gather, as k_tiles': the CTA's shared-memory copy below hs, L1 evict_last below l1_lim,
+  // L1 evict_first for the single-leader users (a lane's consecutive steps read consecutive
+  // labels there), L1 bypass otherwise; L2 evict_last below hot_lim.  (A branch-free version
+  // with predicated loads serialises on the shared destination register, and one load variant
+  // under an address-range L2 policy loses the L1 hits: both measured.)
+  auto gx = [&](unsigned lab) -> double {
+    PSI_ASSERT((double)lab <= A.n_users);
+    if (lab < hs) return hot[lab];
+    if (lab < l1_lim) return ld_l1last(xs + lab, pl);
+    if (lab >= single_lo) return ld_l1first(xs + lab, pf);
+    return ld_hint_na(xs + lab, lab < hot_lim ? pl : pf);
+  };
+
+  const int nitems = P.npieces + P.nwin;
+  int it = 0;
+  if (lane == 0) it = (int)atomicAdd(&A.st->sell_next, 1u);
+  it = __shfl_sync(kFull, it, 0);
+  while (it < nitems) {
+    int nxt = 0;                                   // claim the next item early
+    if (lane == 0) nxt = (int)atomicAdd(&A.st->sell_next, 1u);
+    if (it < P.npieces) {
+      // ---- a piece of a long row
+      const int2 pc = P.piece[it];
+      PSI_ASSERT(pc.x >= 0 && pc.y > 0 && pc.x + (long long)pc.y <= P.nlwords);
+      const unsigned* pw = P.lwords + pc.x;
+      double acc = 0.0;
+      for (int k = 0; k < pc.y; k += 256) {
+        unsigned w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int j = k + q * 32 + lane;
+          w[q] = j < pc.y ? ld_stream(pw + j, pf) : 0xffffffffu;
+        }
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = w[q] != 0xffffffffu ? gx(w[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += v[q];
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) P.ppart[it] = acc;
+    } else {
+      // ---- a window
+      const int w = it - P.npieces;
+      const int r0 = __ldg(P.wrow + w), r1 = __ldg(P.wrow + w + 1);
+      const int gs0 = r0 >> 5;
+      const int nsl = (r1 - r0) >> 5;                // slices of the window (<= 32)
+      // slice s ends at soff[gs0 + s + 1]: lane l holds soff[gs0 + l] (l <= nsl)
+      const unsigned offl = lane <= nsl ? __ldg(P.soff + gs0 + lane) : 0u;
+      const unsigned off0 = __shfl_sync(kFull, offl, 0);
+      const unsigned offe = __ldg(P.soff + gs0 + nsl);
+      const int K = (int)(offe - off0);              // steps of the whole window
+      PSI_ASSERT(nsl >= 1 && nsl <= 32 && (r1 - r0) <= P.wmax && off0 <= offe &&
+                 ((long long)__ldg(P.wstep + w) + ((K + 7) & ~7)) * 32 <= P.nwords);
+      // lane l streams its steps k < K, 8 per 32-byte load, with the index words of the next
+      // two blocks in flight while this block's 8 gathers are (one block ahead left the
+      // gathers waiting on DRAM-latency index loads: C5 2.65 -> 1.98 ms), and cuts its running
+      // sum at the slice ends (uniform branches)
+      const unsigned ws0 = __ldg(P.wstep + w);
+      const unsigned* pw = P.words + (size_t)ws0 * 32 + lane * 8;
+      int s = 0;
+      int end = (int)(__shfl_sync(kFull, offl, 1) - off0);   // end of slice 0
+      double acc = 0.0;
+      unsigned wv[8], wn[8];                         // index words of blocks k and k + 8
+      if (K > 0) ld_stream8(pw, wv);
+      if (K > 8) ld_stream8(pw + 256, wn);
+      for (int k = 0; k < K; k += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = k + q < K ? gx(wv[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) wv[q] = wn[q];
+        if (k + 16 < K) ld_stream8(pw + (size_t)(k + 16) * 32, wn);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (k + q == end && end < K) {             // slice s ends
+            PSI_ASSERT(s + 1 < nsl);
+            Sw[s * 32 + lane] = acc;
+            acc = 0.0;
+            ++s;
+            const unsigned oe = __shfl_sync(kFull, offl, (s + 1) & 31);
+            end = (int)((s + 1 < 32 ? oe : offe) - off0);
+          }
+          acc += v[q];
+        }
+      }
+      if (K > 0) Sw[s * 32 + lane] = acc;
+      __syncwarp();
+      // ---- row-order epilogue over the window (coalesced); long rows are k_fix's
+      const int nr = min(r1, A.n_act) - r0;
+      double eps_acc = 0.0;
+      for (int i = lane; i < nr; i += 32) {
+        const int r = r0 + i;
+        const unsigned ip = __ldg(P.ipos + r);
+        if (ip == 0xffffu) continue;
+        PSI_ASSERT(ip < (unsigned)(r1 - r0));
+        double Sr = Sw[ip];
+        if (r < A.n_heavy) Sr += A.hhot[r];                  // followers < H (k_heavy)
+        if (READOUT) {
+          A.psi[r] = (ld_stream(A.d + r, pf) + ld_stream(A.lam + r, pf) * Sr) / A.n_users;
+        } else {
+          const unsigned long long px = (unsigned)r < hot_lim ? pl : pf;
+          const double xn = fma(ld_stream(A.g + r, pf), Sr, ld_stream(acon + r, pf));
+          const double xp = ld_hint_na(xs + r, px);
+          eps_acc += ld_stream(A.wt + r, pf) * fabs(xn - xp);
+          st_hint(xd + r, xn, A.st_last ? px : pf);
+        }
+      }
+      if (!READOUT) {
+        eps_acc = warp_sum(eps_acc);
+        if (lane == 0) P.epsw[w] = eps_acc;
+      }
+      __syncwarp();
+    }
+    it = __shfl_sync(kFull, nxt, 0);
+  }
+}
+
 // Split rows, eps_t and the stop rule (k_fix), as a device function of any block size >= 32
 // (NT = block size).  p_in / p_out / x are read L2-coherently: in the persistent solver they
 // were written earlier in the same kernel by other CTAs.
@@ -333,7 +492,10 @@ __device__ __forceinline__ void fix_body(const SweepArgs& A, long long t, double
   const int tid = threadIdx.x;
   double eps_acc = 0.0;
 
-  if (blockIdx.x == 0 && tid == 0) A.st->heavy_next = 0;   // k_heavy of this sweep is done
+  if (blockIdx.x == 0 && tid == 0) {       // k_heavy / k_sell of this launch are done
+    A.st->heavy_next = 0;
+    A.st->sell_next = 0;
+  }
   auto finish = [&](int r, double S) {
     if (r < A.n_heavy) S += A.hhot[r];
     if (READOUT) {
@@ -362,6 +524,17 @@ __device__ __forceinline__ void fix_body(const SweepArgs& A, long long t, double
     for (int k = sp.y + 1; k <= sp.z; ++k) S += __ldcg(A.p_in + k);
     finish(sp.x, S);
   }
+  if (A.use_sell) {
+    // k_sell's long rows: their pieces in piece order (+ hhot)
+    const SellPlan& P = A.sell;
+    for (int i = blockIdx.x * NT + tid; i < P.nlong; i += gridDim.x * NT) {
+      const int p0 = P.lp0[i], p1 = P.lp0[i + 1];
+      PSI_ASSERT(p0 < p1 && p1 <= P.npieces);
+      double S = 0.0;
+      for (int q = p0; q < p1; ++q) S += __ldcg(P.ppart + q);
+      finish(P.lrow[i], S);
+    }
+  }
   if (A.ovl) {
     // overlapped sweep: the heavy rows k_tiles completed inside a tile (their edge-stream sum
     // in scold) are finished here, once k_heavy's hhot exists; split heavy rows were above
@@ -369,6 +542,10 @@ __device__ __forceinline__ void fix_body(const SweepArgs& A, long long t, double
       if (!((__ldg(A.hsplit + (r >> 5)) >> (r & 31)) & 1u)) finish(r, __ldcg(A.scold + r));
   }
   if (READOUT) return;
+  // k_sell: the windows' eps_t partials, in a fixed partition and order
+  if (A.use_sell)
+    for (int i = blockIdx.x * NT + tid; i < A.sell.nwin; i += gridDim.x * NT)
+      eps_acc += __ldcg(A.sell.epsw + i);
 
   const double tot = block_sum<NT>(eps_acc, red);
   if (COOP) {
@@ -425,6 +602,7 @@ __global__ void k_init(SweepArgs A, int n) {
     A.st->done = 0;
     A.st->status = 0;
     A.st->heavy_next = 0;
+    A.st->sell_next = 0;
     const LoopParams P = *A.prm;
     if (A.use_cond) cudaGraphSetConditional(A.cond, (P.gap0 > P.eps && P.max_iters > 0) ? 1u : 0u);
   }
@@ -562,6 +740,44 @@ TilesCfg tiles_config(int ntiles, long long n, int tile, bool ovl) {
     case 4: return cfg_for<4, 128>(ntiles, n, hot, l1);
     default: return cfg_for<8, 128>(ntiles, n, hot, l1);
   }
+}
+
+// Launch shape of k_sell: one CTA of kSellWarps warps per SM, the hot cache of x_{t-1} and
+// every warp's window sums in shared memory (PSI_SMEM_HOT / PSI_L1_HOT as for k_tiles).
+TilesCfg sell_config(long long n, int shift) {
+  int dev = 0, sms = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  TilesCfg c{};
+  c.groups = 1;
+  long long hs = env_int("PSI_SMEM_HOT", kDefaultSmemHot);
+  // warps per CTA: kSellWarps (PSI_SELL_WARPS), halved until their window sums and the hot
+  // cache fit in shared memory
+  int warps = std::min(std::max(env_int("PSI_SELL_WARPS", kSellWarps), 1), 32);
+  while (warps > 1 && (size_t)warps * ((size_t)8 << shift) + (size_t)std::max(hs, 0LL) * 8 + 1024 >
+                          (size_t)optin)
+    warps /= 2;
+  c.block = warps * 32;
+  const size_t fixed = (size_t)warps * ((size_t)8 << shift);
+  const long long cap = ((long long)optin - (long long)fixed - 1024) / 8 - 2;
+  if (hs > cap) hs = cap;
+  if (hs > n + 1) hs = n + 1;
+  if (hs < 0) hs = 0;
+  c.hot_smem = (int)hs;
+  c.l1_lim = (int)std::max<long long>(hs, std::min<long long>(env_int("PSI_L1_HOT", kDefaultL1Hot), n + 1));
+  c.smem = fixed + (size_t)((hs + 1) & ~1LL) * 8;
+  c.sweep = (void*)k_sell<false>;
+  c.readout = (void*)k_sell<true>;
+  c.solve = nullptr;
+  c.solve_max_grid = 0;
+  cudaFuncSetAttribute(k_sell<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  cudaFuncSetAttribute(k_sell<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell<false>, c.block, c.smem);
+  if (occ < 1) occ = 1;
+  c.grid = sms * occ;
+  return c;
 }
 
 int fix_grid(int nsplit) {

@@ -31,10 +31,14 @@ def gpu():
     return psi
 
 
-@pytest.fixture(params=["default", "graph"])
+@pytest.fixture(params=["default", "graph", "sell"])
 def driver(request, monkeypatch):
     """Small graphs run in the persistent cooperative solver by default (k_solve); "graph"
-    forces the CUDA-graph WHILE loop (k_init / k_tiles / k_fix) on the same inputs."""
+    forces the CUDA-graph WHILE loop over the edge-balanced tiles (k_init / k_tiles / k_fix),
+    "sell" the same loop over the sliced-ELL layout (k_sell) on the same inputs."""
     if request.param == "graph":
         monkeypatch.setenv("PSI_COOP_TILES", "0")
+        monkeypatch.setenv("PSI_SELL", "0")
+    elif request.param == "sell":
+        monkeypatch.setenv("PSI_SELL", "1")
     return request.param
