@@ -12,7 +12,7 @@ Inputs are resident in HBM when the timed region starts.
 value  = GTEPS over the solve: M * (T + 1) / time-to-eps   (T sweeps + 1 readout pass)
 e2e    = same metric through the C-ABI with HOST buffers: psi_build_graph from pinned host
          arrays (H2D copy + ingest), psi_iterate, psi_get_psi to host, all inside the timed region
-roofline: the sweep (k_tiles + k_fix per sweep), algorithmic bytes per sweep
+roofline: the sweep (k_heavy + k_sell or k_tiles + k_fix), algorithmic bytes per sweep
          B_sweep = 4M + 4(N+1) + 8 N_g + 32 N_f / measured sweep time
 cpu_baseline / --impl reference: the fp64 oracle (oracle/, Alg. 2 with explicit SciPy
          CSR), single core, on a bounded row-block sample of the same graph.
@@ -246,7 +246,7 @@ def oracle_time_to_eps(configs=(1, 3)):
 
 
 # Measured gather ceilings of this design (profiles/r1/ubench_gather_r1.txt): random 8-byte
-# gathers from an L2-resident vector (k_tiles' edge-stream gathers) and from shared memory
+# gathers from an L2-resident vector (the edge stream's gathers) and from shared memory
 # (k_heavy's staged segments), per B200, G gathers/s.
 GATHER_L2_GPS = 281.0
 GATHER_SMEM_GPS = 1040.0
@@ -257,7 +257,7 @@ def gather_ceiling(info, sweep_ms):
     shared-memory gather rate + the edge stream's gathers at the measured L2 rate (serial,
     as the kernels run), beside the HBM roofline."""
     heavy = info["heavy_entries"]
-    stream = info["num_tiles"] * info["tile_edges"] - 0        # edge slots of k_tiles
+    stream = info["stream_edges"]                               # gathers of k_sell / k_tiles
     t_ms = heavy / (GATHER_SMEM_GPS * 1e9) * 1e3 + stream / (GATHER_L2_GPS * 1e9) * 1e3
     return {"heavy_entries": heavy, "stream_gathers": stream,
             "rates_gps": {"smem": GATHER_SMEM_GPS, "l2": GATHER_L2_GPS,
@@ -265,12 +265,17 @@ def gather_ceiling(info, sweep_ms):
             "ceiling_sweep_ms": round(t_ms, 4), "frac_of_gather_ceiling": round(t_ms / sweep_ms, 4)}
 
 
+def sweep_kernel(info):
+    """The edge-stream kernel the library chose: the sliced-ELL sweep or the tiles."""
+    return "k_sell" if info.get("sliced_ell") else "k_tiles"
+
+
 def knobs(info):
     """Every PSI_* environment override in effect (none by default) and the launch shape the
     library chose, so a number can be traced to its configuration."""
     env = {k: v for k, v in sorted(os.environ.items()) if k.startswith("PSI_")}
-    lib = {k: info[k] for k in ("tile_edges", "grid", "block", "hot_smem", "heavy_labels",
-                                "heavy_panels", "n_heavy", "last_solver")}
+    lib = {k: info[k] for k in ("sliced_ell", "tile_edges", "grid", "block", "hot_smem",
+                                "heavy_labels", "heavy_panels", "n_heavy", "last_solver")}
     return {"env": env, "library": lib}
 
 
@@ -449,8 +454,9 @@ def run_ours(args, ws, rank, local):
             "frac": round(achieved / peak, 4), "traffic": _traffic_from_profiles("sweep", args.config),
             "traffic_source": _traffic_from_profiles("source", args.config),
             "gather": gather_ceiling(info, sweep_ms),
-            "kernel": "one sweep = k_heavy + k_tiles<sweep> + k_fix<sweep>; each launch timed "
-                      "with CUDA events on the library stream (psi_time_sweep, 20 sweeps)",
+            "kernel": f"one sweep = k_heavy + {sweep_kernel(info)}<sweep> + k_fix<sweep>; each "
+                      "launch timed with CUDA events on the library stream (psi_time_sweep, 20 "
+                      "sweeps); k_tiles_ms is the edge-stream kernel's time, whichever it is",
             "k_heavy_ms": round(heavy_ms, 4), "k_tiles_ms": round(tiles_ms, 4),
             "k_fix_ms": round(fix_ms, 4),
             "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
@@ -473,7 +479,8 @@ def run_ours(args, ws, rank, local):
            "graph_info": {k: info[k] for k in ("n_f", "n_g", "n_leaderless", "kappa_row", "kappa_col",
                                                "rho_A", "num_tiles", "num_long_rows", "grid", "block", "hot_smem",
                                                "n_heavy", "heavy_entries", "heavy_panels", "heavy_labels",
-                                               "relabeled")}}
+                                               "relabeled", "sliced_ell", "sell_long_rows",
+                                               "sell_pieces", "sell_words", "stream_edges")}}
     g.close()
     del d_in
     torch.cuda.empty_cache()
@@ -546,6 +553,7 @@ def configs_side(dev, configs):
                      "time_to_eps_ms": round(t, 4), "solve_gteps": round(w.m * (T + 1) / t / 1e6, 2),
                      "sweep_ms": round(sweep, 4), "k_heavy_ms": round(hv, 4),
                      "k_tiles_ms": round(ti, 4), "k_fix_ms": round(fx, 4),
+                     "sweep_kernel": sweep_kernel(inf),
                      "sweep_gteps": round(w.m / sweep / 1e6, 2), "B_sweep": byt,
                      "hbm_frac": round(byt / (sweep * 1e-3) / 1e9 / peak, 4),
                      "solver": inf["last_solver"], "ingest_ms": round(inf["ingest_ms"], 2)})

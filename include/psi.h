@@ -96,6 +96,8 @@ typedef struct psi_info {
   int64_t sell_long_rows; /* rows summed in pieces by whole warps (stream length > lmax) */
   int64_t sell_pieces;    /* their pieces */
   int64_t sell_words;     /* index words of the slices (padding included) */
+  int64_t stream_edges;   /* gathers of the edge stream per sweep: followers not summed by the
+                             staged-segment kernel, + one pseudo edge per row without any */
 } psi_info;
 
 /*

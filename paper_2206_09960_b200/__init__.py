@@ -66,7 +66,8 @@ class psi_info(ctypes.Structure):
                 ("last_solver", ctypes.c_int64), ("n_profiles", ctypes.c_int64),
                 ("tile_edges", ctypes.c_int64), ("overlapped", ctypes.c_int64),
                 ("sliced_ell", ctypes.c_int64), ("sell_long_rows", ctypes.c_int64),
-                ("sell_pieces", ctypes.c_int64), ("sell_words", ctypes.c_int64)]
+                ("sell_pieces", ctypes.c_int64), ("sell_words", ctypes.c_int64),
+                ("stream_edges", ctypes.c_int64)]
 
 
 _lib = None

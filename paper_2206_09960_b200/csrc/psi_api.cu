@@ -1114,6 +1114,7 @@ psi_status psi_get_info(const psi_ctx* c, psi_info* out) {
   out->sell_long_rows = c->g.sell_nlong;
   out->sell_pieces = c->g.sell_npieces;
   out->sell_words = c->g.sell_words;
+  out->stream_edges = c->g.m_act;
   return PSI_OK;
 }
 

@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(TB * G, (1024 / (TB * G)) > 0 ? 1024 / (TB * G
 //      partial to epsw[w] (reduced in a fixed order by k_fix).
 // No segmented scans, no flags, no tile barriers: every short row is summed by one lane.
 // Deterministic: every sum has a fixed order whatever warp runs an item.
-template <bool READOUT>
+template <bool READOUT, int DEPTH>
 __global__ void __launch_bounds__(kSellWarps * 32, 1) k_sell(SweepArgs A) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const SellPlan& P = A.sell;
@@ -424,16 +424,19 @@ __global__ void __launch_bounds__(kSellWarps * 32, 1) k_sell(SweepArgs A) {
       int s = 0;
       int end = (int)(__shfl_sync(kFull, offl, 1) - off0);   // end of slice 0
       double acc = 0.0;
-      unsigned wv[8], wn[8];                         // index words of blocks k and k + 8
-      if (K > 0) ld_stream8(pw, wv);
-      if (K > 8) ld_stream8(pw + 256, wn);
+      unsigned wb[DEPTH][8];                         // index words of blocks k .. k + 8(D-1)
+#pragma unroll
+      for (int d = 0; d < DEPTH; ++d)
+        if (K > 8 * d) ld_stream8(pw + 256 * d, wb[d]);
       for (int k = 0; k < K; k += 8) {
         double v[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = k + q < K ? gx(wv[q]) : 0.0;
+        for (int q = 0; q < 8; ++q) v[q] = k + q < K ? gx(wb[0][q]) : 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) wv[q] = wn[q];
-        if (k + 16 < K) ld_stream8(pw + (size_t)(k + 16) * 32, wn);
+        for (int d = 0; d + 1 < DEPTH; ++d)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) wb[d][q] = wb[d + 1][q];
+        if (k + 8 * DEPTH < K) ld_stream8(pw + (size_t)(k + 8 * DEPTH) * 32, wb[DEPTH - 1]);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           if (k + q == end && end < K) {             // slice s ends
@@ -767,14 +770,15 @@ TilesCfg sell_config(long long n, int shift) {
   c.hot_smem = (int)hs;
   c.l1_lim = (int)std::max<long long>(hs, std::min<long long>(env_int("PSI_L1_HOT", kDefaultL1Hot), n + 1));
   c.smem = fixed + (size_t)((hs + 1) & ~1LL) * 8;
-  c.sweep = (void*)k_sell<false>;
-  c.readout = (void*)k_sell<true>;
+  // two index blocks in flight per lane (three measured equal)
+  c.sweep = (void*)k_sell<false, 2>;
+  c.readout = (void*)k_sell<true, 2>;
   c.solve = nullptr;
   c.solve_max_grid = 0;
-  cudaFuncSetAttribute(k_sell<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-  cudaFuncSetAttribute(k_sell<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  cudaFuncSetAttribute(c.sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+  cudaFuncSetAttribute(c.readout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sell<false>, c.block, c.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, c.sweep, c.block, c.smem);
   if (occ < 1) occ = 1;
   c.grid = sms * occ;
   return c;
