@@ -204,6 +204,7 @@ void free_ctx(psi_ctx* c) {
   if (c->pr_graph) cudaGraphDestroy(c->pr_graph);
   for (void* p : {(void*)c->pr.a, (void*)c->pr.a_first, (void*)c->pr.g, (void*)c->pr.dt,
                   (void*)c->pr.x0, (void*)c->pr.pi, (void*)c->g.nlead, (void*)c->g.kinv,
+                  (void*)c->g.kw,
                   (void*)c->g.nf_loff, (void*)c->g.nf_leaders, (void*)c->g.nf_wt,
                   (void*)c->g.nf_lm})
     if (p) cudaFreeAsync(p, c->stream);
@@ -250,6 +251,7 @@ SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   A.d = c->g.d1;
   A.lam = c->g.lam;
   A.n_users = (double)c->n;
+  A.n_lab = (int)c->n;
   A.n_act = (int)c->g.n_act;
   A.hot_lim = (int)c->hot_lim;
   A.psi = c->g.psi;
@@ -502,6 +504,37 @@ psi_status ensure_history(psi_ctx* c, long long need) {
   return PSI_OK;
 }
 
+// ||B||_col (reading R1): the column sums of B are lambda_i sum_{j in F(i)} 1/W_j, i.e.
+// the readout psi_i = (d_i + lambda_i S_i) / N of the sweep's own kernels with x = 1/Wt on the
+// active labels, d = lambda K_w (the follower-less followers' 1/Wt, folded at ingest) and N = 1.
+// Computed once per context by one such pass (k_heavy + k_sell/k_tiles + k_fix), instead of a
+// pass over every input edge in the ingest.
+__global__ void k_col_prep(const double* wt, const double* lam, const double* kw, long long na,
+                           double* x, double* dcol) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < na; i += stride) {
+    x[i] = 1.0 / wt[i];
+    dcol[i] = lam[i] * kw[i];
+  }
+}
+
+// max of non-negative doubles (their bit patterns order the same way): warp max + one atomic
+__global__ void k_max_nonneg(const double* v, long long n, unsigned long long* out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned long long m = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double x = v[i];
+    const unsigned long long b = x > 0.0 ? (unsigned long long)__double_as_longlong(x) : 0ull;
+    m = b > m ? b : m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+    m = y > m ? y : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 __global__ void k_unpermute(const double* src, const double* scale, const int* old_of_new,
                             long long n, double* dst) {
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -509,6 +542,41 @@ __global__ void k_unpermute(const double* src, const double* scale, const int* o
     const double v = scale ? src[i] * scale[i] : src[i];
     dst[old_of_new ? old_of_new[i] : i] = v;
   }
+}
+
+cudaError_t column_norm(psi_ctx* c) {
+  const long long na = c->g.n_act;
+  double kc = 0.0;
+  cudaError_t e = cudaSuccess;
+  if (na > 0) {
+    double *dcol = nullptr, *colsum = nullptr;
+    unsigned long long* dmax = nullptr;
+    if ((e = dev_alloc(&dcol, na * sizeof(double), c->stream)) != cudaSuccess) return e;
+    if ((e = dev_alloc(&colsum, na * sizeof(double), c->stream)) != cudaSuccess) return e;
+    if ((e = dev_alloc(&dmax, sizeof(unsigned long long), c->stream)) != cudaSuccess) return e;
+    cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), c->stream);
+    const int grid = (int)std::max<long long>(1, std::min<long long>((na + 255) / 256, 148LL * 16));
+    k_col_prep<<<grid, 256, 0, c->stream>>>(c->g.wt, c->g.lam, c->g.kw, na, c->x[0], dcol);
+    SweepArgs A = make_args(c, 0);
+    A.use_cond = 0;
+    A.d = dcol;
+    A.n_users = 1.0;
+    A.psi = colsum;                            // (st->iter = 0: the pass reads x[0])
+    if ((e = launch_sweep(c, &A, true)) != cudaSuccess) return e;
+    k_max_nonneg<<<grid, 256, 0, c->stream>>>(colsum, na, dmax);
+    unsigned long long h = 0;
+    if ((e = cudaMemcpyAsync(&h, dmax, sizeof(h), cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return e;
+    memcpy(&kc, &h, 8);
+    cudaFreeAsync(dcol, c->stream);
+    cudaFreeAsync(colsum, c->stream);
+    cudaFreeAsync(dmax, c->stream);
+  }
+  c->g.kappa_col = kc;
+  if (c->g.kw) cudaFreeAsync(c->g.kw, c->stream);
+  c->g.kw = nullptr;
+  return cudaGetLastError();
 }
 
 psi_status copy_out(const psi_ctx* c, const double* src, const double* scale, double* out,
@@ -926,6 +994,7 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   B_CK(dev_alloc(&c->st, sizeof(LoopState), c->stream));
   B_CK(dev_alloc(&c->prm, sizeof(LoopParams), c->stream));
   B_CK(cudaMemsetAsync(c->st, 0, sizeof(LoopState), c->stream));
+  B_CK(column_norm(c));                               // ||B||_col (x[0] is scratch until here)
   // Follower-less users keep x = a0 in both buffers for ever (they are never written).
   B_CK(cudaMemcpyAsync(c->x[0], c->g.a0, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   B_CK(cudaMemcpyAsync(c->x[1], c->g.a0, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));

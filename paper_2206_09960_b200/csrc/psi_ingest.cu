@@ -10,8 +10,9 @@
 //     in a fixed order (ascending leader) -- deterministic, no fp atomics;
 //  3. per-user kernel constants c = mu/w, d = lambda/w,
 //     Wt = W (or 1 if W = 0, reading R5), a = c/Wt, g = mu/Wt;
-//  4. ||B|| in all three readings (R1): kappa_row = max_n Lambda_n/W_n,
-//     kappa_col = max_i lambda_i sum_{j in F(i)} 1/W_j; rho_A = max_n M_n/W_n;
+//  4. ||B|| in all three readings (R1): kappa_row = max_n Lambda_n/W_n, rho_A = max_n M_n/W_n
+//     (kappa_col = max_i lambda_i sum_{j in F(i)} 1/W_j is one pass of the sweep's own
+//     kernels over x = 1/Wt after the ingest, psi_api.cu);
 //  5. locality relabel: users WITH followers ("active": their s can
 //     change) get labels [0, n_act), follower-less users [n_act, n).  Inside the active
 //     range: users with >= 2 leaders sorted by leader count, descending (their x is
@@ -40,6 +41,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 namespace psi {
@@ -252,47 +255,6 @@ __global__ void k_norm_long(const int* list, int nlist, const int* loff, const i
   }
 }
 
-// 1/Wt per user, once (the column sums below gather it per edge instead of dividing per edge:
-// the same rounded reciprocals, so the same sums)
-__global__ void k_recip(const double* wt, long long n, double* iw) {
-  GRID_STRIDE(i, n) iw[i] = 1.0 / wt[i];
-}
-
-// column sums of B = lambda_i sum_{j in F(i)} 1/W_j: thread per short leader row ...
-__global__ void k_kappa_col_short(const int* rp, const int* idx, const double* iw,
-                                  const double* lam, int n, unsigned long long* kmax) {
-  for (long long base = blockIdx.x * (long long)blockDim.x; base < n;
-       base += (long long)gridDim.x * blockDim.x) {
-    const long long i = base + threadIdx.x;
-    unsigned long long m = 0;
-    if (i < n) {
-      const int b = rp[i], e = rp[i + 1];
-      if (e > b && e - b <= kShort) {
-        double s = 0.0;
-        for (int q = b; q < e; ++q) s += iw[idx[q]];
-        m = dbits(lam[i] * s);
-      }
-    }
-    m = warp_max_u64(m);
-    if ((threadIdx.x & 31) == 0 && m) atomicMax(kmax + 2, m);
-  }
-}
-
-// ... and a warp per long one
-__global__ void k_kappa_col_long(const int* list, int nlist, const int* rp, const int* idx,
-                                 const double* iw, const double* lam, unsigned long long* kmax) {
-  const int lane = threadIdx.x & 31;
-  WARP_STRIDE(k, nlist) {
-    const int i = list[k];
-    const int b = rp[i], e = rp[i + 1];
-    double s = 0.0;
-    for (int q = b + lane; q < e; q += 32) s += iw[idx[q]];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-    if (lane == 0) atomicMax(kmax + 2, dbits(lam[i] * s));
-  }
-}
-
 // ------------------------------------------------------------------ 5. relabel
 
 // class histogram: one atomic per class and warp (per-thread atomics on 5 counters serialise)
@@ -423,11 +385,13 @@ __global__ void k_mark_heavy(const int* act, int n, int min_act, unsigned char* 
 
 // new active row r: #active followers in the edge stream (for heavy rows r < n_heavy only
 // those with label >= H; the others, hc[r], go to k_heavy), and K_r = sum of a_n over
-// follower-less followers.  Thread per short row / warp per long row (see kShort).
+// follower-less followers (+ the same sums of 1/max(|L(n)|, 1) for PageRank and of 1/Wt_n for
+// ||B||_col, psi_api.cu).  Thread per short row / warp per long row (see kShort).
 struct RowCountArgs {
   const int* rp; const int* idx; const int* old_of_new; const unsigned char* cls;
   const int* new_of_old; const double* a_old; const int* nlead; int n_act, n_heavy, H;
   int* cnt; long long* hc; double* K; double* Kinv;
+  const double* wt_old; double* Kw;   // Kw_r = sum of 1/Wt_n over follower-less followers
 };
 
 __global__ void k_row_count_short(RowCountArgs R) {
@@ -437,19 +401,21 @@ __global__ void k_row_count_short(RowCountArgs R) {
     if (e - b > kShort) continue;
     const bool heavy = r < R.n_heavy;
     int c = 0, h = 0;
-    double k = 0.0, ki = 0.0;
+    double k = 0.0, ki = 0.0, kw = 0.0;
     for (int q = b; q < e; ++q) {
       const int v = R.idx[q];
       const int nv = R.new_of_old[v];                 // follower-less <=> label >= n_act
       if (nv >= R.n_act) {
         k += R.a_old[v];
         ki += 1.0 / (double)max(R.nlead[v], 1);
+        kw += 1.0 / R.wt_old[v];
       } else if (heavy && nv < R.H) ++h;
       else ++c;
     }
     R.cnt[r] = c > 0 ? c : 1;      // 0 -> one pseudo edge
     R.K[r] = k;
     R.Kinv[r] = ki;
+    R.Kw[r] = kw;
     if (heavy) R.hc[r] = h;
   }
 }
@@ -462,13 +428,14 @@ __global__ void k_row_count_long(RowCountArgs R, const int* list, int nlist) {
     const int b = R.rp[o], e = R.rp[o + 1];
     const bool heavy = r < R.n_heavy;
     int c = 0, h = 0;
-    double k = 0.0, ki = 0.0;
+    double k = 0.0, ki = 0.0, kw = 0.0;
     for (int q = b + lane; q < e; q += 32) {
       const int v = R.idx[q];
       const int nv = R.new_of_old[v];                 // follower-less <=> label >= n_act
       if (nv >= R.n_act) {
         k += R.a_old[v];
         ki += 1.0 / (double)max(R.nlead[v], 1);
+        kw += 1.0 / R.wt_old[v];
       } else if (heavy && nv < R.H) ++h;
       else ++c;
     }
@@ -478,11 +445,13 @@ __global__ void k_row_count_long(RowCountArgs R, const int* list, int nlist) {
     for (int s = 16; s > 0; s >>= 1) {
       k += __shfl_xor_sync(kFull, k, s);
       ki += __shfl_xor_sync(kFull, ki, s);
+      kw += __shfl_xor_sync(kFull, kw, s);
     }
     if (lane == 0) {
       R.cnt[r] = c > 0 ? c : 1;
       R.K[r] = k;
       R.Kinv[r] = ki;
+      R.Kw[r] = kw;
       if (heavy) R.hc[r] = h;
     }
   }
@@ -847,29 +816,34 @@ namespace {
 // Heavy-row plan (psi_heavy.cu): panels of <= out.heavy_slots slots and ~e_panel hot entries,
 // virtual rows of <= vmax entries, contiguous slot ranges per consumer warp balanced by
 // entries; then the entry lists (panel, segment, warp) sorted by (slot, label).
-int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcnt, Tmp& hoff,
-                     cudaStream_t s, Trace& tr, char* msg, size_t msg_len) {
-  const int nseg = out.nseg;
-  const int sh = out.heavy_seg_shift;
-  const int HW = out.heavy_warps, SLOTS = out.heavy_slots;
-  // host buffers of the plan are thread_local and keep their capacity: fresh multi-MB vectors
-  // cost ~1 page fault per 4 KB on every build (~40 ms at C5, measured)
-  static thread_local std::vector<long long> hc;
-  hc.resize(NH);
-  IG_CK(cudaMemcpyAsync(hc.data(), hcnt.p, (size_t)NH * sizeof(long long), cudaMemcpyDeviceToHost, s));
-  // the hot followers of each row stay in input order: the entries are sorted by
-  // (list, slot, label) below, and the round-robin virtual-row split only needs a fixed order
-  IG_CK(cudaStreamSynchronize(s));
+//
+// Host part of the plan (panels, virtual-row slots, per-warp slot ranges) from the hot-entry
+// count of every heavy row.  Pure host work: psi ingest runs it on a helper thread while the
+// device builds the edge stream.  Its buffers persist (a fresh multi-MB vector costs ~1 page
+// fault per 4 KB on every build, ~40 ms at C5, measured) and are guarded by a mutex.
+struct HeavyHostPlan {
+  std::mutex mu;
+  std::vector<long long> hc;
+  std::vector<int> prow, row_panel, pslot_base, wslot;
+  std::vector<int2> rslot;
+  std::vector<unsigned char> slot_warp;
+  int npanels = 0;
+};
+HeavyHostPlan& heavy_host_plan() {
+  static HeavyHostPlan p;
+  return p;
+}
 
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long pps = std::max(1, env_int("PSI_HEAVY_PPS", kDefaultHeavyPPS));
-  const long long e_panel = std::max<long long>((n_ent + pps * sms - 1) / (pps * sms), 32768);
+void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOTS, int sms, int pps) {
+  const std::vector<long long>& hc = P.hc;
+  const long long e_panel = std::max<long long>((n_ent + (long long)pps * sms - 1) / ((long long)pps * sms), 32768);
   const long long vmax = std::max<long long>(e_panel / (2 * HW), 64);
-  static thread_local std::vector<int> prow, row_panel, pslot_base, wslot;
-  static thread_local std::vector<int2> rslot;
-  static thread_local std::vector<unsigned char> slot_warp;
+  std::vector<int>& prow = P.prow;
+  std::vector<int>& row_panel = P.row_panel;
+  std::vector<int>& pslot_base = P.pslot_base;
+  std::vector<int>& wslot = P.wslot;
+  std::vector<int2>& rslot = P.rslot;
+  std::vector<unsigned char>& slot_warp = P.slot_warp;
   prow.assign(1, 0);
   pslot_base.assign(1, 0);
   wslot.clear();
@@ -913,9 +887,24 @@ int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hcn
     p_ent += h;
   }
   close_panel(NH);
-  const int npanels = (int)prow.size() - 1;
+  P.npanels = (int)prow.size() - 1;
+}
+
+// Heavy-row plan (psi_heavy.cu), device part: the host plan P (already made) uploaded, then the
+// entry lists (panel, segment, warp) sorted by (slot, label) and bank-balanced.
+int build_heavy_plan(IngestOut& out, int NH, long long n_ent, Tmp& hot, Tmp& hoff,
+                     HeavyHostPlan& P, cudaStream_t s, Trace& tr, char* msg, size_t msg_len) {
+  const int nseg = out.nseg;
+  const int sh = out.heavy_seg_shift;
+  const int HW = out.heavy_warps, SLOTS = out.heavy_slots;
+  const std::vector<int>& prow = P.prow;
+  const std::vector<int>& row_panel = P.row_panel;
+  const std::vector<int>& pslot_base = P.pslot_base;
+  const std::vector<int>& wslot = P.wslot;
+  const std::vector<int2>& rslot = P.rslot;
+  const std::vector<unsigned char>& slot_warp = P.slot_warp;
+  const int npanels = P.npanels;
   out.npanels = npanels;
-  tr.mark("  heavy: host panel plan");
   out.heavy_entries = n_ent;
 
   IG_CK(dev_alloc(&out.h_prow, prow.size() * sizeof(int), s));
@@ -1558,17 +1547,6 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
           longu.as<int>(), (int)nlong, loff.as<int>(), vals.Current(), lm.as<double2>(),
           a_old.as<double>(), g_old.as<double>(), wt_old.as<double>(), d_old.as<double>(),
           first_leader.as<int>(), kmax);
-    {
-      Tmp iw;
-      IG_CK(iw.alloc((size_t)n * sizeof(double)));
-      k_recip<<<grid_for(n, 256), 256, 0, s>>>(wt_old.as<double>(), n, iw.as<double>());
-      k_kappa_col_short<<<grid_for(n, 256), 256, 0, s>>>(rp, idx_in, iw.as<double>(), lam, N, kmax);
-      nlong = long_segments(rp, nullptr, N, kShort, s, longu);
-      if (nlong < 0) IG_CK(cudaErrorMemoryAllocation);
-      if (nlong > 0)
-        k_kappa_col_long<<<grid_for(nlong * 32, 256), 256, 0, s>>>(longu.as<int>(), (int)nlong, rp,
-                                                                   idx_in, iw.as<double>(), lam, kmax);
-    }
     if (nprof > 1) {
       // the constants (a, g, Wt, d) and ||B||_row of every profile, old labels, same kernels
       IG_CK(bold.alloc((size_t)nprof * 4 * n * sizeof(double)));
@@ -1618,7 +1596,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   IG_CK(cudaStreamSynchronize(s));
   memcpy(&out.kappa_row, &h[0], 8);
   memcpy(&out.rho_A, &h[1], 8);
-  memcpy(&out.kappa_col, &h[2], 8);
+  out.kappa_col = 0.0;                      // set by psi_build_graph's column pass
   out.n_leaderless = (long long)h[4];
   out.n_g = n - out.n_leaderless;
   const long long n_inactive = (long long)h[8 + C_INACTIVE];
@@ -1808,6 +1786,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   const int NA = (int)out.n_act;
   Tmp cntr, K, rp_new;
   IG_CK(dev_alloc(&out.kinv, (size_t)(NA > 0 ? NA : 1) * sizeof(double), s));
+  IG_CK(dev_alloc(&out.kw, (size_t)(NA > 0 ? NA : 1) * sizeof(double), s));
   IG_CK(cntr.alloc((size_t)(NA + 1) * sizeof(int)));
   IG_CK(K.alloc((size_t)(NA > 0 ? NA : 1) * sizeof(double)));
   IG_CK(rp_new.alloc((size_t)(NA + 1) * sizeof(int)));
@@ -1824,7 +1803,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     if (nlongr < 0) IG_CK(cudaErrorMemoryAllocation);
     RowCountArgs R{rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
                    a_old.as<double>(), nlead.as<int>(), NA, NH, Hs, cntr.as<int>(),
-                   hcnt.as<long long>(), K.as<double>(), out.kinv};
+                   hcnt.as<long long>(), K.as<double>(), out.kinv, wt_old.as<double>(), out.kw};
     k_row_count_short<<<grid_for(NA, 256), 256, 0, s>>>(R);
     if (nlongr > 0)
       k_row_count_long<<<grid_for(nlongr * 32, 256), 256, 0, s>>>(R, longr.as<int>(), (int)nlongr);
@@ -1842,6 +1821,28 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
                           cudaMemcpyDeviceToHost, s));
     IG_CK(cudaStreamSynchronize(s));
   }
+  // the heavy rows' host plan runs on a helper thread while the device builds the edge stream
+  HeavyHostPlan& HP = heavy_host_plan();
+  std::unique_lock<std::mutex> hp_lock(HP.mu, std::defer_lock);
+  std::thread hp_thread;
+  if (NH > 0) {
+    hp_lock.lock();
+    HP.hc.resize(NH);
+    IG_CK(cudaMemcpyAsync(HP.hc.data(), hcnt.p, (size_t)NH * sizeof(long long),
+                          cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int pps = std::max(1, env_int("PSI_HEAVY_PPS", kDefaultHeavyPPS));
+    hp_thread = std::thread(plan_heavy_host, std::ref(HP), NH, n_hot_ent, out.heavy_warps,
+                            out.heavy_slots, sms, pps);
+  }
+  // joined on every exit path below (an early error return must not leave it running)
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() { if (t.joinable()) t.join(); }
+  } hp_join{hp_thread};
   Tmp hot;
   IG_CK(hot.alloc((size_t)(n_hot_ent > 0 ? n_hot_ent : 1) * sizeof(int)));
   {
@@ -1884,7 +1885,10 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   }
   tr.mark("edge stream");
   if (NH > 0) {
-    int rc2 = build_heavy_plan(out, NH, n_hot_ent, hot, hcnt, hoff, s, tr, msg, msg_len);
+    hp_thread.join();
+    tr.mark("  heavy: host plan joined");
+    int rc2 = build_heavy_plan(out, NH, n_hot_ent, hot, hoff, HP, s, tr, msg, msg_len);
+    hp_lock.unlock();
     if (rc2 != PSI_OK) return rc2;
   }
   hot.reset();

@@ -176,6 +176,7 @@ struct SweepArgs {
   const double* d;           // readout constant d + lambda K    [n_act]
   const double* lam;         //                                  [n_act]
   double n_users;            // N of psi = (...)/N
+  int n_lab;                 // labels 0..n_lab of x (n_lab = n: the zero sentinel; PSI_CHECKS)
   int n_act;
   int hot_lim;               // labels < hot_lim: L2 evict_last for x gathers/stores
   int hot_smem;              // labels < hot_smem: gathered from the CTA's shared-memory copy
@@ -239,6 +240,8 @@ struct IngestOut {
   int* old_of_new = nullptr;  // [n]
   int* nlead = nullptr;       // [n]     #leaders |L(j)| (PageRank out-degree), new labels
   double* kinv = nullptr;     // [n_act] sum over follower-less followers n of 1/max(|L(n)|, 1)
+  double* kw = nullptr;       // [n_act] sum over follower-less followers n of 1/Wt_n (||B||_col;
+                              //         freed once the column pass has run)
   // Power-NF (caller labels; kept when m <= kPowerNfMaxEdges, else nf_loff == nullptr)
   int* nf_loff = nullptr;
   int* nf_leaders = nullptr;

@@ -204,7 +204,7 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
 #else
       const unsigned lab = w[q] & kLabelMask;
 #endif
-      PSI_ASSERT((double)lab <= A.n_users);             // sentinel label n holds x = 0
+      PSI_ASSERT((int)lab <= A.n_lab);                  // sentinel label n holds x = 0
       fl |= (w[q] >> 31) << q;
 #if defined(PSI_EXP_ONELOAD)                // experiment builds: one global load variant,
       if (lab < hs) v[q] = hot[lab];          // the L2 policy chosen per lane
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kSellWarps * 32, 1) k_sell(SweepArgs A) {
   // with predicated loads serialises on the shared destination register, and one load variant
   // under an address-range L2 policy loses the L1 hits: both measured.)
   auto gx = [&](unsigned lab) -> double {
-    PSI_ASSERT((double)lab <= A.n_users);
+    PSI_ASSERT((int)lab <= A.n_lab);
     if (lab < hs) return hot[lab];
     if (lab < l1_lim) return ld_l1last(xs + lab, pl);
     if (lab >= single_lo) return ld_l1first(xs + lab, pf);
