@@ -392,6 +392,7 @@ struct RowCountArgs {
   const int* new_of_old; const double* a_old; const int* nlead; int n_act, n_heavy, H;
   int* cnt; long long* hc; double* K; double* Kinv;
   const double* wt_old; double* Kw;   // Kw_r = sum of 1/Wt_n over follower-less followers
+  int* lab;                           // [m] new label of every input edge's follower (for the fill)
 };
 
 __global__ void k_row_count_short(RowCountArgs R) {
@@ -405,6 +406,7 @@ __global__ void k_row_count_short(RowCountArgs R) {
     for (int q = b; q < e; ++q) {
       const int v = R.idx[q];
       const int nv = R.new_of_old[v];                 // follower-less <=> label >= n_act
+      R.lab[q] = nv;
       if (nv >= R.n_act) {
         k += R.a_old[v];
         ki += 1.0 / (double)max(R.nlead[v], 1);
@@ -432,6 +434,7 @@ __global__ void k_row_count_long(RowCountArgs R, const int* list, int nlist) {
     for (int q = b + lane; q < e; q += 32) {
       const int v = R.idx[q];
       const int nv = R.new_of_old[v];                 // follower-less <=> label >= n_act
+      R.lab[q] = nv;
       if (nv >= R.n_act) {
         k += R.a_old[v];
         ki += 1.0 / (double)max(R.nlead[v], 1);
@@ -462,8 +465,8 @@ __global__ void k_row_count_long(RowCountArgs R, const int* list, int nlist) {
 // gets one pseudo edge to the sentinel label n (x[n] = 0).  Thread per short row / warp
 // per long row (ballot compaction keeps the input order).
 struct RowFillArgs {
-  const int* rp; const int* idx; const int* old_of_new; const unsigned char* cls;
-  const int* new_of_old; const int* rp_new; int n_act, n, n_heavy, H;
+  const int* rp; const int* lab; const int* old_of_new; const unsigned char* cls;
+  const int* rp_new; int n_act, n, n_heavy, H;   // lab: new follower labels (k_row_count)
   const long long* hoff; int* idx_new; int* hot;
 };
 
@@ -477,7 +480,7 @@ __global__ void k_row_fill_short(RowFillArgs R) {
     int out = start;
     long long hout = heavy ? R.hoff[r] : 0;
     for (int q = b; q < e; ++q) {
-      const int nv = R.new_of_old[R.idx[q]];
+      const int nv = R.lab[q];
       if (nv >= R.n_act) continue;                     // follower-less: folded into K
       if (heavy && nv < R.H) R.hot[hout++] = nv;
       else R.idx_new[out++] = nv;
@@ -499,7 +502,7 @@ __global__ void k_row_fill_long(RowFillArgs R, const int* list, int nlist) {
     for (int q0 = b; q0 < e; q0 += 32) {
       const int q = q0 + lane;
       int nv = R.n_act;
-      if (q < e) nv = R.new_of_old[R.idx[q]];
+      if (q < e) nv = R.lab[q];
       const bool act = nv < R.n_act;                  // follower-less <=> label >= n_act
       const bool is_hot = act && heavy && nv < R.H;
       const bool is_str = act && !is_hot;
@@ -1796,14 +1799,16 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   IG_CK(hcnt.alloc((size_t)(NH + 1) * sizeof(long long)));
   IG_CK(hoff.alloc((size_t)(NH + 1) * sizeof(long long)));
   IG_CK(cudaMemsetAsync(hcnt.p, 0, (size_t)(NH + 1) * sizeof(long long), s));
-  Tmp longr;
+  Tmp longr, labmap;
+  IG_CK(labmap.alloc((size_t)std::max<long long>(m, 1) * sizeof(int)));
   long long nlongr = 0;
   if (NA > 0) {
     nlongr = long_segments(rp, out.old_of_new, NA, kShort, s, longr);
     if (nlongr < 0) IG_CK(cudaErrorMemoryAllocation);
     RowCountArgs R{rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
                    a_old.as<double>(), nlead.as<int>(), NA, NH, Hs, cntr.as<int>(),
-                   hcnt.as<long long>(), K.as<double>(), out.kinv, wt_old.as<double>(), out.kw};
+                   hcnt.as<long long>(), K.as<double>(), out.kinv, wt_old.as<double>(), out.kw,
+                   labmap.as<int>()};
     k_row_count_short<<<grid_for(NA, 256), 256, 0, s>>>(R);
     if (nlongr > 0)
       k_row_count_long<<<grid_for(nlongr * 32, 256), 256, 0, s>>>(R, longr.as<int>(), (int)nlongr);
@@ -1869,7 +1874,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     IG_CK(dev_alloc(&out.edges, (size_t)(m_pad > 0 ? m_pad : 4) * sizeof(unsigned), s));
     int* ed = (int*)out.edges;
     if (NA > 0) {
-      RowFillArgs R{rp, idx_in, out.old_of_new, cls.as<unsigned char>(), new_of_old.as<int>(),
+      RowFillArgs R{rp, labmap.as<int>(), out.old_of_new, cls.as<unsigned char>(),
                     rp_new.as<int>(), NA, N, NH, Hs, hoff.as<long long>(), ed, hot.as<int>()};
       k_row_fill_short<<<grid_for(NA, 256), 256, 0, s>>>(R);
       if (nlongr > 0)
@@ -1883,6 +1888,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     }
     IG_CK(cudaStreamSynchronize(s));
   }
+  labmap.reset();
   tr.mark("edge stream");
   if (NH > 0) {
     hp_thread.join();
