@@ -16,6 +16,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -182,7 +183,7 @@ unsigned long long pool_keep_bytes() {
 
 // Reserve a build's working set in ONE block of the pool the first time a graph this large
 // is built on the device: later builds carve their temporaries out of it instead of mapping
-// new memory around fragments (measured: +0.2-0.6 s C5 builds without it).
+// new memory around fragments (measured: +0.2-2 s C5 builds without enough of it).
 void pool_reserve(int dev, unsigned long long est, cudaStream_t s) {
   if (dev < 0 || dev >= kMaxDevices || pool_keep_bytes() != ~0ull) return;
   std::lock_guard<std::mutex> lk(g_pool_mu);
@@ -854,9 +855,10 @@ psi_status psi_empty_cache(void) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
     return fail(PSI_E_CUDA, "cudaGetDevice failed");
+  API_CK(cudaDeviceSynchronize());                    // stream-ordered frees have completed
+  scratch_release(dev);                               // the build scratch (its own lock first)
   std::lock_guard<std::mutex> lk(g_pool_mu);
   if (!g_pool[dev]) return PSI_OK;
-  API_CK(cudaDeviceSynchronize());                    // stream-ordered frees have completed
   API_CK(cudaMemPoolTrimTo(g_pool[dev], 0));
   g_reserved_for[dev] = 0;
   return PSI_OK;
@@ -888,8 +890,18 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   c->m = m;
   c->dev = dev;
   c->stream = (cudaStream_t)stream;
-  pool_reserve(dev, 16ull * (unsigned long long)m + (unsigned long long)nprof * 160ull *
-                        (unsigned long long)n + (256ull << 20), c->stream);
+  // (the staged inputs and the transpose's sort arrays come from the build scratch, not the pool)
+  {
+    // twice the build's pool working set (~12 B per edge + 160 B per user and profile): with
+    // less headroom the pool maps new memory around fragments now and then (C5 builds of
+    // 0.5-2.3 s instead of 0.34 s; a 40 GB block made every repeated build 338-344 ms, measured)
+    unsigned long long est = 2ull * (12ull * (unsigned long long)m +
+                                     (unsigned long long)nprof * 160ull * (unsigned long long)n) +
+                             (256ull << 20);
+    if (const char* e = getenv("PSI_POOL_RESERVE_GB"))        // measurement: a larger block
+      est = std::max(est, (unsigned long long)(atof(e) * (double)(1ull << 30)));
+    pool_reserve(dev, est, c->stream);
+  }
   auto bail = [&](psi_status st) { free_ctx(c); return st; };
 #define B_CK(call)                                                                          \
   do {                                                                                      \
@@ -903,22 +915,25 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   B_CK(cudaEventCreate(&c->ev1));
   B_CK(cudaEventRecord(c->ev0, c->stream));
 
-  // Stage host inputs (borrowed: copied, never retained).
+  // The build's scratch (staged inputs, the transpose's sort arrays) is per device and kept
+  // across builds; this build owns it until the ingest has returned (psi_ingest.cu).
+  std::unique_lock<std::mutex> scratch_lock(*scratch_mutex(dev));
+  // Stage host inputs (borrowed: copied, never retained) in scratch slot 0.
   const long long* rp_d = (const long long*)row_ptr;
   const int* idx_d = followers;
   const double* lam_d = lambda;
   const double* mu_d = mu;
   void* staged[4] = {nullptr, nullptr, nullptr, nullptr};
-  struct Free4 {
-    void** p;
-    cudaStream_t s;
-    ~Free4() { for (int i = 0; i < 4; ++i) if (p[i]) cudaFreeAsync(p[i], s); }
-  } f4{staged, c->stream};
   if (mem_kind == PSI_MEM_HOST) {
-    B_CK(dev_alloc(&staged[0], (n + 1) * sizeof(long long), c->stream));
-    B_CK(dev_alloc(&staged[1], (m > 0 ? m : 1) * sizeof(int), c->stream));
-    B_CK(dev_alloc(&staged[2], nprof * n * sizeof(double), c->stream));
-    B_CK(dev_alloc(&staged[3], nprof * n * sizeof(double), c->stream));
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t b0 = al((n + 1) * sizeof(long long)), b1 = al((m > 0 ? m : 1) * sizeof(int)),
+                 b2 = al(nprof * n * sizeof(double));
+    unsigned char* sp = nullptr;
+    B_CK(scratch_get(dev, 0, b0 + b1 + 2 * b2, (void**)&sp));
+    staged[0] = sp;
+    staged[1] = sp + b0;
+    staged[2] = sp + b0 + b1;
+    staged[3] = sp + b0 + b1 + b2;
     B_CK(cudaMemcpyAsync(staged[0], row_ptr, (n + 1) * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
     if (m > 0)
       B_CK(cudaMemcpyAsync(staged[1], followers, m * sizeof(int), cudaMemcpyHostToDevice, c->stream));
@@ -930,11 +945,26 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
     idx_d = (const int*)staged[1];
     lam_d = (const double*)staged[2];
     mu_d = (const double*)staged[3];
+    if (const char* e = getenv("PSI_TRACE")) {          // ingest trace: the staging copies
+      if (*e == '1') {
+        const auto h0 = std::chrono::steady_clock::now();
+        cudaEvent_t et;
+        cudaEventCreate(&et);
+        cudaEventRecord(et, c->stream);
+        cudaStreamSynchronize(c->stream);
+        float dms = 0.f;
+        cudaEventElapsedTime(&dms, c->ev0, et);
+        cudaEventDestroy(et);
+        fprintf(stderr, "[psi build ] staging H2D (pool allocs + copies)  device %9.2f ms, host wait %9.2f ms\n",
+                dms, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+      }
+    }
   }
 
   char msg[512] = {0};
   int rc = ingest(n, m, rp_d, idx_d, lam_d, mu_d, nprof, c->stream, c->g, msg, sizeof(msg));
   if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
+  scratch_lock.unlock();          // (stream-ordered: a later build's reuse follows this work)
 
   // Iteration buffers.
   c->tc = c->g.sell ? sell_config(n, c->g.sell_shift)

@@ -717,6 +717,11 @@ __global__ void k_split_fill(const int* rows, long long ns, const int* rp, int t
 // which keeps freed temporaries reserved while a build runs, so the ingest's phases reuse
 // each other's memory instead of re-mapping it)
 thread_local cudaStream_t g_tmp_stream = nullptr;
+// a view of scratch memory with Tmp's accessors
+struct Span {
+  void* p;
+  template <class T> T* as() const { return (T*)p; }
+};
 struct Tmp {
   void* p = nullptr;
   ~Tmp() { reset(); }
@@ -727,6 +732,58 @@ struct Tmp {
   }
   template <class T> T* as() const { return (T*)p; }
 };
+
+}  // namespace
+
+// Per-device scratch for the build's two biggest short-lived buffers -- the staged host inputs
+// (slot 0, psi_api.cu) and the transpose's sort arrays (slot 1) -- allocated with cudaMalloc
+// outside the pool and kept across builds (like a library workspace): the pool then holds only
+// the context's arrays and smaller temporaries, and repeated builds no longer stall on
+// re-mapped pool memory around fragments (C5: 0.2 s transpose phases and 1-1.4 s builds now
+// and then, measured).  psi_empty_cache() frees it.  The owning build holds the mutex.
+namespace {
+constexpr int kScratchDevices = 64;
+struct DevScratch {
+  std::mutex mu;
+  void* p[2] = {nullptr, nullptr};
+  size_t cap[2] = {0, 0};
+};
+DevScratch g_scratch[kScratchDevices];
+}  // namespace
+
+std::mutex* scratch_mutex(int dev) {
+  return (dev >= 0 && dev < kScratchDevices) ? &g_scratch[dev].mu : nullptr;
+}
+cudaError_t scratch_get(int dev, int slot, size_t bytes, void** out) {
+  if (dev < 0 || dev >= kScratchDevices || slot < 0 || slot > 1) return cudaErrorInvalidValue;
+  DevScratch& S = g_scratch[dev];
+  bytes = (bytes + 255) & ~(size_t)255;
+  if (S.cap[slot] < bytes) {
+    if (S.p[slot]) {
+      cudaDeviceSynchronize();
+      cudaFree(S.p[slot]);
+      S.p[slot] = nullptr;
+      S.cap[slot] = 0;
+    }
+    cudaError_t e = cudaMalloc(&S.p[slot], bytes);
+    if (e != cudaSuccess) { S.p[slot] = nullptr; return e; }
+    S.cap[slot] = bytes;
+  }
+  *out = S.p[slot];
+  return cudaSuccess;
+}
+void scratch_release(int dev) {
+  if (dev < 0 || dev >= kScratchDevices) return;
+  DevScratch& S = g_scratch[dev];
+  std::lock_guard<std::mutex> lk(S.mu);
+  for (int i = 0; i < 2; ++i) {
+    if (S.p[i]) cudaFree(S.p[i]);
+    S.p[i] = nullptr;
+    S.cap[i] = 0;
+  }
+}
+
+namespace {
 
 int grid_for(long long work, int block, int cap = 148 * 16) {
   long long g = (work + block - 1) / block;
@@ -1498,12 +1555,23 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   int end_bit = 1;
   while ((1ll << end_bit) < n) ++end_bit;
   {
-    Tmp leader_e, follower_e, leader_s, follower_s, loff, sort_tmp, scan_tmp;
-    IG_CK(leader_e.alloc((size_t)m * sizeof(int)));
-    IG_CK(follower_e.alloc((size_t)m * sizeof(int)));
-    IG_CK(leader_s.alloc((size_t)m * sizeof(int)));
-    IG_CK(follower_s.alloc((size_t)m * sizeof(int)));
+    // the four m-sized sort arrays and the sort's temporary storage: the build's scratch
+    // slot 1 (kept across builds, outside the pool; the caller holds its mutex)
+    Tmp loff, scan_tmp;
     IG_CK(loff.alloc((size_t)(n + 1) * sizeof(int)));
+    int dev = 0;
+    IG_CK(cudaGetDevice(&dev));
+    size_t tb = 0;
+    {
+      cub::DoubleBuffer<unsigned> k0(nullptr, nullptr);
+      cub::DoubleBuffer<int> v0(nullptr, nullptr);
+      IG_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, v0, Mm, 0, end_bit, s));
+    }
+    const size_t ma = (((size_t)std::max<long long>(m, 1) * sizeof(int)) + 255) & ~(size_t)255;
+    unsigned char* sc = nullptr;
+    IG_CK(scratch_get(dev, 1, 4 * ma + tb, (void**)&sc));
+    const Span leader_e{sc}, follower_e{sc + ma}, leader_s{sc + 2 * ma}, follower_s{sc + 3 * ma},
+        sort_tmp{sc + 4 * ma};
     // (follower, leader) pairs in input order: keys = a copy of the input followers, values
     // = the row (leader) of every edge; a stable radix sort by follower is the transpose
     if (m > 0)
@@ -1519,9 +1587,6 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     }
     cub::DoubleBuffer<unsigned> keys((unsigned*)follower_e.p, (unsigned*)follower_s.p);
     cub::DoubleBuffer<int> vals(leader_e.as<int>(), leader_s.as<int>());
-    size_t tb = 0;
-    IG_CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, vals, Mm, 0, end_bit, s));
-    IG_CK(sort_tmp.alloc(tb));
     IG_CK(cub::DeviceRadixSort::SortPairs(sort_tmp.p, tb, keys, vals, Mm, 0, end_bit, s));
     // leaders of user u = sorted pairs [loff[u], loff[u+1]) (lower bounds); #leaders
     k_lower_bounds<<<grid_for(n + 1, 256), 256, 0, s>>>(keys.Current(), Mm, N, loff.as<int>(),

@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <mutex>
 #include <vector>
 
 // PSI_CHECKS builds (lib/libpsi_checked.so, PSI_LIB=checked) add device-side bounds checks
@@ -339,6 +340,13 @@ cudaError_t pagerank_prep(const IngestOut& G, long long n, double alpha, const P
                           cudaStream_t s);
 cudaError_t pagerank_readout(const IngestOut& G, long long n, double alpha, const double* xT,
                              long long T, const PrBuffers& B, cudaStream_t s);
+
+// Build scratch (psi_ingest.cu): two per-device buffers kept across builds outside the pool --
+// slot 0 the staged host inputs, slot 1 the transpose's sort arrays.  A build holds
+// *scratch_mutex(dev) from staging until ingest returns; psi_empty_cache frees them.
+std::mutex* scratch_mutex(int dev);
+cudaError_t scratch_get(int dev, int slot, size_t bytes, void** out);
+void scratch_release(int dev);
 
 // Returns 0 or a negative psi_status; msg gets a description on error.  nprof > 1: lam_dev /
 // mu_dev hold nprof profiles (profile-major, nprof * n); the single-profile outputs are those
