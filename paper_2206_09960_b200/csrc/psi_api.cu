@@ -924,6 +924,16 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   const double* lam_d = lambda;
   const double* mu_d = mu;
   void* staged[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t side = nullptr;
+  cudaEvent_t act_ev = nullptr;
+  struct SideDone {                     // the side copy has finished before the build returns
+    cudaStream_t& s;
+    cudaEvent_t& e;
+    ~SideDone() {
+      if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+      if (e) cudaEventDestroy(e);
+    }
+  } side_done{side, act_ev};
   if (mem_kind == PSI_MEM_HOST) {
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
     const size_t b0 = al((n + 1) * sizeof(long long)), b1 = al((m > 0 ? m : 1) * sizeof(int)),
@@ -937,10 +947,16 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
     B_CK(cudaMemcpyAsync(staged[0], row_ptr, (n + 1) * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
     if (m > 0)
       B_CK(cudaMemcpyAsync(staged[1], followers, m * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    // lambda, mu on a side stream (first used after the transpose: the ingest waits on act_ev),
+    // so their copy overlaps the graph's validation and transpose
+    B_CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    B_CK(cudaEventCreateWithFlags(&act_ev, cudaEventDisableTiming));
+    B_CK(cudaEventRecord(act_ev, c->stream));                 // (after the inputs' staging slot
+    B_CK(cudaStreamWaitEvent(side, act_ev, 0));               //  is this build's, stream order)
     B_CK(cudaMemcpyAsync(staged[2], lambda, nprof * n * sizeof(double), cudaMemcpyHostToDevice,
-                         c->stream));
-    B_CK(cudaMemcpyAsync(staged[3], mu, nprof * n * sizeof(double), cudaMemcpyHostToDevice,
-                         c->stream));
+                         side));
+    B_CK(cudaMemcpyAsync(staged[3], mu, nprof * n * sizeof(double), cudaMemcpyHostToDevice, side));
+    B_CK(cudaEventRecord(act_ev, side));
     rp_d = (const long long*)staged[0];
     idx_d = (const int*)staged[1];
     lam_d = (const double*)staged[2];
@@ -962,7 +978,7 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
   }
 
   char msg[512] = {0};
-  int rc = ingest(n, m, rp_d, idx_d, lam_d, mu_d, nprof, c->stream, c->g, msg, sizeof(msg));
+  int rc = ingest(n, m, rp_d, idx_d, lam_d, mu_d, nprof, c->stream, c->g, msg, sizeof(msg), act_ev);
   if (rc != PSI_OK) return bail(fail(rc, "%s", msg));
   scratch_lock.unlock();          // (stream-ordered: a later build's reuse follows this work)
 

@@ -1495,7 +1495,7 @@ int make_tiling(const int* rp_new, int NA, long long m_pad, int tile, cudaStream
 
 int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
            const double* lam, const double* mu, int nprof, cudaStream_t s, IngestOut& out,
-           char* msg, size_t msg_len) {
+           char* msg, size_t msg_len, cudaEvent_t act_ready) {
   if (nprof < 1) nprof = 1;
   const int N = (int)n, Mm = (int)m;
   Tmp flags;
@@ -1508,9 +1508,6 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   // (the pool's release threshold is set by psi_build_graph: temporaries stay reserved)
   // ---- 1. validation
   k_check_rowptr<<<grid_for(n, 256), 256, 0, s>>>(rp64, n, m, flags.as<int>());
-  for (int p = 0; p < nprof; ++p)
-    k_check_activity<<<grid_for(n, 256), 256, 0, s>>>(lam + (size_t)p * n, mu + (size_t)p * n, n,
-                                                      flags.as<int>());
   IG_CK(cudaMemcpyAsync(&hflags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   IG_CK(cudaStreamSynchronize(s));
   if (hflags & (F_RP0 | F_RPN | F_RPMONO)) {
@@ -1530,10 +1527,6 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
              : (hflags & F_SELF) ? "self loop (a user in its own follower list)"
              : "row not strictly increasing (duplicate or unsorted followers)");
     return PSI_E_GRAPH;
-  }
-  if (hflags & F_ACT) {
-    snprintf(msg, msg_len, "activity: lambda/mu must be finite, >= 0, lambda+mu > 0");
-    return PSI_E_ACTIVITY;
   }
 
   tr.mark("validate");
@@ -1592,6 +1585,18 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     k_lower_bounds<<<grid_for(n + 1, 256), 256, 0, s>>>(keys.Current(), Mm, N, loff.as<int>(),
                                                         nlead.as<int>());
     k_diff<<<grid_for(n, 256), 256, 0, s>>>(loff.as<int>(), N, nlead.as<int>());
+    // the activity vectors (their staging copy may still have been in flight on a side
+    // stream, psi_api.cu): validated here, before their first use
+    if (act_ready) IG_CK(cudaStreamWaitEvent(s, act_ready, 0));
+    for (int p = 0; p < nprof; ++p)
+      k_check_activity<<<grid_for(n, 256), 256, 0, s>>>(lam + (size_t)p * n, mu + (size_t)p * n, n,
+                                                        flags.as<int>());
+    IG_CK(cudaMemcpyAsync(&hflags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+    if (hflags & F_ACT) {
+      snprintf(msg, msg_len, "activity: lambda/mu must be finite, >= 0, lambda+mu > 0");
+      return PSI_E_ACTIVITY;
+    }
     Tmp lm, longu;
     IG_CK(lm.alloc((size_t)n * sizeof(double2)));
     k_pack_activity<<<grid_for(n, 256), 256, 0, s>>>(lam, mu, n, lm.as<double2>());

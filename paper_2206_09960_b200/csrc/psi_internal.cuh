@@ -353,7 +353,7 @@ void scratch_release(int dev);
 // of profile 0, the b_* arrays those of all profiles, and the heavy-row path is off.
 int ingest(long long n, long long m, const long long* rp64_dev, const int* idx_dev,
            const double* lam_dev, const double* mu_dev, int nprof, cudaStream_t s,
-           IngestOut& out, char* msg, size_t msg_len);
+           IngestOut& out, char* msg, size_t msg_len, cudaEvent_t act_ready = nullptr);
 
 // ---- multi-profile batch sweep (psi_batch.cu): kBP profiles per pass over the edge stream
 constexpr int kBP = 4;                   // profiles per group (one 32-byte x gather per edge)
