@@ -368,6 +368,9 @@ __global__ void __launch_bounds__(kSellWarps * 32, 1) k_sell(SweepArgs A) {
   // under an address-range L2 policy loses the L1 hits: both measured.)
   auto gx = [&](unsigned lab) -> double {
     PSI_ASSERT((int)lab <= A.n_lab);
+#ifdef PSI_EXP_GMASK                                     // experiment builds: x confined to L2
+    lab &= (unsigned)(PSI_EXP_GMASK);
+#endif
     if (lab < hs) return hot[lab];
     if (lab < l1_lim) return ld_l1last(xs + lab, pl);
     if (lab >= single_lo) return ld_l1first(xs + lab, pf);
