@@ -84,21 +84,17 @@ __global__ void k_rowptr32(const long long* rp64, int* rp32, long long n1) {
   GRID_STRIDE(r, n1) rp32[r] = (int)rp64[r];
 }
 
-// warp per row: range, self loop, strictly increasing
-__global__ void k_check_edges(const int* rp, const int* idx, int n, int* flags) {
-  const int lane = threadIdx.x & 31;
-  WARP_STRIDE(row, n) {
-    const int b = rp[row], e = rp[row + 1];
-    int f = 0;
-    for (int q = b + lane; q < e; q += 32) {
-      const int v = idx[q];
-      if (v < 0 || v >= n) f |= F_RANGE;
-      if (v == (int)row) f |= F_SELF;
-      if (q + 1 < e && idx[q + 1] <= v) f |= F_ORDER;
-    }
-    f = __reduce_or_sync(kFull, f);
-    if (lane == 0 && f) atomicOr(flags, f);
+// thread per edge (rows expanded): range, self loop, strictly increasing within a row
+__global__ void k_check_edges_flat(const int* idx, const int* row, long long m, int n, int* flags) {
+  int f = 0;
+  GRID_STRIDE(q, m) {
+    const int v = idx[q], r = row[q];
+    if (v < 0 || v >= n) f |= F_RANGE;
+    if (v == r) f |= F_SELF;
+    if (q + 1 < m && row[q + 1] == r && idx[q + 1] <= v) f |= F_ORDER;
   }
+  f = __reduce_or_sync(kFull, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
 }
 
 __global__ void k_check_activity(const double* lam, const double* mu, long long n, int* flags) {
@@ -234,11 +230,22 @@ __global__ void k_norm_long(const int* list, int nlist, const int* loff, const i
     const int u = list[i];
     const int b = loff[u], e = loff[u + 1];
     double W = 0.0, L = 0.0, M = 0.0;
-    for (int q = b + lane; q < e; q += 32) {
-      const double2 v = lm[leaders[q]];
-      W += v.x + v.y;
-      L += v.x;
-      M += v.y;
+    // four strided steps per iteration with their gathers in flight together; the sums take
+    // them in the same order as a one-step loop (bit-identical results)
+    for (int q0 = b + lane; q0 < e; q0 += 128) {
+      int ld[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ld[k] = q0 + 32 * k < e ? leaders[q0 + 32 * k] : -1;
+      double2 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = ld[k] >= 0 ? lm[ld[k]] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (ld[k] < 0) break;
+        W += v[k].x + v[k].y;
+        L += v[k].x;
+        M += v[k].y;
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -258,6 +265,8 @@ __global__ void k_norm_long(const int* list, int nlist, const int* loff, const i
 // ------------------------------------------------------------------ 5. relabel
 
 // class histogram: one atomic per class and warp (per-thread atomics on 5 counters serialise)
+// (into the block's shared counters; flushed once per block by class_flush: one global atomic
+// per class and warp-iteration serialised on 5 addresses took 4-5 ms per pass at C5)
 __device__ __forceinline__ void count_class(unsigned char c, unsigned long long* counts) {
   const unsigned active = __activemask();
   const int lane = threadIdx.x & 31;
@@ -267,17 +276,28 @@ __device__ __forceinline__ void count_class(unsigned char c, unsigned long long*
     if (m && lane == __ffs(m) - 1) atomicAdd(counts + k, (unsigned long long)__popc(m));
   }
 }
+__device__ __forceinline__ void class_init(unsigned long long* sc) {
+  if (threadIdx.x < 5) sc[threadIdx.x] = 0;
+  __syncthreads();
+}
+__device__ __forceinline__ void class_flush(const unsigned long long* sc, unsigned long long* counts) {
+  __syncthreads();
+  if (threadIdx.x < 5 && sc[threadIdx.x]) atomicAdd(counts + threadIdx.x, sc[threadIdx.x]);
+}
 
 __global__ void k_classify(const int* rp, const int* nlead, int n, unsigned char* cls,
                            int* new_of_old, unsigned long long* counts) {
+  __shared__ unsigned long long sc[5];
+  class_init(sc);
   GRID_STRIDE(u, n) {
     const bool active = rp[u + 1] > rp[u];
     const int nl = nlead[u];
     unsigned char c = !active ? C_INACTIVE : nl >= 2 ? C_HOT : nl == 1 ? C_SINGLE : C_ROOT;
     cls[u] = c;
     new_of_old[u] = -1;
-    count_class(c, counts);
+    count_class(c, sc);
   }
+  class_flush(sc, counts);
 }
 
 // selection keys for one relabel stage
@@ -367,6 +387,7 @@ __global__ void k_active_count_long(const int* list, int nlist, const int* rp, c
     const int u = list[i];
     const int b = rp[u], e = rp[u + 1];
     int c = 0;
+#pragma unroll 4
     for (int q = b + lane; q < e; q += 32) c += cls[idx[q]] != C_INACTIVE;
     c = __reduce_add_sync(kFull, c);
     if (lane == 0) act[u] = c;
@@ -376,11 +397,14 @@ __global__ void k_active_count_long(const int* list, int nlist, const int* rp, c
 // heavy rows: active users with >= min_act active followers; recount the classes
 __global__ void k_mark_heavy(const int* act, int n, int min_act, unsigned char* cls,
                              unsigned long long* counts) {
+  __shared__ unsigned long long sc[5];
+  class_init(sc);
   GRID_STRIDE(u, n) {
     unsigned char c = cls[u];
     if (c != C_INACTIVE && act[u] >= min_act) cls[u] = c = C_HEAVY;
-    count_class(c, counts);
+    count_class(c, sc);
   }
+  class_flush(sc, counts);
 }
 
 // new active row r: #active followers in the edge stream (for heavy rows r < n_heavy only
@@ -431,16 +455,25 @@ __global__ void k_row_count_long(RowCountArgs R, const int* list, int nlist) {
     const bool heavy = r < R.n_heavy;
     int c = 0, h = 0;
     double k = 0.0, ki = 0.0, kw = 0.0;
-    for (int q = b + lane; q < e; q += 32) {
-      const int v = R.idx[q];
-      const int nv = R.new_of_old[v];                 // follower-less <=> label >= n_act
-      R.lab[q] = nv;
-      if (nv >= R.n_act) {
-        k += R.a_old[v];
-        ki += 1.0 / (double)max(R.nlead[v], 1);
-        kw += 1.0 / R.wt_old[v];
-      } else if (heavy && nv < R.H) ++h;
-      else ++c;
+    // four strided steps per iteration, their label gathers in flight together (the sums
+    // keep the one-step order: bit-identical)
+    for (int q0 = b + lane; q0 < e; q0 += 128) {
+      int v[4], nv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = q0 + 32 * j < e ? R.idx[q0 + 32 * j] : -1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) nv[j] = v[j] >= 0 ? R.new_of_old[v[j]] : 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (v[j] < 0) break;
+        R.lab[q0 + 32 * j] = nv[j];                  // follower-less <=> label >= n_act
+        if (nv[j] >= R.n_act) {
+          k += R.a_old[v[j]];
+          ki += 1.0 / (double)max(R.nlead[v[j]], 1);
+          kw += 1.0 / R.wt_old[v[j]];
+        } else if (heavy && nv[j] < R.H) ++h;
+        else ++c;
+      }
     }
     c = __reduce_add_sync(kFull, c);
     h = __reduce_add_sync(kFull, h);
@@ -1519,15 +1552,8 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   IG_CK(rp_old.alloc((size_t)(n + 1) * sizeof(int)));
   const int* rp = rp_old.as<int>();
   k_rowptr32<<<grid_for(n + 1, 256), 256, 0, s>>>(rp64, rp_old.as<int>(), n + 1);
-  k_check_edges<<<grid_for(n * 32, 256), 256, 0, s>>>(rp, idx_in, N, flags.as<int>());
-  IG_CK(cudaMemcpyAsync(&hflags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  IG_CK(cudaStreamSynchronize(s));
-  if (hflags & (F_RANGE | F_SELF | F_ORDER)) {
-    snprintf(msg, msg_len, "graph: %s", (hflags & F_RANGE) ? "follower index out of [0, n)"
-             : (hflags & F_SELF) ? "self loop (a user in its own follower list)"
-             : "row not strictly increasing (duplicate or unsorted followers)");
-    return PSI_E_GRAPH;
-  }
+  // (the edges themselves are checked edge-parallel once the transpose has expanded every
+  // edge's row, below)
 
   tr.mark("validate");
   // ---- 2.-4. transpose, normalisers, constants (old labels)
@@ -1577,6 +1603,18 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
       if (nl > 0)
         k_expand_long<<<grid_for(nl * 32, 256), 256, 0, s>>>(longl.as<int>(), (int)nl, rp,
                                                              leader_e.as<int>());
+    }
+    // input contract of the follower lists (include/psi.h): range, no self loop, strictly
+    // increasing within a row -- thread per edge, coalesced, with the expanded rows
+    k_check_edges_flat<<<grid_for(m, 256), 256, 0, s>>>(idx_in, leader_e.as<int>(), m, N,
+                                                        flags.as<int>());
+    IG_CK(cudaMemcpyAsync(&hflags, flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    IG_CK(cudaStreamSynchronize(s));
+    if (hflags & (F_RANGE | F_SELF | F_ORDER)) {
+      snprintf(msg, msg_len, "graph: %s", (hflags & F_RANGE) ? "follower index out of [0, n)"
+               : (hflags & F_SELF) ? "self loop (a user in its own follower list)"
+               : "row not strictly increasing (duplicate or unsorted followers)");
+      return PSI_E_GRAPH;
     }
     cub::DoubleBuffer<unsigned> keys((unsigned*)follower_e.p, (unsigned*)follower_s.p);
     cub::DoubleBuffer<int> vals(leader_e.as<int>(), leader_s.as<int>());
