@@ -65,6 +65,10 @@ def test_batch_config1_profiles(gpu, k):
     r = batch_run(gpu, w.row_ptr, w.followers, lam, mu, 1e-12)
     assert r["psi"].shape == (k, lam.shape[1]) and r["info"]["n_profiles"] == k
     assert r["T"] == r["Tp"].max() and r["status"] == 0
+    # the context's scalars are profile 0's (||B|| by rows / columns, rho_A: P:316)
+    sc = oracle.graph_scalars(oracle.build_operator(w.row_ptr, w.followers, lam[0], mu[0]))
+    for key in ("kappa_row", "kappa_col", "rho_A"):
+        assert abs(r["info"][key] - sc[key]) <= 1e-12 * abs(sc[key]), key
     for p in range(k):
         check_profile(w.row_ptr, w.followers, lam[p], mu[p], 1e-12, r["psi"][p], r["Tp"][p],
                       r["hist"][p])
