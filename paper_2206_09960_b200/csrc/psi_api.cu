@@ -1019,6 +1019,8 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
     B_CK(cudaGetDevice(&dev));
     B_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     c->heavy_grid = std::max(1, std::min(sms, c->g.npanels));
+    if (const char* e = getenv("PSI_HEAVY_GRID"))          // measurement: fewer SMs
+      if (atoi(e) > 0) c->heavy_grid = std::min(c->heavy_grid, atoi(e));
     c->heavy_smem = heavy_smem_bytes(c->g.nseg, c->g.heavy_seg_shift, c->g.heavy_slots,
                                      c->g.heavy_warps);
     c->heavy_block = 32 * (c->g.heavy_warps + 1);

@@ -784,6 +784,7 @@ TilesCfg sell_config(long long n, int shift) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, c.sweep, c.block, c.smem);
   if (occ < 1) occ = 1;
   c.grid = sms * occ;
+  if (env_int("PSI_SELL_GRID", 0) > 0) c.grid = std::min(c.grid, env_int("PSI_SELL_GRID", 0));
   return c;
 }
 
