@@ -26,7 +26,10 @@
  *    limits are never modified.  Like PyTorch's caching allocator, the pool keeps what the
  *    library frees for its next builds (re-mapping made repeated C5 builds 3-5x slower);
  *    psi_empty_cache() returns it to the system (the analogue of torch.cuda.empty_cache()),
- *    and environment variable PSI_POOL_KEEP_GB=<x> caps what a pool keeps to x GiB.
+ *    and environment variable PSI_POOL_KEEP_GB=<x> caps what a pool keeps to x GiB.  The
+ *    first build of a graph reserves about twice its pool working set (C5: ~50 GB) in one
+ *    block, and a per-device build scratch (cudaMalloc, C5: ~24 GB: staged inputs, sort
+ *    arrays) is kept across builds too; builds on one device serialise on that scratch.
  *  - Limits: 1 <= n <= 2^31 - 1 and m <= 2^31 - 1 (int32 indices and offsets
  *    on the device).
  */
@@ -157,8 +160,10 @@ psi_status psi_iterate(psi_ctx* ctx, double eps, int64_t max_iters, int norm,
 psi_status psi_get_psi(const psi_ctx* ctx, double* out, int mem_kind);
 
 /* psi_empty_cache -- return the device memory the library's pool on the CURRENT device holds
- * but no context uses (freed temporaries and destroyed contexts) to the system; synchronises
- * the device.  Live contexts are unaffected.  PSI_E_CUDA on a CUDA error. */
+ * but no context uses (freed temporaries and destroyed contexts), and the device's build
+ * scratch (the staged host inputs and the transpose's sort arrays of psi_build_graph, kept
+ * across builds outside the pool), to the system; synchronises the device.  Live contexts
+ * are unaffected.  PSI_E_CUDA on a CUDA error. */
 psi_status psi_empty_cache(void);
 
 /* psi_get_series -- copy s_T[n] (the paper's series iterate after the last
