@@ -900,6 +900,8 @@ psi_status build(int64_t n, int64_t m, const int64_t* row_ptr, const int32_t* fo
                              (256ull << 20);
     if (const char* e = getenv("PSI_POOL_RESERVE_GB"))        // measurement: a larger block
       est = std::max(est, (unsigned long long)(atof(e) * (double)(1ull << 30)));
+    size_t fr = 0, tot = 0;                                   // never more than half the free memory
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) est = std::min<unsigned long long>(est, fr / 2);
     pool_reserve(dev, est, c->stream);
   }
   auto bail = [&](psi_status st) { free_ctx(c); return st; };
