@@ -235,6 +235,12 @@ void free_ctx(psi_ctx* c) {
   delete c;
 }
 
+// A sliced-ELL plan with no long rows and no heavy rows needs no k_fix: k_sell's last CTA
+// finishes the sweep (eps_t, loop control).  C2: one launch per sweep instead of two.
+bool sell_fused(const psi_ctx* c) {
+  return c->g.sell && c->g.sell_nlong == 0 && c->g.n_heavy == 0 && !c->g.ovl;
+}
+
 SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
   SweepArgs A{};
   A.edges = c->g.edges;
@@ -307,6 +313,7 @@ SweepArgs make_args(psi_ctx* c, cudaGraphConditionalHandle cond) {
     P.nwords = c->g.sell_words;
     P.nlwords = c->g.sell_lwords;
     P.nlong = c->g.sell_nlong;
+    A.sell_fused = sell_fused(c) ? 1 : 0;
   }
   return A;
 }
@@ -351,6 +358,10 @@ cudaError_t add_sweep_nodes(psi_ctx* c, cudaGraph_t g, const cudaGraphNode_t* de
                       readout ? c->tc.readout : c->tc.sweep, c->grid1, c->tc.block, A, nullptr,
                       c->tc.smem)) != cudaSuccess)
     return e;
+  if (sell_fused(c)) {
+    *last = nt;
+    return cudaSuccess;
+  }
   return add_kernel(g, last, &nt, 1, fix_kernel_ptr(readout), c->grid2, kFixBlock, A, nullptr);
 }
 
@@ -433,6 +444,7 @@ cudaError_t launch_sweep(psi_ctx* c, SweepArgs* A, bool readout, cudaEvent_t mid
                   c->stream, c->tc.smem, hv && c->g.ovl && !ovl_serial())) != cudaSuccess)
     return e;
   if (after_tiles && (e = cudaEventRecord(after_tiles, c->stream)) != cudaSuccess) return e;
+  if (sell_fused(c)) return cudaSuccess;
   return launch(fix_kernel_ptr(readout), c->grid2, kFixBlock, A, nullptr, c->stream);
 }
 

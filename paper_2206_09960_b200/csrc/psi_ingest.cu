@@ -1289,8 +1289,11 @@ __global__ void k_sell_long_fill(const int* lrow, int nlong, const int* rp, cons
 }
 
 // Sliced-ELL copy of the edge stream (rows rp / flagged words edges, NA rows) for k_sell.
+// max_pad > 0: give up (rejected = true, nothing kept) when the slices' index words would
+// exceed max_pad x the edge stream's m_act words -- checked before the words are filled.
 int build_sell(IngestOut& out, const int* rp, int NA, long long n, cudaStream_t s, char* msg,
-               size_t msg_len) {
+               size_t msg_len, double max_pad, bool* rejected) {
+  *rejected = false;
   const int shift = out.sell_shift;
   const long long nblk = ((long long)NA + 31) / 32;
   const long long na_pad = nblk * 32;
@@ -1375,6 +1378,16 @@ int build_sell(IngestOut& out, const int* rp, int NA, long long n, cudaStream_t 
     IG_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, ks.as<unsigned>(), out.s_wstep, nwin + 1, s));
     IG_CK(cudaMemcpyAsync(&tot32, out.s_wstep + nwin, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
     IG_CK(cudaStreamSynchronize(s));
+  }
+  if (max_pad > 0.0 && (double)tot32 * 32.0 > max_pad * (double)out.m_act) {
+    for (void** p : {(void**)&out.s_ipos, (void**)&out.s_off, (void**)&out.s_wrow, (void**)&out.s_wstep}) {
+      IG_CK(cudaFreeAsync(*p, s));
+      *p = nullptr;
+    }
+    out.sell_nwin = 0;
+    out.sell_nslices = 0;
+    *rejected = true;
+    return PSI_OK;
   }
   // long rows
   Tmp lrow_all;
@@ -1885,13 +1898,16 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
 
   tr.mark("relabel");
   // The sweep's layout: the sliced-ELL copy of the edge stream (k_sell) for single-profile
-  // graphs with heavy rows (C4/C5: measured faster than the tiles), the
-  // edge-balanced tiles (k_tiles, and k_solve for small graphs) otherwise; PSI_SELL=0/1 forces
+  // graphs with heavy rows (C4/C5: measured faster than the tiles) and for
+  // graphs without them whose slices pad little (C2), the edge-balanced tiles (k_tiles, and
+  // k_solve for small graphs) otherwise; PSI_SELL=0/1 forces
   // the tiles / the sliced-ELL layout (not with the overlapped plan or a batch).
   {
     const int se = env_int("PSI_SELL", -1);
-    out.sell = (out.n_act > 0 && nprof == 1 && !out.ovl && (se == 1 || (se < 0 && out.n_heavy > 0)))
-                   ? 1 : 0;
+    const bool can = out.n_act > 0 && nprof == 1 && !out.ovl;
+    // 2 = decided at step 8 from the layout's padding (graphs without heavy rows: C2's
+    // near-uniform rows pad little and k_sell wins, C3's power-law rows pad 2.4x and lose)
+    out.sell = can && (se == 1 || (se < 0 && out.n_heavy > 0)) ? 1 : (can && se < 0 ? 2 : 0);
   }
   // ---- 6. relabelled edge stream over active rows, folded constants
   const int NA = (int)out.n_act;
@@ -1990,7 +2006,7 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     }
     // rows keep their followers in input order: the sweep's sums have a fixed order either
     // way, and a per-row sort bought nothing measurable
-    if (m_act > 0 && !out.sell) {          // (the sliced-ELL copy needs no flags)
+    if (m_act > 0 && out.sell != 1) {      // (the sliced-ELL copy needs no flags)
       k_flag_rows<<<grid_for(NA, 256), 256, 0, s>>>(rp_new.as<int>(), NA, m_act, m_pad, N,
                                                     out.edges);
     }
@@ -2030,11 +2046,14 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   }
 
   tr.mark("vectors");
+  // small graphs (at most kCoopEdges edge slots) keep the tiles: the persistent cooperative
+  // solver runs the whole loop in one launch there (psi_api.cu use_coop)
+  if (out.sell == 2 && (long long)out.ntiles * out.tile <= kCoopEdges) out.sell = 0;
   // ---- 7. edge tiles: first row of every tile, rows spanning tiles (and, for a batch
   // context, the same for the batch sweep's 512-edge tiles)
   {
     int rc4 = PSI_OK;
-    if (!out.sell) {
+    if (out.sell != 1) {
       rc4 = make_tiling(rp_new.as<int>(), NA, (long long)out.ntiles * out.tile, out.tile, s,
                         &out.tile_row, &out.split, &out.nsplit, &out.nsplit_long, msg, msg_len);
       if (rc4 != PSI_OK) return rc4;
@@ -2061,14 +2080,31 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   // no longer needed
   {
     if (out.sell) {
-      out.sell_shift = std::min(std::max(env_int("PSI_SELL_SHIFT", kSellShift), 5), 10);
+      // windows of 2^shift rows: 256 (C4/C5), fewer on graphs with few active rows so that
+      // every warp of the grid gets >= 3 windows (C2: 64-row windows, 0.086 -> 0.080 ms;
+      // 256-row windows leave a fifth of the warps without one)
+      int shift = kSellShift;
+      if (out.n_heavy == 0) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        while (shift > 5 && ((long long)NA >> shift) < 3LL * sms * kSellWarps) --shift;
+      }
+      out.sell_shift = std::min(std::max(env_int("PSI_SELL_SHIFT", shift), 5), 10);
       out.sell_kcap = std::max(env_int("PSI_SELL_KCAP", kSellKcap), 1);
       out.sell_lmax = std::min(std::max(env_int("PSI_SELL_LMAX", kSellLmax), 1), 2047);
       out.sell_piece = std::max(env_int("PSI_SELL_PIECE", kSellPiece), 32);
-      int rc5 = build_sell(out, rp_new.as<int>(), NA, n, s, msg, msg_len);
+      bool rejected = false;
+      int rc5 = build_sell(out, rp_new.as<int>(), NA, n, s, msg, msg_len,
+                           out.sell == 2 ? kSellMaxPad : 0.0, &rejected);
       if (rc5 != PSI_OK) return rc5;
-      IG_CK(cudaFreeAsync(out.edges, s));
-      out.edges = nullptr;
+      if (rejected) {
+        out.sell = 0;                                // the tiles built at step 7 stay
+      } else {
+        out.sell = 1;
+        IG_CK(cudaFreeAsync(out.edges, s));
+        out.edges = nullptr;
+      }
       tr.mark("sliced-ELL");
     }
   }

@@ -73,11 +73,14 @@ constexpr int kDefaultHeavyPPS = 1;      // heavy panels per SM (entry budget pe
 constexpr int kDefaultGroups = 8;        // tile groups (of kBlock threads) per sweep CTA
 constexpr long long kCoopEdges = 1LL << 23;  // k_solve up to this many edge slots (PSI_COOP_TILES: tiles)
 constexpr int kDefaultSmemHot = 4096;    // labels of x_{t-1} cached in shared memory per CTA
+constexpr int kSmemHotLarge512 = 12288;  // 512-edge tiles on graphs with >= 2^22 users (C3)
 constexpr int kDefaultL1Hot = 16384;     // labels below this gather through L1 (evict_last)
 // sliced-ELL sweep (k_sell, SellPlan)
 constexpr int kSellWarps = 32;           // warps per k_sell CTA (one CTA per SM)
 constexpr int kSellShift = 8;            // rows per window <= 256 (sort scope and smem sums)
 constexpr int kSellKcap = 256;           // window cut after ~256 x 32 stream edges
+constexpr double kSellMaxPad = 1.6;       // graphs without heavy rows: k_sell if its index words
+                                         // are <= 1.6 x the stream's (C2 1.45: k_sell; C3 2.4: tiles)
 constexpr int kSellLmax = 1024;          // longer stream rows are summed in pieces by warps
 constexpr int kSellPiece = 4096;         // followers per piece of a long row
 
@@ -205,6 +208,9 @@ struct SweepArgs {
   // sliced-ELL sweep (k_sell) instead of the edge-balanced tiles (k_tiles)
   int use_sell;
   SellPlan sell;
+  // 1: no long rows and no heavy rows -- k_sell's last CTA reduces eps_t and runs the loop
+  // control itself, and no k_fix is launched (psi_sweep.cu sell_finish)
+  int sell_fused;
 };
 
 // ---- launchers (psi_sweep.cu)

@@ -148,8 +148,7 @@ struct TileSmem {
 
 // G tile groups of kBlock threads per CTA (named barriers 1..G); the CTA's shared hot
 // cache holds x_{t-1}[0, hot_smem): the most-gathered labels, read from
-// shared memory instead of L2.  Gathers of labels in [hot_smem, l1_lim) allocate in L1
-// (evict_last); all others bypass L1, so streaming cold gathers cannot evict them.
+// shared memory instead of L2; all other gathers bypass L1.
 // x loads of the sweep: the read-only path (L1, .nc) in a sweep kernel; in the persistent
 // small-graph solver (COH) x was written earlier in the same kernel, so L2-coherent loads.
 template <bool COH>
@@ -171,8 +170,6 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
   const unsigned long long pf = pol_evict_first(), pl = pol_evict_last();
   const unsigned hot_lim = (unsigned)A.hot_lim;
   const unsigned hs = (unsigned)A.hot_smem;
-  const unsigned l1_lim = (unsigned)A.l1_lim;
-  const unsigned single_lo = (unsigned)A.single_lo;
   const int ntiles = A.ntiles;
   const bool st_last = A.st_last;
   const double* __restrict__ acon = (t == 0 && A.a_first) ? A.a_first : A.a;
@@ -206,17 +203,12 @@ __device__ __forceinline__ void tiles_body(const SweepArgs& A, unsigned char* ds
 #endif
       PSI_ASSERT((int)lab <= A.n_lab);                  // sentinel label n holds x = 0
       fl |= (w[q] >> 31) << q;
-#if defined(PSI_EXP_ONELOAD)                // experiment builds: one global load variant,
-      if (lab < hs) v[q] = hot[lab];          // the L2 policy chosen per lane
-      else v[q] = COH ? __ldcg(xs + lab)
-                      : (PSI_EXP_ONELOAD == 1 ? ld_hint_na(xs + lab, lab < hot_lim ? pl : pf)
-                                              : ld_hint(xs + lab, lab < hot_lim ? pl : pf));
-#else
+      // one global load variant (L1 bypass, the L2 policy chosen per lane): the L1 classes of
+      // k_sell's gx (evict_last hot band, evict_first single-leader users) cost three load
+      // instructions per gather here -- C2 0.087 -> 0.083, C3 0.377 -> 0.358 ms without them;
+      // only graphs without heavy rows (C5 with the tiles forced: 1 % slower) run this kernel
       if (lab < hs) v[q] = hot[lab];
-      else if (lab < l1_lim) v[q] = ldx<COH>(xs + lab, pl, 0);
-      else if (lab >= single_lo) v[q] = ldx<COH>(xs + lab, pf, 1);
       else v[q] = ldx<COH>(xs + lab, lab < hot_lim ? pl : pf, 2);
-#endif
     }
     if (tid == 0)
       sm.next_flag = (k + 1 >= ntiles) ? 1 : (int)(ld_stream(A.edges + (size_t)(k + 1) * (TB * kEpt), pf) >> 31);
@@ -325,6 +317,68 @@ __global__ void __launch_bounds__(TB * G, (1024 / (TB * G)) > 0 ? 1024 / (TB * G
   // overlapped sweep: launched programmatically beside k_heavy (psi_api.cu); complete only
   // after it, so whatever follows k_tiles in stream order also follows k_heavy
   if (A.ovl) asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Alg. 2's loop control after the fixed-order reduction of eps_t (one thread): the history,
+// gap = ||B|| eps_t (line 325), t + 1, and the graph's WHILE condition (gap > eps && t < max_iters,
+// Eq. (16) / line 320) -- no host round trip.
+__device__ __forceinline__ void loop_control(const SweepArgs& A, long long t, double eps_sum) {
+  const LoopParams P = *A.prm;
+  const double eps_t = eps_sum + (t == 0 ? P.eps1_extra : 0.0);
+  if (t < P.hist_cap) P.history[t] = eps_t;
+  const double gap = P.kappa * eps_t;
+  const bool bad = !isfinite(eps_t);
+  A.st->eps_t = eps_t;
+  A.st->gap = gap;
+  A.st->iter = t + 1;
+  A.st->done = 0;
+  if (bad) A.st->status |= 1;
+  const unsigned cont = (!bad && gap > P.eps && t + 1 < P.max_iters) ? 1u : 0u;
+  if (A.use_cond) cudaGraphSetConditional(A.cond, cont);
+}
+
+// k_sell on a plan with no long rows and no heavy rows (SweepArgs::sell_fused) finishes the
+// sweep itself: the last CTA to arrive (atomic ticket) reduces the windows' eps_t partials in a
+// fixed order (strided per thread, then a fixed shuffle tree) and runs the loop control, so the
+// sweep is ONE launch (no k_fix: C2 -10 us per sweep).  It also resets the work counter.
+template <bool READOUT>
+__device__ __forceinline__ void sell_finish(const SweepArgs& A, long long t) {
+  __shared__ double red[32];
+  __shared__ int last;
+  __threadfence();                     // this CTA's epsw / x_t / psi stores, before the ticket
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&A.st->done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) A.st->sell_next = 0;      // every CTA has made its last claim
+  if (READOUT) {
+    if (threadIdx.x == 0) A.st->done = 0;
+    return;
+  }
+  // 16 independent loads in flight per thread (one L2 round trip for up to 16K windows at
+  // 1024 threads; a dependent strided loop took ~8 us at C2's 15.6K windows)
+  double v = 0.0;
+  const int nw = A.sell.nwin, step = (int)blockDim.x;
+  for (int b = 0; b < nw; b += 16 * step) {
+    double q[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int i = b + k * step + (int)threadIdx.x;
+      q[k] = i < nw ? __ldcg(A.sell.epsw + i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v += q[k];
+  }
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double r = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+    r = warp_sum(r);
+    if (lane == 0) loop_control(A, t, r);
+  }
 }
 
 // ---------------------------------------------------------------- sliced-ELL sweep (k_sell)
@@ -483,6 +537,7 @@ __global__ void __launch_bounds__(kSellWarps * 32, 1) k_sell(SweepArgs A) {
     }
     it = __shfl_sync(kFull, nxt, 0);
   }
+  if (A.sell_fused) sell_finish<READOUT>(A, t);
 }
 
 // Split rows, eps_t and the stop rule (k_fix), as a device function of any block size >= 32
@@ -575,20 +630,7 @@ __device__ __forceinline__ void fix_body(const SweepArgs& A, long long t, double
   v = 0.0;
   for (int q = tid; q < (int)gridDim.x; q += NT) v += __ldcg(A.eps_part2 + q);
   const double e2 = block_sum<NT>(v, red);
-  if (tid == 0) {
-    const LoopParams P = *A.prm;
-    const double eps_t = e1 + e2 + (t == 0 ? P.eps1_extra : 0.0);
-    if (t < P.hist_cap) P.history[t] = eps_t;
-    const double gap = P.kappa * eps_t;
-    const bool bad = !isfinite(eps_t);
-    A.st->eps_t = eps_t;
-    A.st->gap = gap;
-    A.st->iter = t + 1;
-    A.st->done = 0;
-    if (bad) A.st->status |= 1;
-    const unsigned cont = (!bad && gap > P.eps && t + 1 < P.max_iters) ? 1u : 0u;
-    if (A.use_cond) cudaGraphSetConditional(A.cond, cont);
-  }
+  if (tid == 0) loop_control(A, t, e1 + e2);
 }
 
 template <bool READOUT>
@@ -738,8 +780,14 @@ TilesCfg tiles_config(int ntiles, long long n, int tile, bool ovl) {
   const int hot = env_int("PSI_SMEM_HOT", kDefaultSmemHot);
   const int l1 = env_int("PSI_L1_HOT", kDefaultL1Hot);
   if (tile == 512) {
-    // 15 groups of 64 threads (barrier ids 1..15): one CTA and one hot cache per SM
-    return cfg_for<15, 64>(ntiles, n, hot, l1);
+    // 15 groups of 64 threads (barrier ids 1..15): one CTA and one hot cache per SM.  Large
+    // graphs without heavy rows take a 12288-label hot cache: with every other gather
+    // bypassing L1, the shared-memory copy is where the hubs' gathers are served on chip
+    // (C3: 0.359 -> 0.343 ms; 8192: 0.347, 16384: 0.355, 20480: 0.601 -- L1 too small for
+    // the stream; profiles/r2/tune_c3_smemhot_s4e.txt).  Small graphs keep 4096: the copy is
+    // re-read every sweep, by k_solve too.
+    const int hot512 = env_int("PSI_SMEM_HOT", n >= (1LL << 22) ? kSmemHotLarge512 : kDefaultSmemHot);
+    return cfg_for<15, 64>(ntiles, n, hot512, l1);
   }
   const int G = env_int("PSI_GROUPS", kDefaultGroups);
   switch (G) {

@@ -204,6 +204,9 @@ def test_config1_vs_exact(gpu):
 def test_config2_parity_and_pagerank(gpu):
     w = psigen.make_config(2)
     ref, got = parity(gpu, w)
+    # near-uniform ER rows: the sliced-ELL layout pads little, so the library picks it, and
+    # with no long rows k_sell finishes each sweep itself (no k_fix launch)
+    assert got["info"]["sliced_ell"] == 1 and got["info"]["sell_long_rows"] == 0
     pi, _, _ = oracle.pagerank_power(w.row_ptr, w.followers, 0.5, eps=1e-14)
     assert oracle.max_rel_error(pi, got["psi"]) < 1e-9     # psi = PageRank(0.5)
 
@@ -214,6 +217,7 @@ def test_config3_parity(gpu):
     w = psigen.make_config(3)
     ref, got = parity(gpu, w, full=True)
     assert got["info"]["n_leaderless"] > 0
+    assert got["info"]["sliced_ell"] == 0        # power-law rows pad the slices 2.4x: tiles
 
 
 def test_kappa_col_counterexample_through_cabi(gpu, driver):

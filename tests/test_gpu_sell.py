@@ -157,3 +157,28 @@ def test_sell_config3_parity(gpu, monkeypatch):
     w = psigen.make_config(3)
     ref, got = parity(gpu, w, full=True)
     assert got["info"]["sliced_ell"] == 1
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_sell_fused_finish(gpu, seed, monkeypatch):
+    """No long rows and no heavy rows: k_sell's last CTA reduces eps_t and runs the stop rule
+    itself (no k_fix launch).  Fixed-count parity, the eps_t history, the eps-mode stop (T
+    within one sweep) and the readout, through the graph loop and the direct launches."""
+    rng, rp, f, lam, mu = random_graph(100 + seed)
+    sell_env(monkeypatch, shift=5 + seed % 4, lmax=2047, kcap=(1, 4, 1000)[seed % 3])
+    if seed % 2:
+        monkeypatch.setenv("PSI_GRAPH", "0")
+    norm = ("row", "col", "one")[seed % 3]
+    T = int(rng.integers(0, 40))
+    ref = oracle.power_psi(rp, f, lam, mu, eps=0.0, max_iters=T, norm=norm)
+    got = gpu_run(gpu, rp, f, lam, mu, 0.0, T, norm)
+    assert got["info"]["sliced_ell"] == 1 and got["info"]["sell_long_rows"] == 0
+    assert got["info"]["n_heavy"] == 0
+    assert got["T"] == ref.iterations
+    assert oracle.max_rel_error(ref.psi, got["psi"]) <= 1e-12
+    np.testing.assert_allclose(got["hist"], ref.history, rtol=1e-6,
+                               atol=1e-13 * max(1.0, np.abs(ref.s).sum()))
+    ref2 = oracle.power_psi(rp, f, lam, mu, eps=1e-10, norm=norm)
+    got2 = gpu_run(gpu, rp, f, lam, mu, 1e-10, 10_000, norm)
+    assert abs(got2["T"] - ref2.iterations) <= 1
+    assert oracle.max_rel_error(ref2.psi, got2["psi"]) <= 1e-9
