@@ -616,8 +616,10 @@ __global__ void k_heavy_fill(const unsigned long long* keys, long long nk, const
 // position taking the run's remaining entry whose bank pair that instruction has used least
 // in the block.  Measured: 5.5 -> 4.6 wavefronts per gather instruction at C5 (ideal 2);
 // reordering whole runs as well gained nothing in a model of this greedy.
-// A run keeps its order where it crosses a block boundary (so every block is independent:
-// one lane per block, a warp per list) and when it is longer than 32.  Deterministic.
+// Every block permutes only inside the portions of runs that lie in it (so every block is
+// independent: one lane per block, a warp per list), whatever the run's length: portions of
+// up to 32 entries by a scan of the remaining entries, longer ones (hub rows, whose sorted
+// labels would otherwise stay in order) through 16 bank-pair buckets.  Deterministic.
 constexpr int kBalBlock = 128;
 // blocks of 128 positions of every list (the balance kernel's work items)
 __global__ void k_list_blocks(const long long* lstart, long long nlists, long long* nb) {
@@ -653,26 +655,23 @@ __global__ void __launch_bounds__(kBalBlock) k_heavy_balance(const unsigned* in,
       const unsigned bk = w & 15;
       if (((c >> (4 * bk)) & 15ull) < 15ull) cnt[q & 7][t] = c + (1ull << (4 * bk));
     };
+    // every maximal same-slot portion [q, r) of the block is permuted inside itself (the set of
+    // entries at the block's positions does not change, so blocks stay independent -- also for
+    // runs that cross block boundaries or span several blocks)
     int q = q0;
-    if (q0 > 0) {                                     // the tail of a run from the last block
-      const unsigned sl = src[q0 - 1] >> sh;
-      while (q < q1 && (src[q] >> sh) == sl) { dst[q] = src[q]; count(q, src[q]); ++q; }
-    }
-    while (q < q1) {                                  // runs starting in this block
+    while (q < q1) {
       const unsigned sl = src[q] >> sh;
       int r = q + 1;
-      while (r < len_l && (src[r] >> sh) == sl) ++r;
-      const int in_blk = min(r, q1) - q;              // entries placed inside the block
-      if (r - q > 32) {
-        for (int i = 0; i < in_blk; ++i) { dst[q + i] = src[q + i]; count(q + i, src[q + i]); }
-      } else {
+      while (r < q1 && (src[r] >> sh) == sl) ++r;
+      const int n = r - q;
+      if (n <= 32) {
         unsigned w[32];
-        for (int j = 0; j < in_blk; ++j) w[j] = src[q + j];
+        for (int j = 0; j < n; ++j) w[j] = src[q + j];
         unsigned used = 0;
-        for (int i = 0; i < in_blk; ++i) {
+        for (int i = 0; i < n; ++i) {
           const unsigned long long c = cnt[(q + i) & 7][t];
           int bj = 0, bv = 1 << 30;
-          for (int j = 0; j < in_blk; ++j) {
+          for (int j = 0; j < n; ++j) {
             if ((used >> j) & 1u) continue;
             const int v = (int)((c >> (4 * (w[j] & 15))) & 15ull);
             if (v < bv) { bv = v; bj = j; }
@@ -681,8 +680,38 @@ __global__ void __launch_bounds__(kBalBlock) k_heavy_balance(const unsigned* in,
           dst[q + i] = w[bj];
           count(q + i, w[bj]);
         }
+      } else {
+        // long portion (a hub's virtual row): its entries bucketed by bank pair, every position
+        // taking an entry of the pair its instruction has used least in the block (ties: the
+        // fullest bucket).  Sorted labels of a dense run otherwise put whole half-warps on two
+        // or three pairs (a model: 3.1 -> 2.0 wavefronts per half-warp instruction).
+        unsigned w[kBalBlock];
+        unsigned char head[16], end[16];
+        {
+          unsigned char c16[16];
+          for (int b16 = 0; b16 < 16; ++b16) c16[b16] = 0;
+          for (int j = 0; j < n; ++j) ++c16[src[q + j] & 15];
+          int a = 0;
+          for (int b16 = 0; b16 < 16; ++b16) { head[b16] = (unsigned char)a; a += c16[b16]; end[b16] = (unsigned char)a; }
+          unsigned char fill[16];
+          for (int b16 = 0; b16 < 16; ++b16) fill[b16] = head[b16];
+          for (int j = 0; j < n; ++j) { const unsigned e = src[q + j]; w[fill[e & 15]++] = e; }
+        }
+        for (int i = 0; i < n; ++i) {
+          const unsigned long long c = cnt[(q + i) & 7][t];
+          int bb = 0, bv = 1 << 30;
+          for (int b16 = 0; b16 < 16; ++b16) {
+            const int left = end[b16] - head[b16];
+            if (left == 0) continue;
+            const int v = ((int)((c >> (4 * b16)) & 15ull) << 8) - left;
+            if (v < bv) { bv = v; bb = b16; }
+          }
+          const unsigned e = w[head[bb]++];
+          dst[q + i] = e;
+          count(q + i, e);
+        }
       }
-      q = min(r, q1);                                 // the rest belongs to the next block
+      q = r;
     }
   }
 }
