@@ -1766,6 +1766,12 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     out.heavy_seg_shift = kOvlSegShift;
     out.heavy_slots = kOvlSlots;
     out.heavy_warps = kOvlWarps;
+  } else {
+    // measurement knobs: the plan shape (segment size / slots per panel trade the TMA fills of
+    // a panel against runs per row); (slots + 1) << seg_shift must fit kEntBits
+    out.heavy_seg_shift = std::min(std::max(env_int("PSI_HEAVY_SEG_SHIFT", out.heavy_seg_shift), 10), 13);
+    out.heavy_slots = std::min(std::max(env_int("PSI_HEAVY_SLOTS", out.heavy_slots), 1024),
+                               (1 << (kEntBits - out.heavy_seg_shift)) - 1024);
   }
   const int kSegR = 1 << out.heavy_seg_shift;   // labels per staged segment
   long long h_default = kMinHeavyLabels;
