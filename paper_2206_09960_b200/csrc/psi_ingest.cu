@@ -945,8 +945,11 @@ namespace {
 // fault per 4 KB on every build, ~40 ms at C5, measured) and are guarded by a mutex.
 struct HeavyHostPlan {
   std::mutex mu;
-  std::vector<long long> hc;
-  std::vector<int> prow, row_panel, pslot_base, wslot;
+  std::vector<long long> hc, cum_h;
+  std::vector<int> prow, row_panel, pslot_base, wslot, cum_nv;
+  int sel_num = 100, sel_cap = 0;              // panel shape chosen by the search
+  int sel_tail = 0, sel_from = 0;              //   tail target (% of the chosen one) from sel_from % of the entries
+  long long sim_base = 0, sim_best = 0;        //   and the simulated makespans (entries)
   std::vector<int2> rslot;
   std::vector<unsigned char> slot_warp;
   int npanels = 0;
@@ -956,9 +959,130 @@ HeavyHostPlan& heavy_host_plan() {
   return p;
 }
 
-void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOTS, int sms, int pps) {
+// Panel shape search (search != 0): k_heavy's CTAs claim the panels in index order, so the sweep
+// lasts as long as the busiest CTA -- with ~1 full-size panel per SM a handful of panels over
+// the SM count is a second wave (C4: 162 panels on 148 SMs, k_heavy 0.445 ms for 0.25 ms of
+// mean work).  The entry target and the slot cap of a panel are chosen from a few candidates by
+// simulating that claim order with cost(panel) = entries + nseg * kPanelSegCost (the streamed
+// segments of a panel cost about as much as 3000 entries each: C5, 366 vs 461 panels).  The
+// default shape stays unless a candidate's makespan is >= 4 % shorter (the model's error).
+constexpr long long kPanelSegCost = 3000;
+long long heavy_makespan(const std::vector<long long>& cum_h, const std::vector<int>& cum_nv, int NH,
+                         long long e_panel, int slot_cap, int sms, long long fixed,
+                         std::vector<long long>& busy, long long e_tail = 0, long long tail_from = 0,
+                         int* npan = nullptr) {
+  busy.assign(sms, 0);                    // a binary min-heap of the CTAs' finish times
+  long long makespan = 0;
+  int start = 0, np = 0;
+  while (start < NH) {
+    // the panel takes rows [start, end): the first row always, then while both caps hold
+    const long long h_lim = cum_h[start] + (e_tail > 0 && cum_h[start] >= tail_from ? e_tail : e_panel);
+    const long long v_lim = (long long)cum_nv[start] + slot_cap;
+    // largest end with cum_h[end] <= h_lim and cum_nv[end] <= v_lim: gallop, then bisect (local)
+    int lo = start + 1, hi = NH;
+    for (int step = 1; lo + step < NH; step <<= 1) {
+      if (cum_h[lo + step] <= h_lim && cum_nv[lo + step] <= v_lim) {
+        lo += step;
+      } else {
+        hi = lo + step - 1;
+        break;
+      }
+    }
+    while (lo < hi) {
+      const int mid = lo + ((hi - lo + 1) >> 1);
+      if (cum_h[mid] <= h_lim && cum_nv[mid] <= v_lim) lo = mid; else hi = mid - 1;
+    }
+    const int end = lo;
+    const long long cost = cum_h[end] - cum_h[start] + fixed;
+    // earliest-free CTA takes it: replace the heap's root and sift down
+    long long t = busy[0] + cost;
+    makespan = std::max(makespan, t);
+    int i = 0;
+    for (;;) {
+      int c = 2 * i + 1;
+      if (c >= sms) break;
+      if (c + 1 < sms && busy[c + 1] < busy[c]) ++c;
+      if (busy[c] >= t) break;
+      busy[i] = busy[c];
+      i = c;
+    }
+    busy[i] = t;
+    start = end;
+    ++np;
+  }
+  if (npan) *npan = np;
+  return makespan;
+}
+
+void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOTS, int sms, int pps,
+                     int nseg, int search) {
   const std::vector<long long>& hc = P.hc;
-  const long long e_panel = std::max<long long>((n_ent + (long long)pps * sms - 1) / ((long long)pps * sms), 32768);
+  long long e_panel = std::max<long long>((n_ent + (long long)pps * sms - 1) / ((long long)pps * sms), 32768);
+  int slot_cap = SLOTS;
+  long long e_tail = 0, tail_from = 0;          // tapered tail (search): target of the late panels
+  if (search && NH > 0) {
+    const long long vmax0 = std::max<long long>(e_panel / (2 * HW), 64);
+    std::vector<long long>& cum_h = P.cum_h;
+    std::vector<int>& cum_nv = P.cum_nv;
+    cum_h.resize((size_t)NH + 1);
+    cum_nv.resize((size_t)NH + 1);
+    cum_h[0] = 0;
+    cum_nv[0] = 0;
+    for (int r = 0; r < NH; ++r) {
+      const long long h = hc[r];
+      cum_h[r + 1] = cum_h[r] + h;
+      cum_nv[r + 1] = cum_nv[r] + (int)std::min<long long>(h > 0 ? (h + vmax0 - 1) / vmax0 : 0, SLOTS);
+    }
+    const long long fixed = (long long)nseg * kPanelSegCost;
+    std::vector<long long> busy;
+    int base_panels = 0;
+    const long long base = heavy_makespan(cum_h, cum_nv, NH, e_panel, SLOTS, sms, fixed, busy, 0, 0, &base_panels);
+    long long best = base;
+    P.sel_num = 100;
+    P.sel_cap = SLOTS;
+    // nothing to gain where the default is already within 8 % of an even split of its work
+    // (C5: 6 %); the candidates run on the helper thread beside the edge-stream build
+    const bool worth = base * 100 > (n_ent + fixed * base_panels) / sms * 108;
+    static const int kCapEighths[] = {8, 6, 5, 4, 3};
+    for (int num = worth ? 150 : 0; num >= 50; num -= 5)       // entry target, % of the default
+      for (int d : kCapEighths) {                             // slot cap = SLOTS * d / 8
+        const long long e = std::max<long long>(e_panel * num / 100, 32768);
+        const int cap = SLOTS * d / 8;
+        const long long m = heavy_makespan(cum_h, cum_nv, NH, e, cap, sms, fixed, busy);
+        if (m < best && m * 100 <= base * 96) {
+          best = m;
+          P.sel_num = num;
+          P.sel_cap = cap;
+        }
+      }
+    // a tapered tail: the panels that start after tail_from entries take a smaller target (the
+    // last panels claimed decide how uneven the CTAs finish)
+    const long long e_sel = std::max<long long>(e_panel * P.sel_num / 100, 32768);
+    const int cap_sel = P.sel_cap;
+    P.sel_tail = 0;
+    P.sel_from = 0;
+    for (int from = worth ? 50 : 100; from <= 90; from += 10)   // % of the entries before the tail
+      for (int tnum = 70; tnum >= 20; tnum -= 10) {           // tail target, % of the chosen one
+        const long long et = std::max<long long>(e_sel * tnum / 100, 32768);
+        const long long tf = n_ent / 100 * from;
+        const long long m = heavy_makespan(cum_h, cum_nv, NH, e_sel, cap_sel, sms, fixed, busy, et, tf);
+        if (m < best && m * 100 <= base * 96) {
+          best = m;
+          P.sel_tail = tnum;
+          P.sel_from = from;
+        }
+      }
+    P.sim_base = base;
+    P.sim_best = best;
+    if (best < base) {
+      e_panel = e_sel;
+      slot_cap = cap_sel;
+      if (P.sel_tail > 0) {
+        e_tail = std::max<long long>(e_sel * P.sel_tail / 100, 32768);
+        tail_from = n_ent / 100 * P.sel_from;
+      }
+    }
+  }
   const long long vmax = std::max<long long>(e_panel / (2 * HW), 64);
   std::vector<int>& prow = P.prow;
   std::vector<int>& row_panel = P.row_panel;
@@ -976,7 +1100,7 @@ void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOT
   std::vector<long long> slot_w(SLOTS);          // entries of each slot of the open panel
   std::vector<int> ws(HW + 1);
   int nslots = 0;
-  long long p_ent = 0;
+  long long p_ent = 0, tot_ent = 0;            // entries of the open panel / of all rows so far
   auto close_panel = [&](int r_end) {
     long long T = 0;
     for (int k = 0; k < nslots; ++k) T += slot_w[k];
@@ -999,7 +1123,8 @@ void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOT
     const long long h = hc[r];
     long long nv = h > 0 ? (h + vmax - 1) / vmax : 0;
     if (nv > SLOTS) nv = SLOTS;
-    if (r > prow.back() && (nslots + nv > SLOTS || p_ent + h > e_panel)) close_panel(r);
+    const long long e_cur = e_tail > 0 && tot_ent - p_ent >= tail_from ? e_tail : e_panel;
+    if (r > prow.back() && (nslots + nv > slot_cap || p_ent + h > e_cur)) close_panel(r);
     rslot[r] = make_int2(nslots, (int)nv);
     row_panel[r] = (int)prow.size() - 1;
     if (nv > 0) {
@@ -1007,6 +1132,7 @@ void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOT
       for (long long k = 0; k < nv; ++k) slot_w[nslots++] = q + (k < rem ? 1 : 0);
     }
     p_ent += h;
+    tot_ent += h;
   }
   close_panel(NH);
   P.npanels = (int)prow.size() - 1;
@@ -1999,8 +2125,10 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int pps = std::max(1, env_int("PSI_HEAVY_PPS", kDefaultHeavyPPS));
+    // the search runs with the default panels-per-SM only (PSI_HEAVY_PPS is a measurement knob)
+    const int search = env_int("PSI_HEAVY_SEARCH", 1) != 0 && env_int("PSI_HEAVY_PPS", -1) < 0 ? 1 : 0;
     hp_thread = std::thread(plan_heavy_host, std::ref(HP), NH, n_hot_ent, out.heavy_warps,
-                            out.heavy_slots, sms, pps);
+                            out.heavy_slots, sms, pps, out.nseg, search);
   }
   // joined on every exit path below (an early error return must not leave it running)
   struct Joiner {
@@ -2052,6 +2180,10 @@ int ingest(long long n, long long m, const long long* rp64, const int* idx_in,
   if (NH > 0) {
     hp_thread.join();
     tr.mark("  heavy: host plan joined");
+    if (tr.on)
+      fprintf(stderr, "[psi ingest]   heavy: panel shape %d %% of the entry target, slot cap %d: %d panels, "
+              "tail %d %% from %d %% of the entries; simulated makespan %lld -> %lld entries\n", HP.sel_num,
+              HP.sel_cap, HP.npanels, HP.sel_tail, HP.sel_from, HP.sim_base, HP.sim_best);
     int rc2 = build_heavy_plan(out, NH, n_hot_ent, hot, hoff, HP, s, tr, msg, msg_len);
     hp_lock.unlock();
     if (rc2 != PSI_OK) return rc2;
