@@ -291,6 +291,9 @@ def test_repeated_iterate_on_one_context(gpu):
     {"PSI_HEAVY": "1", "PSI_OVERLAP": "1"},                 # k_heavy || k_tiles (overlapped plan)
     {"PSI_HEAVY": "1", "PSI_OVERLAP": "1", "PSI_HEAVY_MIN": "2", "PSI_HEAVY_LABELS": "24576"},
     {"PSI_HEAVY": "1", "PSI_OVERLAP": "0"},                 # serial plan
+    {"PSI_HEAVY": "1", "PSI_HEAVY_SEARCH": "0"},            # fixed panel shape (no claim-order search)
+    {"PSI_HEAVY": "1", "PSI_HEAVY_MIN": "2", "PSI_HEAVY_LABELS": "24576", "PSI_HEAVY_SLOTS": "2048"},  # many small panels
+    {"PSI_HEAVY": "1", "PSI_HEAVY_SEG_SHIFT": "12", "PSI_HEAVY_SLOTS": "16384"},   # 32 KB segments, 16384 slots
 ])
 def test_heavy_rows_parity(gpu, env, monkeypatch):
     """psi_build_graph reads the heavy-row knobs; every split of the work between k_heavy
