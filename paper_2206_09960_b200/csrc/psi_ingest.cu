@@ -945,7 +945,7 @@ namespace {
 // fault per 4 KB on every build, ~40 ms at C5, measured) and are guarded by a mutex.
 struct HeavyHostPlan {
   std::mutex mu;
-  std::vector<long long> hc, cum_h;
+  std::vector<long long> hc, cum_h, pent;       // pent: entries of every panel of the plan
   std::vector<int> prow, row_panel, pslot_base, wslot, cum_nv;
   int sel_num = 100, sel_cap = 0;              // panel shape chosen by the search
   int sel_tail = 0, sel_from = 0;              //   tail target (% of the chosen one) from sel_from % of the entries
@@ -965,7 +965,8 @@ HeavyHostPlan& heavy_host_plan() {
 // mean work).  The entry target and the slot cap of a panel are chosen from a few candidates by
 // simulating that claim order with cost(panel) = entries + nseg * kPanelSegCost (the streamed
 // segments of a panel cost about as much as 3000 entries each: C5, 366 vs 461 panels).  The
-// default shape stays unless a candidate's makespan is >= 4 % shorter (the model's error).
+// default shape is planned first and stays unless a candidate's makespan is >= 4 % shorter
+// (the model's error); only then the plan is made a second time.
 constexpr long long kPanelSegCost = 3000;
 long long heavy_makespan(const std::vector<long long>& cum_h, const std::vector<int>& cum_nv, int NH,
                          long long e_panel, int slot_cap, int sms, long long fixed,
@@ -1014,75 +1015,32 @@ long long heavy_makespan(const std::vector<long long>& cum_h, const std::vector<
   return makespan;
 }
 
-void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOTS, int sms, int pps,
-                     int nseg, int search) {
-  const std::vector<long long>& hc = P.hc;
-  long long e_panel = std::max<long long>((n_ent + (long long)pps * sms - 1) / ((long long)pps * sms), 32768);
-  int slot_cap = SLOTS;
-  long long e_tail = 0, tail_from = 0;          // tapered tail (search): target of the late panels
-  if (search && NH > 0) {
-    const long long vmax0 = std::max<long long>(e_panel / (2 * HW), 64);
-    std::vector<long long>& cum_h = P.cum_h;
-    std::vector<int>& cum_nv = P.cum_nv;
-    cum_h.resize((size_t)NH + 1);
-    cum_nv.resize((size_t)NH + 1);
-    cum_h[0] = 0;
-    cum_nv[0] = 0;
-    for (int r = 0; r < NH; ++r) {
-      const long long h = hc[r];
-      cum_h[r + 1] = cum_h[r] + h;
-      cum_nv[r + 1] = cum_nv[r] + (int)std::min<long long>(h > 0 ? (h + vmax0 - 1) / vmax0 : 0, SLOTS);
+// list scheduling of panel costs in index order on sms CTAs (the claim order of k_heavy)
+long long claim_makespan(const std::vector<long long>& cost, int sms, std::vector<long long>& busy) {
+  busy.assign(sms, 0);
+  long long makespan = 0;
+  for (long long c : cost) {
+    const long long t = busy[0] + c;
+    makespan = std::max(makespan, t);
+    int i = 0;
+    for (;;) {
+      int k = 2 * i + 1;
+      if (k >= sms) break;
+      if (k + 1 < sms && busy[k + 1] < busy[k]) ++k;
+      if (busy[k] >= t) break;
+      busy[i] = busy[k];
+      i = k;
     }
-    const long long fixed = (long long)nseg * kPanelSegCost;
-    std::vector<long long> busy;
-    int base_panels = 0;
-    const long long base = heavy_makespan(cum_h, cum_nv, NH, e_panel, SLOTS, sms, fixed, busy, 0, 0, &base_panels);
-    long long best = base;
-    P.sel_num = 100;
-    P.sel_cap = SLOTS;
-    // nothing to gain where the default is already within 8 % of an even split of its work
-    // (C5: 6 %); the candidates run on the helper thread beside the edge-stream build
-    const bool worth = base * 100 > (n_ent + fixed * base_panels) / sms * 108;
-    static const int kCapEighths[] = {8, 6, 5, 4, 3};
-    for (int num = worth ? 150 : 0; num >= 50; num -= 5)       // entry target, % of the default
-      for (int d : kCapEighths) {                             // slot cap = SLOTS * d / 8
-        const long long e = std::max<long long>(e_panel * num / 100, 32768);
-        const int cap = SLOTS * d / 8;
-        const long long m = heavy_makespan(cum_h, cum_nv, NH, e, cap, sms, fixed, busy);
-        if (m < best && m * 100 <= base * 96) {
-          best = m;
-          P.sel_num = num;
-          P.sel_cap = cap;
-        }
-      }
-    // a tapered tail: the panels that start after tail_from entries take a smaller target (the
-    // last panels claimed decide how uneven the CTAs finish)
-    const long long e_sel = std::max<long long>(e_panel * P.sel_num / 100, 32768);
-    const int cap_sel = P.sel_cap;
-    P.sel_tail = 0;
-    P.sel_from = 0;
-    for (int from = worth ? 50 : 100; from <= 90; from += 10)   // % of the entries before the tail
-      for (int tnum = 70; tnum >= 20; tnum -= 10) {           // tail target, % of the chosen one
-        const long long et = std::max<long long>(e_sel * tnum / 100, 32768);
-        const long long tf = n_ent / 100 * from;
-        const long long m = heavy_makespan(cum_h, cum_nv, NH, e_sel, cap_sel, sms, fixed, busy, et, tf);
-        if (m < best && m * 100 <= base * 96) {
-          best = m;
-          P.sel_tail = tnum;
-          P.sel_from = from;
-        }
-      }
-    P.sim_base = base;
-    P.sim_best = best;
-    if (best < base) {
-      e_panel = e_sel;
-      slot_cap = cap_sel;
-      if (P.sel_tail > 0) {
-        e_tail = std::max<long long>(e_sel * P.sel_tail / 100, 32768);
-        tail_from = n_ent / 100 * P.sel_from;
-      }
-    }
+    busy[i] = t;
   }
+  return makespan;
+}
+
+// One pass of the plan: panels closed at slot_cap slots or e_panel entries (e_tail for the
+// panels that start after tail_from entries, if e_tail > 0).
+void plan_heavy_pass(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOTS, long long e_panel,
+                     int slot_cap, long long e_tail, long long tail_from) {
+  const std::vector<long long>& hc = P.hc;
   const long long vmax = std::max<long long>(e_panel / (2 * HW), 64);
   std::vector<int>& prow = P.prow;
   std::vector<int>& row_panel = P.row_panel;
@@ -1093,6 +1051,7 @@ void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOT
   prow.assign(1, 0);
   pslot_base.assign(1, 0);
   wslot.clear();
+  P.pent.clear();
   row_panel.resize(NH);
   rslot.resize(NH);
   slot_warp.clear();
@@ -1116,6 +1075,7 @@ void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOT
     wslot.insert(wslot.end(), ws.begin(), ws.end());
     prow.push_back(r_end);
     pslot_base.push_back(pslot_base.back() + nslots);
+    P.pent.push_back(p_ent);
     nslots = 0;
     p_ent = 0;
   };
@@ -1136,6 +1096,70 @@ void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOT
   }
   close_panel(NH);
   P.npanels = (int)prow.size() - 1;
+}
+
+void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOTS, int sms, int pps,
+                     int nseg, int search) {
+  const std::vector<long long>& hc = P.hc;
+  const long long e_panel = std::max<long long>((n_ent + (long long)pps * sms - 1) / ((long long)pps * sms), 32768);
+  plan_heavy_pass(P, NH, n_ent, HW, SLOTS, e_panel, SLOTS, 0, 0);      // the default shape
+  P.sel_num = 100;
+  P.sel_cap = SLOTS;
+  P.sel_tail = P.sel_from = 0;
+  P.sim_base = P.sim_best = 0;
+  if (!search || NH <= 0) return;
+  // its makespan under the claim order, from the panels just made; nothing to gain where that is
+  // within 8 % of an even split of the work (C5: 6 % -- no search, no second pass)
+  const long long fixed = (long long)nseg * kPanelSegCost;
+  std::vector<long long> busy, cost(P.pent);
+  for (long long& c : cost) c += fixed;
+  const long long base = claim_makespan(cost, sms, busy);
+  P.sim_base = P.sim_best = base;
+  if (base * 100 <= (n_ent + fixed * P.npanels) / sms * 108) return;
+  const long long vmax0 = std::max<long long>(e_panel / (2 * HW), 64);
+  std::vector<long long>& cum_h = P.cum_h;
+  std::vector<int>& cum_nv = P.cum_nv;
+  cum_h.resize((size_t)NH + 1);
+  cum_nv.resize((size_t)NH + 1);
+  cum_h[0] = 0;
+  cum_nv[0] = 0;
+  for (int r = 0; r < NH; ++r) {
+    const long long h = hc[r];
+    cum_h[r + 1] = cum_h[r] + h;
+    cum_nv[r + 1] = cum_nv[r] + (int)std::min<long long>(h > 0 ? (h + vmax0 - 1) / vmax0 : 0, SLOTS);
+  }
+  long long best = base;
+  static const int kCapEighths[] = {8, 6, 5, 4, 3};
+  for (int num = 150; num >= 50; num -= 5)                    // entry target, % of the default
+    for (int d : kCapEighths) {                               // slot cap = SLOTS * d / 8
+      const long long e = std::max<long long>(e_panel * num / 100, 32768);
+      const int cap = SLOTS * d / 8;
+      const long long m = heavy_makespan(cum_h, cum_nv, NH, e, cap, sms, fixed, busy);
+      if (m < best && m * 100 <= base * 96) {
+        best = m;
+        P.sel_num = num;
+        P.sel_cap = cap;
+      }
+    }
+  // a tapered tail: the panels that start after tail_from entries take a smaller target (the
+  // last panels claimed decide how uneven the CTAs finish)
+  const long long e_sel = std::max<long long>(e_panel * P.sel_num / 100, 32768);
+  for (int from = 50; from <= 90; from += 10)                 // % of the entries before the tail
+    for (int tnum = 70; tnum >= 20; tnum -= 10) {             // tail target, % of the chosen one
+      const long long et = std::max<long long>(e_sel * tnum / 100, 32768);
+      const long long m = heavy_makespan(cum_h, cum_nv, NH, e_sel, P.sel_cap, sms, fixed, busy, et,
+                                         n_ent / 100 * from);
+      if (m < best && m * 100 <= base * 96) {
+        best = m;
+        P.sel_tail = tnum;
+        P.sel_from = from;
+      }
+    }
+  P.sim_best = best;
+  if (best < base)
+    plan_heavy_pass(P, NH, n_ent, HW, SLOTS, e_sel, P.sel_cap,
+                    P.sel_tail > 0 ? std::max<long long>(e_sel * P.sel_tail / 100, 32768) : 0,
+                    n_ent / 100 * P.sel_from);
 }
 
 // Heavy-row plan (psi_heavy.cu), device part: the host plan P (already made) uploaded, then the
