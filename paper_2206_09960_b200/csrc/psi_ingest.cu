@@ -664,6 +664,7 @@ __global__ void __launch_bounds__(kBalBlock) k_heavy_balance(const unsigned* in,
       int r = q + 1;
       while (r < q1 && (src[r] >> sh) == sl) ++r;
       const int n = r - q;
+      PSI_ASSERT(n >= 1 && n <= kBalBlock && q1 - q0 <= kBalBlock);
       if (n <= 32) {
         unsigned w[32];
         for (int j = 0; j < n; ++j) w[j] = src[q + j];
@@ -706,6 +707,7 @@ __global__ void __launch_bounds__(kBalBlock) k_heavy_balance(const unsigned* in,
             const int v = ((int)((c >> (4 * b16)) & 15ull) << 8) - left;
             if (v < bv) { bv = v; bb = b16; }
           }
+          PSI_ASSERT(head[bb] < end[bb]);
           const unsigned e = w[head[bb]++];
           dst[q + i] = e;
           count(q + i, e);
