@@ -1117,7 +1117,9 @@ void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOT
   for (long long& c : cost) c += fixed;
   const long long base = claim_makespan(cost, sms, busy);
   P.sim_base = P.sim_best = base;
-  if (base * 100 <= (n_ent + fixed * P.npanels) / sms * 108) return;
+  // (PSI_HEAVY_SEARCH_GATE / PSI_HEAVY_SEARCH_GAIN: measurement knobs for the two thresholds, %)
+  const int gate = env_int("PSI_HEAVY_SEARCH_GATE", 8), gain = env_int("PSI_HEAVY_SEARCH_GAIN", 4);
+  if (base * 100 <= (n_ent + fixed * P.npanels) / sms * (100 + gate)) return;
   const long long vmax0 = std::max<long long>(e_panel / (2 * HW), 64);
   std::vector<long long>& cum_h = P.cum_h;
   std::vector<int>& cum_nv = P.cum_nv;
@@ -1137,7 +1139,7 @@ void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOT
       const long long e = std::max<long long>(e_panel * num / 100, 32768);
       const int cap = SLOTS * d / 8;
       const long long m = heavy_makespan(cum_h, cum_nv, NH, e, cap, sms, fixed, busy);
-      if (m < best && m * 100 <= base * 96) {
+      if (m < best && m * 100 <= base * (100 - gain)) {
         best = m;
         P.sel_num = num;
         P.sel_cap = cap;
@@ -1151,7 +1153,7 @@ void plan_heavy_host(HeavyHostPlan& P, int NH, long long n_ent, int HW, int SLOT
       const long long et = std::max<long long>(e_sel * tnum / 100, 32768);
       const long long m = heavy_makespan(cum_h, cum_nv, NH, e_sel, P.sel_cap, sms, fixed, busy, et,
                                          n_ent / 100 * from);
-      if (m < best && m * 100 <= base * 96) {
+      if (m < best && m * 100 <= base * (100 - gain)) {
         best = m;
         P.sel_tail = tnum;
         P.sel_from = from;
